@@ -1,0 +1,133 @@
+/*
+ * qflex_b200.h -- C ABI of the B200-native RQC contraction library
+ * (libqflex_b200.so, built from paper_1811_09599_b200/csrc/ for sm_100a).
+ *
+ * The reference (`rqcsim`, pure Python) exposes this hot path only as
+ * Python functions; every entry point below replaces one reference call
+ * site and is bound from Python with ctypes
+ * (paper_1811_09599_b200/_lib.py; binding recipe in INTEGRATION.md).
+ *
+ * Conventions
+ *   - All tensor pointers are DEVICE pointers owned by the caller
+ *     (torch buffers); the library never frees them.
+ *   - Row-major ("C order") storage everywhere, as in the reference
+ *     (SPEC.md:101).  complex64 = interleaved float32 (re, im);
+ *     complex128 = interleaved float64.
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     asynchronous on it.  NULL = legacy default stream.
+ *   - Every function returns an int status: QF_OK (0) or a negative
+ *     code; qf_last_error() returns the message of the last failure on
+ *     the calling host thread.  Python maps QF_ERR_INVALID -> ValueError,
+ *     QF_ERR_MEMORY -> MemoryBudgetError, others -> RuntimeError, the
+ *     same exception classes the reference raises.
+ *   - Thread safety: callable from one host thread per GPU concurrently;
+ *     internal caches are mutex-protected.
+ */
+#ifndef QFLEX_B200_H
+#define QFLEX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QF_OK 0
+#define QF_ERR_INVALID (-1)     /* bad shape / perm / argument   -> ValueError        */
+#define QF_ERR_CUDA (-2)        /* CUDA launch or runtime error  -> RuntimeError      */
+#define QF_ERR_MEMORY (-3)      /* workspace allocation failed   -> MemoryBudgetError */
+#define QF_ERR_UNSUPPORTED (-4) /* not built for this device     -> RuntimeError      */
+
+/* GEMM engine selection for qf_cgemm_* */
+#define QF_GEMM_AUTO 0   /* tcgen05 3xTF32 where the shape pays, else FFMA        */
+#define QF_GEMM_FFMA 1   /* K3: plain fp32 FFMA complex GEMM (baseline)           */
+#define QF_GEMM_TC3 2    /* K2: tcgen05 kind::tf32 3xTF32 complex GEMM (sm_100a)  */
+
+/* operand layouts */
+#define QF_OP_N 0        /* A stored [M][K] (lda >= K); B stored [K][N] (ldb >= N) */
+#define QF_OP_T 1        /* A stored [K][M] (lda >= M); B stored [N][K] (ldb >= K) */
+
+/* Last error message of this host thread ("" if none). */
+const char *qf_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int qf_version(void);
+
+/* Properties of device `dev`: SM count and compute capability. */
+int qf_device_info(int dev, int *sm_count, int *cc_major, int *cc_minor);
+
+/*
+ * K1 -- general tensor index permutation.
+ *   dst = ascontiguousarray(transpose(src, perm)), bit-exact.
+ * Replaces rq/tensor_core.py:290-330 (permute_fast, the L/R move kernels
+ * rq/_kernels.py:105-151) and rq/tensor_core.py:271-273 (permute_naive);
+ * same (dims, perm) meaning as plan_permutation rq/tensor_core.py:81.
+ * elem_bytes: 8 (complex64) or 16 (complex128).  src and dst must not
+ * alias.  rank <= 64; dims may contain 1s; rank 0 copies one element.
+ */
+int qf_permute(const void *src, void *dst, int rank, const int64_t *dims,
+               const int32_t *perm, int elem_bytes, void *stream);
+int qf_permute_c64(const void *src, void *dst, int rank, const int64_t *dims,
+                   const int32_t *perm, void *stream);
+
+/*
+ * K4 -- index slicing (Tensor.fix, rq/tensor_core.py:366-372, used by
+ * Net2D.fix_outputs rq/network_builder.py:134-149 and the executor's cut
+ * slicing rq/contraction_plan.py:450-466), batched over bit-strings.
+ * View src as [outer][dim][inner]; for b in [0, nidx):
+ *   dst[b][o][i] = src[o][idx[b]][i]
+ * idx is a DEVICE int32 array of nidx entries, each in [0, dim).
+ */
+int qf_gather_axis(const void *src, void *dst, int64_t outer, int64_t dim,
+                   int64_t inner, const int32_t *idx, int64_t nidx,
+                   int elem_bytes, void *stream);
+
+/* Single-value form of qf_gather_axis (host value, no index array). */
+int qf_fix_axis(const void *src, void *dst, int64_t outer, int64_t dim,
+                int64_t inner, int64_t value, int elem_bytes, void *stream);
+
+/*
+ * K2/K3 -- strided-batched complex GEMM, row-major:
+ *   C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b],  b in [0, batch)
+ * op(A) is M x K, op(B) is K x N, C[b] is M x N with leading dim ldc.
+ * Replaces the `(m x k) @ (k x n)` at rq/tensor_core.py:417 (numpy ->
+ * OpenBLAS cgemm).  mode: QF_GEMM_AUTO / _FFMA / _TC3.  K may be 0.
+ */
+int qf_cgemm_c64(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
+                 const void *A, int64_t lda, int64_t strideA, int opA,
+                 const void *B, int64_t ldb, int64_t strideB, int opB,
+                 void *C, int64_t ldc, int64_t strideC,
+                 float alpha_re, float alpha_im, float beta_re, float beta_im,
+                 void *stream);
+
+/* complex128 twin (FFMA/DFMA only), for dtype=complex128 engines. */
+int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
+                  const void *A, int64_t lda, int64_t strideA, int opA,
+                  const void *B, int64_t ldb, int64_t strideB, int opB,
+                  void *C, int64_t ldc, int64_t strideC,
+                  double alpha_re, double alpha_im, double beta_re, double beta_im,
+                  void *stream);
+
+/*
+ * K5 -- path-sum accumulation (rq/amplitude_engine.py:123,153-157):
+ *   y[i] += x[i] for i in [0, n) complex elements.
+ */
+int qf_accumulate(const void *x, void *y, int64_t n, int elem_bytes, void *stream);
+
+/*
+ * Stream-ordered workspace the GEMM split-K path uses (the only memory
+ * the library owns).  Reserve up front to keep allocation out of timed
+ * regions; released by qf_workspace_release.
+ */
+int qf_workspace_reserve(int64_t bytes, void *stream);
+int qf_workspace_release(void);
+
+/* Number of kernels this library launched on the calling thread since the
+ * last reset (for the bench's gpu_launches claim). */
+int64_t qf_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QFLEX_B200_H */

@@ -1,0 +1,132 @@
+"""ctypes binding of libqflex_b200.so (the C ABI in include/qflex_b200.h).
+
+PyTorch is used only for device buffers and the current CUDA stream; every
+numeric operation on the amplitude path goes through this library.  There
+is no CPU fallback: importing works without a GPU (so host-side tooling and
+the CPU test-suite run anywhere), but any call that needs the library
+raises if the shared object is missing or no CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libqflex_b200.so")
+
+QF_OK = 0
+QF_ERR_INVALID = -1
+QF_ERR_CUDA = -2
+QF_ERR_MEMORY = -3
+QF_ERR_UNSUPPORTED = -4
+
+GEMM_AUTO, GEMM_FFMA, GEMM_TC3 = 0, 1, 2
+OP_N, OP_T = 0, 1
+
+# every exported symbol declared in include/qflex_b200.h
+EXPORTS = (
+    "qf_last_error", "qf_version", "qf_device_info", "qf_permute", "qf_permute_c64",
+    "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_zgemm_c128", "qf_accumulate",
+    "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
+)
+
+
+class LibraryMissingError(RuntimeError):
+    """The CUDA library is not built (or not loadable) on this machine."""
+
+
+class MemoryBudgetError(RuntimeError):
+    """Executing (or estimating) a plan would exceed the memory budget
+    (mirrors rqcsim.contraction_plan.MemoryBudgetError, rq/contraction_plan.py:56)."""
+
+
+_lib = None
+_lock = threading.Lock()
+
+_c_void_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+def _declare(lib):
+    lib.qf_last_error.restype = ctypes.c_char_p
+    lib.qf_last_error.argtypes = []
+    lib.qf_version.restype = ctypes.c_int
+    lib.qf_device_info.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                   ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+    lib.qf_permute.argtypes = [_c_void_p, _c_void_p, ctypes.c_int, ctypes.POINTER(_i64),
+                               ctypes.POINTER(_i32), ctypes.c_int, _c_void_p]
+    lib.qf_permute_c64.argtypes = [_c_void_p, _c_void_p, ctypes.c_int, ctypes.POINTER(_i64),
+                                   ctypes.POINTER(_i32), _c_void_p]
+    lib.qf_gather_axis.argtypes = [_c_void_p, _c_void_p, _i64, _i64, _i64, _c_void_p, _i64,
+                                   ctypes.c_int, _c_void_p]
+    lib.qf_fix_axis.argtypes = [_c_void_p, _c_void_p, _i64, _i64, _i64, _i64, ctypes.c_int,
+                                _c_void_p]
+    lib.qf_cgemm_c64.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64,
+                                 _c_void_p, _i64, _i64, ctypes.c_int,
+                                 _c_void_p, _i64, _i64, ctypes.c_int,
+                                 _c_void_p, _i64, _i64,
+                                 ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                 _c_void_p]
+    lib.qf_zgemm_c128.argtypes = [_i64, _i64, _i64, _i64,
+                                  _c_void_p, _i64, _i64, ctypes.c_int,
+                                  _c_void_p, _i64, _i64, ctypes.c_int,
+                                  _c_void_p, _i64, _i64,
+                                  ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                  ctypes.c_double, _c_void_p]
+    lib.qf_accumulate.argtypes = [_c_void_p, _c_void_p, _i64, ctypes.c_int, _c_void_p]
+    lib.qf_workspace_reserve.argtypes = [_i64, _c_void_p]
+    lib.qf_workspace_release.argtypes = []
+    lib.qf_launch_count.argtypes = [ctypes.c_int]
+    lib.qf_launch_count.restype = _i64
+    for name in EXPORTS:
+        if name not in ("qf_last_error", "qf_launch_count"):
+            getattr(lib, name).restype = ctypes.c_int
+    return lib
+
+
+def load(path: Optional[str] = None):
+    """Load (once) and return the ctypes handle; raises LibraryMissingError."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = path or LIB_PATH
+        if not os.path.exists(p):
+            raise LibraryMissingError(
+                f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        try:
+            lib = _declare(ctypes.CDLL(p))
+        except OSError as exc:  # pragma: no cover - depends on the box
+            raise LibraryMissingError(f"cannot load {p}: {exc}") from None
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(status: int, what: str = "qflex"):
+    if status == QF_OK:
+        return
+    msg = load().qf_last_error().decode(errors="replace")
+    if status == QF_ERR_INVALID:
+        raise ValueError(f"{what}: {msg}")
+    if status == QF_ERR_MEMORY:
+        raise MemoryBudgetError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed ({status}): {msg}")
+
+
+def dims_array(dims: Sequence[int]):
+    return (_i64 * max(1, len(dims)))(*[int(d) for d in dims])
+
+
+def perm_array(perm: Sequence[int]):
+    return (_i32 * max(1, len(perm)))(*[int(p) for p in perm])
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(load().qf_launch_count(1 if reset else 0))

@@ -1,0 +1,286 @@
+"""Amplitudes and batches of amplitudes on the B200 (the drop-in surface).
+
+Mirrors `rqcsim.amplitude_engine` (rq/amplitude_engine.py): the engine
+owns the all-outputs-open device network per input state and the plan,
+slices outputs per query and sums the plan's paths.  Additions, all
+device-side:
+
+  * `amplitudes(in_bits, out_bits_list)` -- many bit-strings through ONE
+    plan walk: their output slices form a leading '@b' axis on every site
+    tensor, so each pairwise contraction is one batched GEMM.
+  * `amplitude_batches(...)` -- the same for the open-qubit batch mode
+    (many s_AB at once).
+  * multi-GPU: with torch.distributed initialised (one process per GPU),
+    each rank sums a contiguous chunk of the path list and one NCCL
+    all-reduce combines the partial amplitudes (`slices.py`).
+
+Results return to the host once per call (complex / numpy arrays), exactly
+the types the reference returns.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import IO, Iterable, Optional, Sequence, Union
+
+import numpy as np
+
+from . import slices
+from .circuits import Circuit
+from .contraction_plan import ContractionPlan, PlanExecutor, builtin_plan, enumerate_paths
+from .network_builder import Net2D, build_3d, contract_time, out_label
+from .tensor_core import accumulate_buffer, device_buffer, torch
+
+
+@dataclass(frozen=True)
+class FidelitySpec:
+    """Fraction f of paths to keep (seeded uniform draw when f < 1)."""
+
+    f: float = 1.0
+    seed: int = 0
+
+    def __post_init__(self):
+        if not 0.0 < self.f <= 1.0:
+            raise ValueError(f"fidelity fraction must be in (0, 1], got {self.f}")
+
+    def paths_for(self, cut_dims: Sequence[int]) -> list:
+        return enumerate_paths(cut_dims, f=self.f, seed=self.seed)
+
+
+@dataclass(frozen=True)
+class PathStats:
+    paths_total: int
+    paths_used: int
+    flops: int
+    peak_bytes: int
+
+
+@dataclass(frozen=True)
+class AmplitudeBatch:
+    """Amplitudes for one fixed s_AB and many completions of the open region."""
+
+    in_bits: str
+    s_ab: str
+    c_sites: tuple
+    c_values: tuple
+    amplitudes: np.ndarray
+    fidelity: FidelitySpec
+    stats: PathStats
+
+    def __len__(self) -> int:
+        return len(self.c_values)
+
+    def out_bits(self, i: int) -> str:
+        bits = list(self.s_ab)
+        for q, b in zip(self.c_sites, format(self.c_values[i], f"0{len(self.c_sites)}b")):
+            bits[q] = b
+        return "".join(bits)
+
+
+def _bits_str(value, n: int) -> str:
+    if isinstance(value, str):
+        if len(value) != n or set(value) - {"0", "1"}:
+            raise ValueError(f"need {n} bits, got {value!r}")
+        return value
+    if not 0 <= value < 2 ** n:
+        raise ValueError(f"bit value {value} out of range for {n} qubits")
+    return format(int(value), f"0{n}b")
+
+
+def _completions(n_open: int, n_c: int, seed: int) -> np.ndarray:
+    """The n_c completions of the open region (rq/amplitude_engine.py:159-164)."""
+    if n_c == 2 ** n_open:
+        return np.arange(n_c)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return np.sort(rng.choice(2 ** n_open, size=n_c, replace=False))
+
+
+class AmplitudeEngine:
+    """Computes amplitudes of one circuit via its contraction plan, on the
+    current CUDA device (or `device`)."""
+
+    def __init__(self, circuit: Circuit, plan: Optional[ContractionPlan] = None, *,
+                 dtype=np.complex64, thread_count: int = 1, memory_budget: Optional[int] = None,
+                 device=None, group=None):
+        self.circuit = circuit
+        self.plan = plan if plan is not None else builtin_plan(circuit.lattice)
+        self.dtype = np.dtype(dtype)
+        if self.dtype not in (np.dtype(np.complex64), np.dtype(np.complex128)):
+            raise ValueError(f"dtype must be complex64 or complex128, got {self.dtype}")
+        self.thread_count = thread_count
+        self.memory_budget = memory_budget
+        self.device = device
+        self.group = group
+        self._nets: dict = {}
+
+    # -- network -----------------------------------------------------------
+
+    def _torch_device(self):
+        if self.device is not None:
+            return torch.device("cuda", self.device) if isinstance(self.device, int) else self.device
+        return torch.device("cuda", torch.cuda.current_device())
+
+    def base_net(self, in_bits: Union[str, int] = 0) -> Net2D:
+        key = _bits_str(in_bits, self.circuit.n)
+        net = self._nets.get(key)
+        if net is None:
+            with torch.cuda.device(self._torch_device()):
+                net = contract_time(build_3d(self.circuit, in_bits=key, out_bits=None,
+                                             dtype=self.dtype))
+            self._nets[key] = net
+        return net
+
+    def _executor(self, net: Net2D) -> PlanExecutor:
+        return PlanExecutor(net, self.plan, thread_count=self.thread_count,
+                            memory_budget=self.memory_budget)
+
+    # -- path sums ----------------------------------------------------------
+
+    def _sum_paths(self, ex: PlanExecutor, paths, finish, size: int):
+        """Sum finish(ex.run(p)) (a flat device buffer of `size` entries)
+        over this rank's share of `paths`; all-reduce across ranks."""
+        shard = slices.current_shard(self.group)
+        mine = shard.take(paths)
+        acc = device_buffer(size, torch.complex64 if self.dtype == np.complex64
+                            else torch.complex128)
+        acc.zero_()
+        for p in mine:
+            accumulate_buffer(finish(ex.run(p)), acc, size)
+        slices.reduce_partials(acc, self.group)
+        flops = slices.reduce_int(ex.flops, self.group, acc.device)
+        return acc[:size], flops
+
+    def amplitude(self, in_bits: Union[str, int], out_bits: Union[str, int],
+                  fidelity: FidelitySpec = FidelitySpec()) -> tuple:
+        """One amplitude <out|U|in>, summed over the selected paths."""
+        out = _bits_str(out_bits, self.circuit.n)
+        with torch.cuda.device(self._torch_device()):
+            net = self.base_net(in_bits).fix_outputs({q: int(b) for q, b in enumerate(out)})
+            ex = self._executor(net)
+            paths = fidelity.paths_for(ex.cut_dims)
+            acc, flops = self._sum_paths(ex, paths, lambda t: t.data, 1)
+            total = complex(acc.cpu().numpy()[0])
+        return total, PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
+
+    def amplitudes(self, in_bits: Union[str, int], out_bits: Sequence,
+                   fidelity: FidelitySpec = FidelitySpec(), *,
+                   chunk: Optional[int] = None) -> tuple:
+        """Many amplitudes at once; returns (ndarray, PathStats per amplitude).
+
+        Bit-strings ride as the '@b' GEMM batch axis through one plan walk
+        per chunk (default: all of them)."""
+        n = self.circuit.n
+        outs = [_bits_str(o, n) for o in out_bits]
+        bits = np.array([[int(c) for c in o] for o in outs], dtype=np.int32).reshape(len(outs), n)
+        chunk = chunk or max(1, len(outs))
+        result = np.empty(len(outs), dtype=self.dtype)
+        stats = None
+        with torch.cuda.device(self._torch_device()):
+            base = self.base_net(in_bits)
+            for lo in range(0, len(outs), chunk):
+                part = bits[lo:lo + chunk]
+                net = base.fix_outputs_batch(part, tuple(range(n)))
+                ex = self._executor(net)
+                paths = fidelity.paths_for(ex.cut_dims)
+                acc, flops = self._sum_paths(ex, paths, lambda t: t.data, len(part))
+                result[lo:lo + len(part)] = acc.cpu().numpy()
+                stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
+        return result, stats
+
+    def amplitude_batch(self, in_bits: Union[str, int], s_ab: Union[str, int],
+                        c_sites: Sequence[int], n_c: int, *, seed: int = 0,
+                        fidelity: FidelitySpec = FidelitySpec()) -> AmplitudeBatch:
+        """n_c completions of the open region `c_sites` sharing the fixed
+        bits s_ab (rq/amplitude_engine.py:128-170)."""
+        return self.amplitude_batches(in_bits, [s_ab], c_sites, n_c, seeds=[seed],
+                                      fidelity=fidelity)[0]
+
+    def amplitude_batches(self, in_bits: Union[str, int], s_ab_list: Sequence,
+                          c_sites: Sequence[int], n_c: int, *, seeds: Sequence[int],
+                          fidelity: FidelitySpec = FidelitySpec()) -> list:
+        """Several open-qubit batches (one per s_AB) in one plan walk."""
+        n = self.circuit.n
+        c_sites = tuple(sorted(c_sites))
+        if not c_sites:
+            raise ValueError("batch region is empty")
+        if len(set(c_sites)) != len(c_sites):
+            raise ValueError("duplicate sites in batch region")
+        if not 1 <= n_c <= 2 ** len(c_sites):
+            raise ValueError(f"n_c={n_c} not in [1, 2^{len(c_sites)}]")
+        if len(seeds) != len(s_ab_list):
+            raise ValueError("one seed per s_AB is required")
+        sabs = [_bits_str(s, n) for s in s_ab_list]
+        fixed = tuple(q for q in range(n) if q not in set(c_sites))
+        nb = len(sabs)
+        width = 2 ** len(c_sites)
+        order = ("@b",) + tuple(out_label(q) for q in c_sites)
+        with torch.cuda.device(self._torch_device()):
+            base = self.base_net(in_bits)
+            bits = np.array([[int(s[q]) for q in fixed] for s in sabs], dtype=np.int32)
+            bits = bits.reshape(nb, len(fixed))
+            net = base.fix_outputs_batch(bits, fixed)
+            ex = self._executor(net)
+            paths = fidelity.paths_for(ex.cut_dims)
+            acc, flops = self._sum_paths(ex, paths, lambda t: t.transpose_to(order).data,
+                                         nb * width)
+            table = acc.cpu().numpy().reshape(nb, width)
+        stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
+        out = []
+        ins = _bits_str(in_bits, n)
+        for i, s in enumerate(sabs):
+            vals = _completions(len(c_sites), n_c, seeds[i])
+            out.append(AmplitudeBatch(ins, s, c_sites, tuple(int(v) for v in vals),
+                                      table[i][vals], fidelity, stats))
+        return out
+
+    def state(self, in_bits: Union[str, int] = 0,
+              fidelity: FidelitySpec = FidelitySpec()) -> np.ndarray:
+        """Full output state (qubit 0 = leading bit); desk-scale diagnostic."""
+        order = tuple(out_label(q) for q in range(self.circuit.n))
+        with torch.cuda.device(self._torch_device()):
+            net = self.base_net(in_bits)
+            ex = self._executor(net)
+            paths = fidelity.paths_for(ex.cut_dims)
+            acc, _ = self._sum_paths(ex, paths, lambda t: t.transpose_to(order).data,
+                                     2 ** self.circuit.n)
+            return acc.cpu().numpy()
+
+
+def mixed_state_samples(circuit: Circuit, f: float, count: int, seed: int = 0) -> np.ndarray:
+    """Bit-strings from a fidelity-f mixture of the exact output distribution
+    (computed on the device) and the uniform distribution
+    (rq/amplitude_engine.py:199-218)."""
+    if not 0.0 <= f <= 1.0:
+        raise ValueError(f"fidelity must be in [0, 1], got {f}")
+    eng = AmplitudeEngine(circuit, dtype=np.complex128)
+    probs = np.abs(eng.state(0)) ** 2
+    probs = probs / probs.sum()
+    rng = np.random.Generator(np.random.PCG64(seed))
+    exact = rng.choice(probs.size, size=count, p=probs)
+    uniform = rng.integers(0, probs.size, size=count)
+    return np.where(rng.random(count) < f, exact, uniform)
+
+
+def amplitude_record(in_bits: str, out_bits: str, amplitude: complex, fidelity: FidelitySpec,
+                     stats: PathStats) -> dict:
+    a = complex(amplitude)
+    return {"in": in_bits, "out": out_bits, "re": a.real, "im": a.imag, "f_target": fidelity.f,
+            "f_achieved_estimate": (2 ** len(in_bits)) * abs(a) ** 2,
+            "paths": stats.paths_used, "seed": fidelity.seed}
+
+
+def batch_records(batch: AmplitudeBatch) -> Iterable[dict]:
+    for i in range(len(batch)):
+        yield amplitude_record(batch.in_bits, batch.out_bits(i), batch.amplitudes[i],
+                               batch.fidelity, batch.stats)
+
+
+def write_amplitudes(fh: IO[str], records: Iterable[dict]):
+    for rec in records:
+        fh.write(json.dumps(rec) + "\n")
+
+
+def read_amplitudes(fh: IO[str]) -> list:
+    return [json.loads(line) for line in fh if line.strip()]

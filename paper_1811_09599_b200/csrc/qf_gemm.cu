@@ -1,0 +1,396 @@
+// K3 -- complex GEMM on the fp32 (or fp64) SIMT pipes, and the dispatcher
+// behind qf_cgemm_c64 / qf_zgemm_c128.
+//
+// Replaces `arr_a.reshape(m, k) @ arr_b.reshape(k, n)` at
+// rq/tensor_core.py:417 (numpy -> OpenBLAS cgemm).  Strided-batched,
+// row-major, both operands in N or T layout so callers can skip operand
+// permutations whenever the shared labels are already a prefix/suffix.
+//
+// Two kernels:
+//   * tiled   : 64x64 complex tile, 4x4 complex outputs per thread,
+//               register-prefetched double buffer through smem.
+//   * skinny  : M*N <= 256 outputs (dot products, GEMVs against a few
+//               columns -- the `result` steps of every plan): K split over
+//               CTAs, deterministic two-pass reduction through a
+//               stream-ordered workspace.  HBM-bound by design.
+// K2 (tcgen05 3xTF32) lives in qf_gemm_tc.cu; QF_GEMM_AUTO routes there
+// when the shape fills tensor-core tiles.
+#include <algorithm>
+
+#include "qf_common.cuh"
+
+namespace qf {
+
+template <typename R>
+struct C2;
+template <>
+struct C2<float> {
+  using T = float2;
+};
+template <>
+struct C2<double> {
+  using T = double2;
+};
+
+template <typename V>
+__device__ __forceinline__ void cfma(V &acc, const V &a, const V &b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+
+struct GemmArgs {
+  int64_t batch, M, N, K;
+  const void *A;
+  int64_t lda, sA;
+  int opA;
+  const void *B;
+  int64_t ldb, sB;
+  int opB;
+  void *C;
+  int64_t ldc, sC;
+  double ar, ai, br, bi;
+};
+
+// ---------------------------------------------------------------------------
+// tiled SIMT kernel
+
+constexpr int TBM = 64, TBN = 64, TTHREADS = 256;
+template <typename R>
+struct TileK {
+  static constexpr int v = 16;
+};
+template <>
+struct TileK<double> {
+  static constexpr int v = 8;
+};
+
+template <typename R>
+__global__ void __launch_bounds__(TTHREADS, 2)
+    cgemm_tiled_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
+  using V = typename C2<R>::T;
+  constexpr int TBK = TileK<R>::v;
+  constexpr int NLD = TBM * TBK / TTHREADS;
+  __shared__ V As[2][TBK][TBM + 1];
+  __shared__ V Bs[2][TBK][TBN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const V *Ab = (const V *)g.A;
+  const V *Bb = (const V *)g.B;
+  V *Cb = (V *)g.C;
+  const V zero = {R(0), R(0)};
+  const R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
+  const bool use_beta = (br != R(0) || bi != R(0));
+
+  for (int64_t work = blockIdx.x; work < tiles * g.batch; work += gridDim.x) {
+    int64_t b = work / tiles;
+    int64_t tile = work - b * tiles;
+    int64_t m0 = (tile / tiles_n) * TBM, n0 = (tile % tiles_n) * TBN;
+    const V *A = Ab + b * g.sA;
+    const V *B = Bb + b * g.sB;
+    V *C = Cb + b * g.sC;
+
+    V acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = zero;
+
+    V ra[NLD], rb[NLD];
+    auto load = [&](int64_t k0) {
+#pragma unroll
+      for (int r = 0; r < NLD; ++r) {
+        int l = tid + TTHREADS * r;
+        int m, k;
+        if (g.opA == QF_OP_N) {
+          k = l % TBK;
+          m = l / TBK;
+        } else {
+          m = l % TBM;
+          k = l / TBM;
+        }
+        int64_t gm = m0 + m, gk = k0 + k;
+        V v = zero;
+        if (gm < g.M && gk < g.K) v = (g.opA == QF_OP_N) ? A[gm * g.lda + gk] : A[gk * g.lda + gm];
+        ra[r] = v;
+        int n;
+        if (g.opB == QF_OP_N) {
+          n = l % TBN;
+          k = l / TBN;
+        } else {
+          k = l % TBK;
+          n = l / TBK;
+        }
+        int64_t gn = n0 + n;
+        gk = k0 + k;
+        V w = zero;
+        if (gn < g.N && gk < g.K) w = (g.opB == QF_OP_N) ? B[gk * g.ldb + gn] : B[gn * g.ldb + gk];
+        rb[r] = w;
+      }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+      for (int r = 0; r < NLD; ++r) {
+        int l = tid + TTHREADS * r;
+        int m, k, n, kb;
+        if (g.opA == QF_OP_N) {
+          k = l % TBK;
+          m = l / TBK;
+        } else {
+          m = l % TBM;
+          k = l / TBM;
+        }
+        As[buf][k][m] = ra[r];
+        if (g.opB == QF_OP_N) {
+          n = l % TBN;
+          kb = l / TBN;
+        } else {
+          kb = l % TBK;
+          n = l / TBK;
+        }
+        Bs[buf][kb][n] = rb[r];
+      }
+    };
+
+    int64_t nk = (g.K + TBK - 1) / TBK;
+    __syncthreads();  // previous work item finished reading smem
+    if (nk > 0) {
+      load(0);
+      store(0);
+    }
+    __syncthreads();
+    for (int64_t kt = 0; kt < nk; ++kt) {
+      int buf = kt & 1;
+      if (kt + 1 < nk) load((kt + 1) * TBK);
+#pragma unroll
+      for (int k = 0; k < TBK; ++k) {
+        V a[4], bb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[buf][k][ty + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][k][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) cfma(acc[i][j], a[i], bb[j]);
+      }
+      if (kt + 1 < nk) store(buf ^ 1);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int64_t gm = m0 + ty + 16 * i;
+      if (gm >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int64_t gn = n0 + tx + 16 * j;
+        if (gn >= g.N) continue;
+        V v = acc[i][j];
+        V o;
+        o.x = ar * v.x - ai * v.y;
+        o.y = ar * v.y + ai * v.x;
+        if (use_beta) {
+          V c = C[gm * g.ldc + gn];
+          o.x += br * c.x - bi * c.y;
+          o.y += br * c.y + bi * c.x;
+        }
+        C[gm * g.ldc + gn] = o;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// skinny split-K kernel: M*N <= 256 outputs
+
+constexpr int STHREADS = 256;
+
+template <typename R>
+__global__ void __launch_bounds__(STHREADS)
+    cgemm_skinny_kernel(const __grid_constant__ GemmArgs g, int P, int Ppad, int64_t kchunk,
+                        int nsplit, void *ws) {
+  using V = typename C2<R>::T;
+  __shared__ V red[STHREADS];
+  const int tid = threadIdx.x;
+  const int KL = STHREADS / Ppad;
+  const int p = tid % Ppad, kl = tid / Ppad;
+  const int64_t split = blockIdx.x;
+  const int64_t b = blockIdx.y;
+  const V *A = (const V *)g.A + b * g.sA;
+  const V *B = (const V *)g.B + b * g.sB;
+  V acc = {R(0), R(0)};
+  if (p < P) {
+    int64_t m = p / g.N, n = p % g.N;
+    int64_t k0 = split * kchunk, k1 = min(g.K, k0 + kchunk);
+    const V *ap = (g.opA == QF_OP_N) ? A + m * g.lda : A + m;
+    int64_t as = (g.opA == QF_OP_N) ? 1 : g.lda;
+    const V *bp = (g.opB == QF_OP_N) ? B + n : B + n * g.ldb;
+    int64_t bs = (g.opB == QF_OP_N) ? g.ldb : 1;
+    int64_t k = k0 + kl;
+    // 4-way unrolled for memory-level parallelism
+    V acc2 = {R(0), R(0)};
+    for (; k + 3 * KL < k1; k += 4 * KL) {
+      V a0 = ap[k * as], a1 = ap[(k + KL) * as], a2 = ap[(k + 2 * KL) * as],
+        a3 = ap[(k + 3 * KL) * as];
+      V b0 = bp[k * bs], b1 = bp[(k + KL) * bs], b2 = bp[(k + 2 * KL) * bs],
+        b3 = bp[(k + 3 * KL) * bs];
+      cfma(acc, a0, b0);
+      cfma(acc2, a1, b1);
+      cfma(acc, a2, b2);
+      cfma(acc2, a3, b3);
+    }
+    for (; k < k1; k += KL) cfma(acc, ap[k * as], bp[k * bs]);
+    acc.x += acc2.x;
+    acc.y += acc2.y;
+  }
+  red[tid] = acc;
+  __syncthreads();
+  for (int s = KL / 2; s >= 1; s >>= 1) {
+    if (kl < s) {
+      V o = red[tid + s * Ppad];
+      red[tid].x += o.x;
+      red[tid].y += o.y;
+    }
+    __syncthreads();
+  }
+  if (kl == 0 && p < P) ((V *)ws)[(b * nsplit + split) * P + p] = red[tid];
+}
+
+template <typename R>
+__global__ void cgemm_skinny_reduce(const __grid_constant__ GemmArgs g, int P, int nsplit,
+                                    const void *ws) {
+  using V = typename C2<R>::T;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= g.batch * P) return;
+  int64_t b = t / P;
+  int p = (int)(t - b * P);
+  const V *w = (const V *)ws + b * nsplit * P + p;
+  R sx = 0, sy = 0;
+  for (int s = 0; s < nsplit; ++s) {
+    V v = w[(int64_t)s * P];
+    sx += v.x;
+    sy += v.y;
+  }
+  int64_t m = p / g.N, n = p % g.N;
+  V *C = (V *)g.C + b * g.sC + m * g.ldc + n;
+  R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
+  V o;
+  o.x = ar * sx - ai * sy;
+  o.y = ar * sy + ai * sx;
+  if (br != R(0) || bi != R(0)) {
+    V c = *C;
+    o.x += br * c.x - bi * c.y;
+    o.y += br * c.y + bi * c.x;
+  }
+  *C = o;
+}
+
+template <typename R>
+__global__ void cgemm_scale_kernel(const __grid_constant__ GemmArgs g) {
+  // K == 0: C = beta * C
+  using V = typename C2<R>::T;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t per = g.M * g.N;
+  if (t >= g.batch * per) return;
+  int64_t b = t / per, r = t - b * per, m = r / g.N, n = r - m * g.N;
+  V *C = (V *)g.C + b * g.sC + m * g.ldc + n;
+  R br = (R)g.br, bi = (R)g.bi;
+  V o = {R(0), R(0)};
+  if (br != R(0) || bi != R(0)) {
+    V c = *C;
+    o.x = br * c.x - bi * c.y;
+    o.y = br * c.y + bi * c.x;
+  }
+  *C = o;
+}
+
+// ---------------------------------------------------------------------------
+// dispatch
+
+int validate(const GemmArgs &g) {
+  QF_REQUIRE(g.batch >= 0 && g.M >= 0 && g.N >= 0 && g.K >= 0, "gemm: negative extent");
+  QF_REQUIRE(g.opA == QF_OP_N || g.opA == QF_OP_T, "gemm: opA must be N or T");
+  QF_REQUIRE(g.opB == QF_OP_N || g.opB == QF_OP_T, "gemm: opB must be N or T");
+  QF_REQUIRE(g.ldc >= std::max<int64_t>(1, g.N), "gemm: ldc < N");
+  QF_REQUIRE(g.lda >= std::max<int64_t>(1, g.opA == QF_OP_N ? g.K : g.M), "gemm: lda too small");
+  QF_REQUIRE(g.ldb >= std::max<int64_t>(1, g.opB == QF_OP_N ? g.N : g.K), "gemm: ldb too small");
+  return QF_OK;
+}
+
+template <typename R>
+int gemm_simt(const GemmArgs &g, cudaStream_t s) {
+  if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
+  if (g.K == 0) {
+    int64_t total = g.batch * g.M * g.N;
+    cgemm_scale_kernel<R><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(g);
+    return check_launch("cgemm_scale");
+  }
+  int64_t P = g.M * g.N;
+  if (P <= 256 && g.K >= 256) {
+    int Ppad = 1;
+    while (Ppad < P) Ppad <<= 1;
+    int KL = STHREADS / Ppad;
+    int64_t target_ctas = (int64_t)sm_count() * 8;
+    int64_t nsplit = std::max<int64_t>(1, target_ctas / std::max<int64_t>(1, g.batch));
+    int64_t min_chunk = (int64_t)KL * 64;
+    nsplit = std::min<int64_t>(nsplit, (g.K + min_chunk - 1) / min_chunk);
+    nsplit = std::max<int64_t>(1, std::min<int64_t>(nsplit, 4096));
+    int64_t kchunk = (g.K + nsplit - 1) / nsplit;
+    nsplit = (g.K + kchunk - 1) / kchunk;
+    QF_REQUIRE(g.batch <= 65535, "gemm: skinny batch %lld exceeds 65535", (long long)g.batch);
+    int st = QF_OK;
+    void *ws = workspace(g.batch * nsplit * P * (int64_t)sizeof(typename C2<R>::T), s, &st);
+    if (st != QF_OK) return st;
+    dim3 grid((unsigned)nsplit, (unsigned)g.batch);
+    cgemm_skinny_kernel<R><<<grid, STHREADS, 0, s>>>(g, (int)P, Ppad, kchunk, (int)nsplit, ws);
+    int rc = check_launch("cgemm_skinny");
+    if (rc != QF_OK) return rc;
+    int64_t total = g.batch * P;
+    cgemm_skinny_reduce<R><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(g, (int)P, (int)nsplit,
+                                                                           ws);
+    return check_launch("cgemm_skinny_reduce");
+  }
+  int64_t tiles_n = (g.N + TBN - 1) / TBN, tiles_m = (g.M + TBM - 1) / TBM;
+  int64_t tiles = tiles_n * tiles_m;
+  int64_t work = tiles * g.batch;
+  int64_t grid = std::min<int64_t>(work, (int64_t)sm_count() * 4);
+  cgemm_tiled_kernel<R><<<(unsigned)grid, TTHREADS, 0, s>>>(g, tiles_n, tiles);
+  return check_launch("cgemm_tiled");
+}
+
+// from qf_gemm_tc.cu
+int gemm_tc3(const GemmArgs &g, cudaStream_t s);
+bool tc3_eligible(const GemmArgs &g);
+
+}  // namespace qf
+
+extern "C" {
+
+int qf_cgemm_c64(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                 int64_t lda, int64_t strideA, int opA, const void *B, int64_t ldb, int64_t strideB,
+                 int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re, float alpha_im,
+                 float beta_re, float beta_im, void *stream) {
+  qf::GemmArgs g{batch, M, N, K, A, lda, strideA, opA, B, ldb, strideB, opB, C, ldc, strideC,
+                 alpha_re, alpha_im, beta_re, beta_im};
+  int st = qf::validate(g);
+  if (st != QF_OK) return st;
+  cudaStream_t s = qf::as_stream(stream);
+  if (mode == QF_GEMM_TC3) return qf::gemm_tc3(g, s);
+  if (mode == QF_GEMM_AUTO && qf::tc3_eligible(g)) return qf::gemm_tc3(g, s);
+  QF_REQUIRE(mode == QF_GEMM_AUTO || mode == QF_GEMM_FFMA, "gemm: unknown mode %d", mode);
+  return qf::gemm_simt<float>(g, s);
+}
+
+int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K, const void *A, int64_t lda,
+                  int64_t strideA, int opA, const void *B, int64_t ldb, int64_t strideB, int opB,
+                  void *C, int64_t ldc, int64_t strideC, double alpha_re, double alpha_im,
+                  double beta_re, double beta_im, void *stream) {
+  qf::GemmArgs g{batch, M, N, K, A, lda, strideA, opA, B, ldb, strideB, opB, C, ldc, strideC,
+                 alpha_re, alpha_im, beta_re, beta_im};
+  int st = qf::validate(g);
+  if (st != QF_OK) return st;
+  return qf::gemm_simt<double>(g, qf::as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,405 @@
+"""Device tensors, index permutation and pairwise contraction on the B200.
+
+Drop-in for the hot-path layer of `rqcsim.tensor_core` (rq/tensor_core.py):
+
+  Tensor(labels, array)            rq/tensor_core.py:338-388  (device-resident here)
+  contract(a, b)                   rq/tensor_core.py:391-419
+  plan_permutation / permute_fast  rq/tensor_core.py:81-151, 290-330
+  permute_naive                    rq/tensor_core.py:271-273
+
+Every numeric operation is a call into libqflex_b200.so (K1 permutation,
+K2/K3 complex GEMM, K4 slicing).  PyTorch only owns the device buffers.
+
+B200 design points
+  * A contraction is `[batch] x (M x K) @ (K x N)` on the GEMM engine;
+    operands are NOT permuted when the summed labels already form a
+    contiguous prefix or suffix (the GEMM reads either layout, N or T), and
+    the order of the summed index follows the larger operand so that the
+    big intermediate is almost never touched by K1.
+  * Labels that start with '@' are batch (hyper-)edges: kept, not summed,
+    when shared.  The engine uses '@b' to batch many bit-strings through
+    one plan walk as the GEMM batch dimension.
+  * Buffers are flat 1-D torch tensors (rank-30 tensors exceed torch's
+    dimension limit); `dims` carries the shape.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+
+try:  # torch is plumbing only (device buffers + current stream)
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+BATCH_PREFIX = "@"
+
+_TORCH_OF = {}
+_NP_OF = {}
+if torch is not None:
+    _TORCH_OF = {np.dtype(np.complex64): torch.complex64, np.dtype(np.complex128): torch.complex128}
+    _NP_OF = {torch.complex64: np.dtype(np.complex64), torch.complex128: np.dtype(np.complex128)}
+
+# GEMM engine for contractions: "auto" (tcgen05 3xTF32 where it pays), "ffma", "tc3"
+_GEMM_MODES = {"auto": _lib.GEMM_AUTO, "ffma": _lib.GEMM_FFMA, "tc3": _lib.GEMM_TC3}
+_gemm_mode = _lib.GEMM_AUTO
+
+
+def set_gemm_mode(mode: str) -> str:
+    """Select the complex64 GEMM engine; returns the previous mode name."""
+    global _gemm_mode
+    if mode not in _GEMM_MODES:
+        raise ValueError(f"gemm mode must be one of {sorted(_GEMM_MODES)}")
+    prev = next(k for k, v in _GEMM_MODES.items() if v == _gemm_mode)
+    _gemm_mode = _GEMM_MODES[mode]
+    return prev
+
+
+def get_gemm_mode() -> str:
+    return next(k for k, v in _GEMM_MODES.items() if v == _gemm_mode)
+
+
+def _require_cuda():
+    if torch is None or not torch.cuda.is_available():
+        raise RuntimeError("paper_1811_09599_b200 computes on a CUDA device; none is available "
+                           "(there is no CPU fallback)")
+    _lib.load()
+
+
+def stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def device_buffer(n: int, dtype, device=None):
+    _require_cuda()
+    return torch.empty(max(int(n), 1), dtype=dtype, device=device or torch.cuda.current_device())
+
+
+def _elem_bytes(t) -> int:
+    return 8 if t.dtype == torch.complex64 else 16
+
+
+# ---------------------------------------------------------------------------
+# raw device ops on flat buffers
+
+
+def permute_buffer(src, dims: Sequence[int], perm: Sequence[int], out=None):
+    """out = ascontiguous(transpose(src.view(dims), perm)) on the device (K1)."""
+    n = math.prod(dims)
+    if out is None:
+        out = device_buffer(n, src.dtype, src.device)
+    st = _lib.load().qf_permute(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                len(dims), _lib.dims_array(dims), _lib.perm_array(perm),
+                                _elem_bytes(src), stream_handle())
+    _lib.check(st, "permute")
+    return out
+
+
+def fix_buffer(src, dims: Sequence[int], axis: int, value: int):
+    """src[..., value, ...] along `axis`, contiguous (K4)."""
+    outer = math.prod(dims[:axis])
+    inner = math.prod(dims[axis + 1:])
+    out = device_buffer(outer * inner, src.dtype, src.device)
+    st = _lib.load().qf_fix_axis(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                 outer, int(dims[axis]), inner, int(value), _elem_bytes(src),
+                                 stream_handle())
+    _lib.check(st, "fix")
+    return out
+
+
+def gather_buffer(src, dims: Sequence[int], axis: int, idx):
+    """dst[b, ...] = src[..., idx[b], ...] (K4, batched); idx: device int32."""
+    outer = math.prod(dims[:axis])
+    inner = math.prod(dims[axis + 1:])
+    nidx = int(idx.numel())
+    out = device_buffer(outer * inner * nidx, src.dtype, src.device)
+    st = _lib.load().qf_gather_axis(ctypes.c_void_p(src.data_ptr()),
+                                    ctypes.c_void_p(out.data_ptr()), outer, int(dims[axis]), inner,
+                                    ctypes.c_void_p(idx.data_ptr()), nidx, _elem_bytes(src),
+                                    stream_handle())
+    _lib.check(st, "gather")
+    return out
+
+
+def accumulate_buffer(x, y, n: Optional[int] = None):
+    """y[:n] += x[:n] (K5)."""
+    n = int(x.numel()) if n is None else int(n)
+    st = _lib.load().qf_accumulate(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(y.data_ptr()), n,
+                                   _elem_bytes(y), stream_handle())
+    _lib.check(st, "accumulate")
+
+
+def gemm_buffer(batch, M, N, K, A, opA, B, opB, C, alpha=1.0, beta=0.0, mode=None):
+    """C[b] = alpha op(A[b]) op(B[b]) + beta C[b] on flat row-major buffers."""
+    lda = K if opA == _lib.OP_N else M
+    ldb = N if opB == _lib.OP_N else K
+    lib = _lib.load()
+    sA, sB, sC = M * K, K * N, M * N
+    if C.dtype == torch.complex64:
+        st = lib.qf_cgemm_c64(_gemm_mode if mode is None else mode, batch, M, N, K,
+                              ctypes.c_void_p(A.data_ptr()), max(lda, 1), sA, opA,
+                              ctypes.c_void_p(B.data_ptr()), max(ldb, 1), sB, opB,
+                              ctypes.c_void_p(C.data_ptr()), max(N, 1), sC,
+                              float(np.real(alpha)), float(np.imag(alpha)),
+                              float(np.real(beta)), float(np.imag(beta)), stream_handle())
+    else:
+        st = lib.qf_zgemm_c128(batch, M, N, K,
+                               ctypes.c_void_p(A.data_ptr()), max(lda, 1), sA, opA,
+                               ctypes.c_void_p(B.data_ptr()), max(ldb, 1), sB, opB,
+                               ctypes.c_void_p(C.data_ptr()), max(N, 1), sC,
+                               float(np.real(alpha)), float(np.imag(alpha)),
+                               float(np.real(beta)), float(np.imag(beta)), stream_handle())
+    _lib.check(st, "gemm")
+
+
+# ---------------------------------------------------------------------------
+# labelled device tensor
+
+
+class Tensor:
+    """A row-major device tensor with one string label per index.
+
+    `array` (numpy) may be passed instead of a device buffer; it is
+    uploaded once.  `.array` downloads a numpy copy (API compatibility with
+    the reference's numpy-backed Tensor)."""
+
+    __slots__ = ("labels", "data", "dims")
+
+    def __init__(self, labels: Sequence[str], array, dims: Optional[Sequence[int]] = None):
+        labels = tuple(labels)
+        if len(set(labels)) != len(labels):
+            raise ValueError(f"duplicate labels: {labels}")
+        if isinstance(array, np.ndarray) or np.isscalar(array):
+            arr = np.asarray(array)
+            if arr.dtype not in _TORCH_OF:
+                arr = arr.astype(np.complex64)
+            dims = arr.shape
+            _require_cuda()
+            data = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1)).to(
+                torch.cuda.current_device())
+        else:
+            data = array
+            if dims is None:
+                dims = tuple(array.shape)
+            data = data.reshape(-1)
+        dims = tuple(int(d) for d in dims)
+        if len(dims) != len(labels):
+            raise ValueError(f"{len(dims)}-d array with {len(labels)} labels")
+        self.labels = labels
+        self.data = data
+        self.dims = dims
+
+    @property
+    def size(self) -> int:
+        return math.prod(self.dims)
+
+    @property
+    def nbytes(self) -> int:
+        return self.size * _elem_bytes(self.data)
+
+    @property
+    def dtype(self):
+        return _NP_OF[self.data.dtype]
+
+    @property
+    def array(self) -> np.ndarray:
+        flat = self.data[: self.size].cpu().numpy()
+        return flat.reshape(self.dims) if self.dims else flat.reshape(())
+
+    def dim_of(self, label: str) -> int:
+        return self.dims[self.labels.index(label)]
+
+    def relabel(self, mapping: dict) -> "Tensor":
+        return Tensor(tuple(mapping.get(l, l) for l in self.labels), self.data, self.dims)
+
+    def fix(self, label: str, value: int) -> "Tensor":
+        """Slice one index to a fixed value, dropping it (device gather)."""
+        ax = self.labels.index(label)
+        if not 0 <= value < self.dims[ax]:
+            raise ValueError(f"value {value} out of range for {label!r} (dim {self.dims[ax]})")
+        out = fix_buffer(self.data, self.dims, ax, value)
+        return Tensor(self.labels[:ax] + self.labels[ax + 1:], out,
+                      self.dims[:ax] + self.dims[ax + 1:])
+
+    def gather(self, label: str, idx, batch_label: str = "@b") -> "Tensor":
+        """Batch slice: new leading `batch_label` axis, entry b = fix(label, idx[b])."""
+        ax = self.labels.index(label)
+        out = gather_buffer(self.data, self.dims, ax, idx)
+        return Tensor((batch_label,) + self.labels[:ax] + self.labels[ax + 1:], out,
+                      (int(idx.numel()),) + self.dims[:ax] + self.dims[ax + 1:])
+
+    def transpose_to(self, labels: Sequence[str], thread_count: int = 1) -> "Tensor":
+        labels = tuple(labels)
+        if labels == self.labels:
+            return self
+        if sorted(labels) != sorted(self.labels):
+            raise ValueError(f"{labels} is not a permutation of {self.labels}")
+        perm = [self.labels.index(l) for l in labels]
+        out = permute_buffer(self.data, self.dims, perm)
+        return Tensor(labels, out, tuple(self.dims[p] for p in perm))
+
+    def scalar(self) -> complex:
+        if self.labels:
+            raise ValueError(f"tensor still has indexes {self.labels}")
+        return complex(self.data[0].item())
+
+    def __repr__(self):
+        return f"Tensor({self.labels}, dims={self.dims}, dtype={self.dtype}, device)"
+
+
+def _is_batch(label: str) -> bool:
+    return label.startswith(BATCH_PREFIX)
+
+
+@dataclass(frozen=True)
+class ContractShape:
+    """GEMM view of one pairwise contraction (per batch entry)."""
+
+    batch: int
+    m: int
+    k: int
+    n: int
+
+    @property
+    def flops(self) -> int:
+        """Reference convention: 8 real ops per complex multiply-add,
+        counted per batch entry (rq/contraction_plan.py:516)."""
+        return 8 * self.m * self.k * self.n
+
+
+def contract_shape(a: Tensor, b: Tensor) -> ContractShape:
+    bset, aset = set(b.labels), set(a.labels)
+    bt = m = k = 1
+    for l, d in zip(a.labels, a.dims):
+        if l in bset:
+            if _is_batch(l):
+                bt *= d
+            else:
+                k *= d
+        else:
+            m *= d
+    n = math.prod(d for l, d in zip(b.labels, b.dims) if l not in aset)
+    return ContractShape(bt, m, k, n)
+
+
+def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int = 10) -> Tensor:
+    """Contract over all shared labels (batch '@' labels are kept).
+
+    Output labels: batch labels (a's order), then a's free labels, then
+    b's free labels -- the reference's a_free + b_free order
+    (rq/tensor_core.py:396-419) with the batch axis in front."""
+    if a.data.dtype != b.data.dtype:
+        raise ValueError(f"dtype mismatch: {a.dtype} vs {b.dtype}")
+    bset, aset = set(b.labels), set(a.labels)
+    batch = [l for l in a.labels if l in bset and _is_batch(l)]
+    shared_a = [l for l in a.labels if l in bset and not _is_batch(l)]
+    for l in batch + shared_a:
+        if a.dim_of(l) != b.dim_of(l):
+            raise ValueError(f"dimension mismatch on {l!r}: {a.dim_of(l)} vs {b.dim_of(l)}")
+    a_free = [l for l in a.labels if l not in bset]
+    b_free = [l for l in b.labels if l not in aset]
+    # summed-index order follows the bigger operand so it is not permuted
+    if a.size >= b.size:
+        k_order = shared_a
+    else:
+        k_order = [l for l in b.labels if l in aset and not _is_batch(l)]
+
+    def operand(t: Tensor, free, first_is_free):
+        n_layout = batch + (free + k_order if first_is_free else k_order + free)
+        t_layout = batch + (k_order + free if first_is_free else free + k_order)
+        if list(t.labels) == n_layout:
+            return t, _lib.OP_N
+        if list(t.labels) == t_layout:
+            return t, _lib.OP_T
+        return t.transpose_to(n_layout), _lib.OP_N
+
+    A, opA = operand(a, a_free, True)      # N: [batch][M][K], T: [batch][K][M]
+    B, opB = operand(b, b_free, False)     # N: [batch][K][N], T: [batch][N][K]
+    bt = math.prod(a.dim_of(l) for l in batch)
+    m = math.prod(a.dim_of(l) for l in a_free)
+    k = math.prod(a.dim_of(l) for l in k_order)
+    n = math.prod(b.dim_of(l) for l in b_free)
+    out = device_buffer(bt * m * n, a.data.dtype, a.data.device)
+    gemm_buffer(bt, m, n, k, A.data, opA, B.data, opB, out)
+    labels = tuple(batch + a_free + b_free)
+    dims = tuple(a.dim_of(l) for l in batch + a_free) + tuple(b.dim_of(l) for l in b_free)
+    return Tensor(labels, out, dims)
+
+
+# ---------------------------------------------------------------------------
+# permutation API shims (reference signatures; one device pass whatever the plan)
+
+
+@dataclass(frozen=True)
+class Move:
+    kind: str
+    group_perm: tuple
+    gamma: int
+
+
+@dataclass(frozen=True)
+class PermutePlan:
+    """(dims, perm) of a transpose.  The reference decomposes it into CPU
+    cache-sized L/R moves (rq/tensor_core.py:81-206); on the B200 the whole
+    permutation is one shared-memory-tiled pass (K1), so `moves` is empty
+    and `device_pass` describes what runs."""
+
+    dims: tuple
+    perm: tuple
+    moves: tuple = ()
+    mu: int = 5
+    nu: int = 10
+    fallback: Optional[str] = None
+    device_pass: str = "tiled"
+
+    @property
+    def out_dims(self) -> tuple:
+        return tuple(self.dims[p] for p in self.perm)
+
+    def move_summary(self) -> list:
+        return [(m.kind, m.gamma) for m in self.moves]
+
+
+def plan_permutation(dims: Sequence[int], perm: Sequence[int], mu: int = 5, nu: int = 10) -> PermutePlan:
+    dims = tuple(int(d) for d in dims)
+    perm = tuple(int(p) for p in perm)
+    if sorted(perm) != list(range(len(dims))):
+        raise ValueError(f"perm {perm} is not a permutation of 0..{len(dims) - 1}")
+    if mu < 0 or nu < mu:
+        raise ValueError(f"need 0 <= mu <= nu, got mu={mu}, nu={nu}")
+    if any(d < 1 for d in dims):
+        raise ValueError("dims must be positive")
+    identity = perm == tuple(range(len(dims)))
+    return PermutePlan(dims, perm, (), mu, nu, None, "none" if identity else "tiled")
+
+
+def _as_device(array):
+    if torch is not None and isinstance(array, torch.Tensor):
+        return array.reshape(-1), None
+    arr = np.ascontiguousarray(array)
+    if arr.dtype not in _TORCH_OF:
+        raise ValueError(f"permutation supports complex64/complex128, got {arr.dtype}")
+    _require_cuda()
+    return torch.from_numpy(arr.reshape(-1)).to(torch.cuda.current_device()), arr.dtype
+
+
+def permute_fast(array, plan: PermutePlan, thread_count: int = 1, workspace=None, map_cache=None):
+    """Apply `plan` on the device.  numpy in -> numpy out; torch in -> torch out."""
+    data, np_dtype = _as_device(array)
+    out = permute_buffer(data, plan.dims, plan.perm)[: math.prod(plan.dims)]
+    if np_dtype is None:
+        return out.view(plan.out_dims) if len(plan.out_dims) <= 25 else out
+    return out.cpu().numpy().reshape(plan.out_dims)
+
+
+def permute_naive(array, perm: Sequence[int]):
+    """Same result as the reference's numpy transpose, computed by K1."""
+    shape = tuple(array.shape)
+    return permute_fast(array, plan_permutation(shape, perm))

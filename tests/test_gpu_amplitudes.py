@@ -1,0 +1,172 @@
+"""End-to-end parity on the B200: every golden amplitude / batch case the
+reference produced, through the product's public API (single, batched,
+open-qubit batch), plus the oracle on cases without golden values.
+
+Tolerance: relative L2 <= 1e-4 over each case's amplitude vector for
+complex64 (BASELINE.json north_star), 1e-10 for complex128."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1811_09599_b200 as qf
+from conftest import golden_amps, rel_l2
+from oracle import rqc_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _tol(dtype):
+    return 1e-10 if dtype == "complex128" else 1e-4
+
+
+def _engine(golden, case):
+    circ = qf.parse_circuit(golden["circuits"][case["circuit"]])
+    plan = qf.parse_plan(golden["plans"][case["plan"]])
+    return qf.AmplitudeEngine(circ, plan, dtype=np.dtype(case["dtype"]))
+
+
+def _cases(golden, kind):
+    return [c["name"] for c in golden[kind]]
+
+
+@pytest.fixture(scope="module", params=["auto", "ffma"])
+def gemm_mode(request):
+    prev = qf.set_gemm_mode(request.param)
+    yield request.param
+    qf.set_gemm_mode(prev)
+
+
+@pytest.mark.parametrize("idx", range(19))
+def test_amplitude_cases_batched(golden, idx, gemm_mode):
+    if idx >= len(golden["amplitudes"]):
+        pytest.skip("no such case")
+    case = golden["amplitudes"][idx]
+    eng = _engine(golden, case)
+    fid = qf.FidelitySpec(case["f"], case["fseed"])
+    got, stats = eng.amplitudes(case["in_bits"], case["out_bits"], fid)
+    assert rel_l2(got, golden_amps(case)) < _tol(case["dtype"]), case["name"]
+    assert (stats.paths_total, stats.paths_used, stats.flops) == \
+        (case["paths_total"], case["paths_used"], case["flops"])
+
+
+@pytest.mark.parametrize("idx", range(19))
+def test_amplitude_cases_single_call(golden, idx):
+    if idx >= len(golden["amplitudes"]):
+        pytest.skip("no such case")
+    case = golden["amplitudes"][idx]
+    eng = _engine(golden, case)
+    fid = qf.FidelitySpec(case["f"], case["fseed"])
+    outs = case["out_bits"][:3]
+    got = []
+    for o in outs:
+        a, stats = eng.amplitude(case["in_bits"], o, fid)
+        got.append(a)
+        assert stats.flops == case["flops"]
+    want = golden_amps(case)[: len(outs)]
+    assert rel_l2(got, want) < _tol(case["dtype"]), case["name"]
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_batch_cases(golden, idx, gemm_mode):
+    if idx >= len(golden["batches"]):
+        pytest.skip("no such case")
+    case = golden["batches"][idx]
+    eng = _engine(golden, case)
+    b = eng.amplitude_batch(case["in_bits"], case["s_ab"], case["c_sites"], case["n_c"],
+                            seed=case["seed"], fidelity=qf.FidelitySpec(case["f"], case["fseed"]))
+    assert list(b.c_values) == case["c_values"]
+    assert [b.out_bits(i) for i in range(len(b))] == case["out_bits"]
+    assert (b.stats.paths_used, b.stats.flops) == (case["paths_used"], case["flops"])
+    assert rel_l2(b.amplitudes, golden_amps(case)) < _tol(case["dtype"]), case["name"]
+
+
+def test_many_batches_in_one_walk_equal_single_batches(golden):
+    case = next(c for c in golden["batches"] if c["name"] == "b70_t16_b64_f64")
+    eng = _engine(golden, case)
+    rng = np.random.Generator(np.random.PCG64(99))
+    sabs = ["".join(str(int(b)) for b in rng.integers(0, 2, size=70)) for _ in range(3)]
+    sabs.append(case["s_ab"])
+    fid = qf.FidelitySpec(case["f"], case["fseed"])
+    many = eng.amplitude_batches(case["in_bits"], sabs, case["c_sites"], 64, seeds=[0] * 4,
+                                 fidelity=fid)
+    assert rel_l2(many[-1].amplitudes, golden_amps(case)) < 1e-4
+    for s, b in zip(sabs, many):
+        one = eng.amplitude_batch(case["in_bits"], s, case["c_sites"], 64, seed=0, fidelity=fid)
+        assert rel_l2(b.amplitudes, one.amplitudes) < 1e-5
+
+
+def test_config2_full_1024_bitstrings_vs_oracle(golden):
+    """Config 2 as benchmarked: 1024 seeded bit-strings; the first 48 are
+    golden (reference), a seeded sample of the rest is checked against the
+    oracle."""
+    case = next(c for c in golden["amplitudes"] if c["name"] == "config2_c64")
+    eng = _engine(golden, case)
+    rng = np.random.Generator(np.random.PCG64(0))
+    outs = [format(int(v), "025b") for v in rng.integers(0, 2 ** 25, size=1024)]
+    assert outs[:48] == case["out_bits"]
+    got, stats = eng.amplitudes(0, outs)
+    assert rel_l2(got[:48], golden_amps(case)) < 1e-4
+    ora = O.OracleEngine(golden["circuits"][case["circuit"]], golden["plans"][case["plan"]],
+                         np.complex128)
+    pick = np.random.default_rng(1).choice(1024, size=24, replace=False)
+    want = [ora.amplitude(0, outs[i])[0] for i in pick]
+    assert rel_l2(got[pick], want) < 1e-4
+    # fidelity-estimator sanity: N * mean |a|^2 ~ 1 for a chaotic circuit (f=1)
+    est = (2 ** 25) * float(np.mean(np.abs(got) ** 2))
+    assert 0.7 < est < 1.3
+
+
+def test_state_and_cut_identity(golden):
+    """Full state vs the double-precision state-vector oracle; the cut sum
+    equals the uncut contraction (acceptance C2 analogue)."""
+    text = golden["circuits"]["g3x4_t12_s8"]
+    circ = qf.parse_circuit(text)
+    psi = O.statevector(text, 0)
+    for n_cuts in (0, 1, 2, 3):
+        eng = qf.AmplitudeEngine(circ, qf.grid_plan(circ.lattice, n_cuts=n_cuts),
+                                 dtype=np.complex128)
+        assert rel_l2(eng.state(0), psi) < 1e-10
+    eng = qf.AmplitudeEngine(circ, qf.grid_plan(circ.lattice, n_cuts=2))
+    assert rel_l2(eng.state(0), psi) < 1e-4
+
+
+def test_reuse_cache_is_transparent(golden):
+    circ = qf.parse_circuit(golden["circuits"]["g4x4_t16_s3"])
+    plan = qf.grid_plan(circ.lattice, n_cuts=2)
+    eng = qf.AmplitudeEngine(circ, plan, dtype=np.complex128)
+    net = eng.base_net(0).fix_outputs({q: 0 for q in range(16)})
+    dims = plan.cut_dims(net.bond_dim)
+    paths = qf.enumerate_paths(dims)
+    with_cache = sum(qf.execute_plan(net, plan, p).scalar() for p in paths)
+    ex = qf.PlanExecutor(net, plan, enable_reuse=False)
+    without = sum(ex.run(p).scalar() for p in paths)
+    assert abs(with_cache - without) < 1e-12
+
+
+def test_memory_budget_and_errors(golden):
+    circ = qf.parse_circuit(golden["circuits"]["g4x4_t16_s0"])
+    eng = qf.AmplitudeEngine(circ, qf.grid_plan(circ.lattice, 1), memory_budget=1024)
+    with pytest.raises(qf.MemoryBudgetError):
+        eng.amplitude(0, 5)
+    eng = qf.AmplitudeEngine(circ)
+    with pytest.raises(ValueError):
+        eng.amplitude(0, 2 ** 16)
+    with pytest.raises(ValueError):
+        eng.amplitude_batch(0, 0, (14, 15), 5)
+    with pytest.raises(ValueError):
+        eng.amplitude_batch(0, 0, (), 1)
+
+
+def test_nonzero_input_and_bristlecone72_fold(golden):
+    text = golden["circuits"]["b72_t8_s0"]
+    circ = qf.parse_circuit(text)
+    # the 72-site frame folds its two corners into their neighbours
+    eng = qf.AmplitudeEngine(circ, qf.load_plan("bristlecone-70").__class__(
+        "bristlecone-72", (), (("contract", qf.ContractStep(
+            tuple(f"t{s}" for s in range(72) if s not in (0, 71)), "r", None)), ("output", "r")),
+        ()))
+    net = eng.base_net(0)
+    assert sorted(net.tensors) == [s for s in range(72) if s not in (0, 71)]
