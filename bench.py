@@ -1,0 +1,410 @@
+"""Benchmark: RQC amplitudes/s on the B200 (BASELINE.json metric).
+
+Workload (N=1 headline, BASELINE.json configs[1] = "config 2"): seeded
+grid:5x5 random circuit, depth 1+24+1 (bond dim 8), 1024 seed-drawn output
+bit-strings, plan grid_plan(lattice, n_cuts=1) -- one cut of dimension 8
+across the middle column (8 slices).  One *step* = all 1024 amplitudes
+(every slice of every bit-string).
+
+  value  : amplitudes/s with inputs resident in HBM (device-timed, CUDA
+           events on the launching stream, max over ranks).
+  e2e    : the same through the public API `AmplitudeEngine.amplitudes`
+           with host bit-strings in and host amplitudes out every step.
+  roofline / kernels : the dominant kernel's achieved rate from per-launch
+           CUDA events (tensor_core.KernelTimer) in a separate profiled step.
+  cpu_baseline : the CPU oracle port (oracle/rqc_oracle.py, the reference
+           algorithm restated in numpy) on a bounded sample, all host cores.
+
+Multi-GPU (torchrun, one process per GPU): `--shard bitstrings` (default,
+weak scaling: each rank computes its own 1024 bit-strings, no collective);
+`--shard slices` (the config as stated: the 8 slices are split across
+ranks and the partial amplitudes all-reduced over NCCL, strong scaling).
+
+`--impl reference` times the reference's algorithm on the host cores (the
+oracle port, multi-process) for the same metric/config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+N_BITSTRINGS = 1024
+LATTICE, DEPTH, SEED, N_CUTS = "grid:5x5", "1+24+1", 0, 1
+
+
+def workload_config(shard: str, world: int) -> dict:
+    return {"workload": "config2: grid:5x5 RQC 1+24+1 (bond 8), 1024 bitstrings/rank, "
+                        "grid_plan n_cuts=1 (8 slices of dim-8 cut)",
+            "lattice": LATTICE, "depth": DEPTH, "circuit_seed": SEED, "cuts": N_CUTS,
+            "bitstrings_per_step": N_BITSTRINGS * (world if shard == "bitstrings" else 1),
+            "parallelism": f"{shard}-sharded x{world}",
+            "l2": "working set > L2 (126 MB): 1024 x 2^18-entry intermediates per step"}
+
+
+def bitstrings(rank: int, n: int, count: int) -> list:
+    rng = np.random.Generator(np.random.PCG64(SEED + rank))
+    return [format(int(v), f"0{n}b") for v in rng.integers(0, 2 ** n, size=count)]
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port on host cores (never the product)
+
+
+def _oracle_worker(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    circuit_text, plan_text, outs = args
+    from oracle import rqc_oracle
+    eng = rqc_oracle.OracleEngine(circuit_text, plan_text, np.complex64)
+    t0 = time.perf_counter()
+    for o in outs:
+        eng.amplitude(0, o)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_rate(circuit_text: str, plan_text: str, outs: list, procs: int) -> dict:
+    """Amplitudes/s of the numpy oracle with `procs` single-threaded worker
+    processes (spawned with every BLAS/OpenMP pool pinned to 1 thread)."""
+    import multiprocessing as mp
+    env_keys = ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS")
+    saved = {k: os.environ.get(k) for k in env_keys}
+    for k in env_keys:
+        os.environ[k] = "1"
+    try:
+        ctx = mp.get_context("spawn")
+        chunks = [outs[i::procs] for i in range(procs)]
+        chunks = [c for c in chunks if c]
+        with ctx.Pool(len(chunks)) as pool:
+            pool.map(_oracle_worker, [(circuit_text, plan_text, c[:1]) for c in chunks])  # warm
+            t0 = time.perf_counter()
+            pool.map(_oracle_worker, [(circuit_text, plan_text, c) for c in chunks])
+            wall = time.perf_counter() - t0
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return {"value": len(outs) / wall, "unit": "amplitudes/s", "cores": len(chunks),
+            "kind": "port", "seconds": wall,
+            "sample": f"{len(outs)} of the 1024 config-2 bit-strings, oracle/rqc_oracle.py "
+                      f"(numpy restatement of the reference), {len(chunks)} processes x 1 thread"}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world: int, backend: str):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+        return False
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+
+
+def peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        d["source"] = "MEASURED_PEAKS.json (measured)"
+        return d
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "B200_PROFILING.md fallback"}
+
+
+def run_gpu(args):
+    import torch
+
+    import paper_1811_09599_b200 as qf
+    from paper_1811_09599_b200 import _lib
+    from paper_1811_09599_b200 import tensor_core as tc
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    init_dist(world, "nccl")
+    dev = torch.device("cuda", local)
+    if args.gemm:
+        qf.set_gemm_mode(args.gemm)
+
+    lat = qf.Lattice.named(LATTICE)
+    circ = qf.generate_rqc(lat, DEPTH, SEED)
+    plan = qf.grid_plan(lat, n_cuts=N_CUTS)
+    shard = args.shard
+    group = None
+    if shard == "slices" and world > 1:
+        import torch.distributed as dist
+        group = dist.group.WORLD
+    eng = qf.AmplitudeEngine(circ, plan, device=local, group=group)
+    outs = bitstrings(rank if shard == "bitstrings" else 0, circ.n, N_BITSTRINGS)
+    bits_host = torch.tensor([[int(c) for c in o] for o in outs], dtype=torch.int32).pin_memory()
+    # ---- device-resident step (value) ----
+    base = eng.base_net(0)
+    bits_dev = bits_host.t().contiguous().to(dev)       # (sites, B): row j = bits of site j
+
+    def step_device():
+        net = base.fix_outputs_batch_device(bits_dev, tuple(range(circ.n)))
+        ex = eng._executor(net)
+        paths = qf.FidelitySpec().paths_for(ex.cut_dims)
+        acc, _ = eng._sum_paths(ex, paths, lambda t: t.data, N_BITSTRINGS)
+        return acc
+
+    def step_e2e():
+        res, _ = eng.amplitudes(0, outs)
+        return res
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    _lib.launch_count(reset=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        start.record()
+        for _ in range(args.steps):
+            acc = step_device()
+        end.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = _lib.launch_count(reset=True) // max(args.steps, 1)
+    ms = max_over_ranks(start.elapsed_time(end) / args.steps, world, dev)
+    amps_per_step = N_BITSTRINGS * (world if shard == "bitstrings" else 1)
+    value = amps_per_step / (ms / 1e3)
+
+    # ---- end-to-end through the public API (host in, host out) ----
+    for _ in range(max(1, args.warmup // 2)):
+        step_e2e()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(args.steps):
+        res = step_e2e()
+    e1.record()
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall_ms), world, dev)
+    e2e = amps_per_step / (e2e_ms / 1e3)
+
+    # ---- per-kernel profile (one extra, separately timed step) ----
+    with tc.KernelTimer() as kt:
+        step_device()
+    kinds = kt.summary()
+    stats_flops = qf.estimate_cost(plan, lat, DEPTH).total_flops  # per amplitude
+    pk = peaks()
+    result = None
+    if rank == 0:
+        kern = {}
+        for kind, d in kinds.items():
+            kern[kind] = {"launches": d["launches"], "ms": round(d["ms"], 4),
+                          "share": None, "tflops": d["flops"] / d["ms"] / 1e9 if d["ms"] else None,
+                          "gbs": d["bytes"] / d["ms"] / 1e6 if d["ms"] else None}
+        total = sum(d["ms"] for d in kinds.values()) or 1.0
+        for kind in kern:
+            kern[kind]["share"] = round(kinds[kind]["ms"] / total, 4)
+        dom = max(kinds, key=lambda k: kinds[k]["ms"])
+        d = kinds[dom]
+        if dom == "gemm":
+            ai = d["flops"] / max(d["bytes"], 1)
+            ridge = pk.get("tf32_tflops", pk["bf16_tflops"] / 2) * 1e12 / (pk["hbm_gbs"] * 1e9)
+        else:
+            ai, ridge = 0.0, 1.0
+        if dom == "gemm" and ai >= ridge:
+            achieved = d["flops"] / d["ms"] / 1e9
+            peak = pk.get("tf32_tflops", pk["bf16_tflops"] / 2) / 3
+            roof = {"bound": "tensor", "unit": "TFLOP/s", "kernel": dom,
+                    "peak_basis": "TF32 dense / 3 (3xTF32 complex)"}
+        else:
+            achieved = d["bytes"] / d["ms"] / 1e6
+            peak = pk["hbm_gbs"]
+            roof = {"bound": "hbm", "unit": "GB/s", "kernel": dom,
+                    "peak_basis": f"hbm_gbs {pk['source']}"}
+        roof.update({"achieved": round(achieved, 2), "peak": peak,
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "algorithmic": f"{dom}: {'8*m*k*n flops' if roof['bound'] == 'tensor' else 'bytes = operands + output (gemm) / 16 B per element (permute)'} per launch, summed over {d['launches']} launches in one step"})
+        clk = clocks.summary()
+        cpu = None
+        if not args.no_cpu_baseline:
+            sample = max(8, min(256, int(args.cpu_sample)))
+            cpu = cpu_oracle_rate(qf.write_circuit(circ), qf.format_plan(plan), outs[:sample],
+                                  host_cores())
+        result = {
+            "metric": "amplitudes/s", "value": round(value, 2), "unit": "amplitudes/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak" if shard == "bitstrings" else "strong",
+            "vs_baseline": None, "dtype": "c64 (fp32 complex; 3xTF32 on tensor cores)",
+            "data": "synthetic (seeded RQC + seeded bit-strings; the paper's circuit files are "
+                    "not in the container)",
+            "config": workload_config(shard, world),
+            "sustained_tflops": round(amps_per_step * stats_flops / (ms / 1e3) / 1e12, 3),
+            "flops_per_amplitude": stats_flops,
+            "gemm_mode": qf.get_gemm_mode(),
+            "e2e": {"value": round(e2e, 2), "unit": "amplitudes/s",
+                    "h2d_bytes_per_step": int(bits_host.numel() * 4),
+                    "d2h_bytes_per_step": int(amps_per_step // world * 8),
+                    "api": "AmplitudeEngine.amplitudes(0, host bit-strings) -> host ndarray"},
+            "roofline": roof, "kernels": kern, "gpu_launches": int(launches),
+            "clocks": clk, "cpu_baseline": cpu,
+        }
+    barrier(world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return result
+
+
+def run_reference(args):
+    """The reference algorithm on the host cores (oracle port), same metric."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    sys.path.insert(0, ROOT)
+    import paper_1811_09599_b200 as qf  # host-side circuit/plan text only
+    lat = qf.Lattice.named(LATTICE)
+    circ = qf.generate_rqc(lat, DEPTH, SEED)
+    plan = qf.grid_plan(lat, n_cuts=N_CUTS)
+    outs = bitstrings(0, circ.n, N_BITSTRINGS)
+    cores = host_cores()
+    sample = max(cores, min(N_BITSTRINGS, int(args.cpu_sample)))
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_rate(qf.write_circuit(circ), qf.format_plan(plan), outs[:sample], cores)
+        if i >= args.warmup:
+            rates.append(r)
+    secs = sum(r["seconds"] for r in rates)
+    value = sample * len(rates) / secs
+    cpu = dict(rates[-1])
+    cpu["value"] = round(value, 3)
+    return {"impl": "reference", "metric": "amplitudes/s", "value": round(value, 3),
+            "unit": "amplitudes/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(secs / len(rates) * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64",
+            "data": "synthetic (seeded RQC + seeded bit-strings)",
+            "config": workload_config("bitstrings", 1),
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(value, 3), "unit": "amplitudes/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--shard", choices=["bitstrings", "slices"], default="bitstrings")
+    ap.add_argument("--gemm", choices=["auto", "ffma", "tc3"], default=None)
+    ap.add_argument("--cpu-sample", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    if out is not None:
+        print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,9 @@ int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
  */
 int qf_accumulate(const void *x, void *y, int64_t n, int elem_bytes, void *stream);
 
+/* y[0:bytes) = 0, stream-ordered (accumulator reset before a path sum). */
+int qf_fill_zero(void *y, int64_t bytes, void *stream);
+
 /*
  * Stream-ordered workspace the GEMM split-K path uses (the only memory
  * the library owns).  Reserve up front to keep allocation out of timed

@@ -31,7 +31,7 @@ from . import slices
 from .circuits import Circuit
 from .contraction_plan import ContractionPlan, PlanExecutor, builtin_plan, enumerate_paths
 from .network_builder import Net2D, build_3d, contract_time, out_label
-from .tensor_core import accumulate_buffer, device_buffer, torch
+from .tensor_core import accumulate_buffer, device_buffer, torch, zero_buffer
 
 
 @dataclass(frozen=True)
@@ -145,7 +145,7 @@ class AmplitudeEngine:
         mine = shard.take(paths)
         acc = device_buffer(size, torch.complex64 if self.dtype == np.complex64
                             else torch.complex128)
-        acc.zero_()
+        zero_buffer(acc)
         for p in mine:
             accumulate_buffer(finish(ex.run(p)), acc, size)
         slices.reduce_partials(acc, self.group)

@@ -174,6 +174,13 @@ int qf_accumulate(const void *x, void *y, int64_t n, int elem_bytes, void *strea
   return qf::check_launch("accumulate");
 }
 
+int qf_fill_zero(void *y, int64_t bytes, void *stream) {
+  QF_REQUIRE(bytes >= 0, "fill_zero: negative size");
+  if (bytes == 0) return QF_OK;
+  QF_CUDA(cudaMemsetAsync(y, 0, (size_t)bytes, qf::as_stream(stream)));
+  return QF_OK;
+}
+
 int qf_workspace_reserve(int64_t bytes, void *stream) {
   int st = QF_OK;
   qf::workspace(bytes, qf::as_stream(stream), &st);

@@ -86,6 +86,60 @@ def _elem_bytes(t) -> int:
     return 8 if t.dtype == torch.complex64 else 16
 
 
+class KernelTimer:
+    """Collects CUDA-event timings of every library call made while active
+    (bench.py's per-kernel roofline).  Each record: (kind, start, end,
+    algorithmic flops, algorithmic bytes)."""
+
+    def __init__(self):
+        self.records = []
+
+    def __enter__(self):
+        global _timer
+        self._prev = _timer
+        _timer = self
+        return self
+
+    def __exit__(self, *exc):
+        global _timer
+        _timer = self._prev
+        return False
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for kind, a, b, flops, nbytes in self.records:
+            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0, "bytes": 0})
+            d["launches"] += 1
+            d["ms"] += a.elapsed_time(b)
+            d["flops"] += flops
+            d["bytes"] += nbytes
+        return out
+
+
+_timer: Optional[KernelTimer] = None
+
+
+class _timed:
+    __slots__ = ("kind", "flops", "nbytes", "ev")
+
+    def __init__(self, kind, flops=0, nbytes=0):
+        self.kind, self.flops, self.nbytes = kind, flops, nbytes
+
+    def __enter__(self):
+        if _timer is not None:
+            self.ev = torch.cuda.Event(enable_timing=True)
+            self.ev.record()
+        return self
+
+    def __exit__(self, *exc):
+        if _timer is not None:
+            end = torch.cuda.Event(enable_timing=True)
+            end.record()
+            _timer.records.append((self.kind, self.ev, end, self.flops, self.nbytes))
+        return False
+
+
 # ---------------------------------------------------------------------------
 # raw device ops on flat buffers
 
@@ -95,9 +149,10 @@ def permute_buffer(src, dims: Sequence[int], perm: Sequence[int], out=None):
     n = math.prod(dims)
     if out is None:
         out = device_buffer(n, src.dtype, src.device)
-    st = _lib.load().qf_permute(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                len(dims), _lib.dims_array(dims), _lib.perm_array(perm),
-                                _elem_bytes(src), stream_handle())
+    with _timed("permute", 0, 2 * n * _elem_bytes(src)):
+        st = _lib.load().qf_permute(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                    len(dims), _lib.dims_array(dims), _lib.perm_array(perm),
+                                    _elem_bytes(src), stream_handle())
     _lib.check(st, "permute")
     return out
 
@@ -128,6 +183,13 @@ def gather_buffer(src, dims: Sequence[int], axis: int, idx):
     return out
 
 
+def zero_buffer(y):
+    """y[:] = 0 (stream-ordered memset)."""
+    st = _lib.load().qf_fill_zero(ctypes.c_void_p(y.data_ptr()), int(y.numel()) * _elem_bytes(y),
+                                  stream_handle())
+    _lib.check(st, "fill_zero")
+
+
 def accumulate_buffer(x, y, n: Optional[int] = None):
     """y[:n] += x[:n] (K5)."""
     n = int(x.numel()) if n is None else int(n)
@@ -142,6 +204,14 @@ def gemm_buffer(batch, M, N, K, A, opA, B, opB, C, alpha=1.0, beta=0.0, mode=Non
     ldb = N if opB == _lib.OP_N else K
     lib = _lib.load()
     sA, sB, sC = M * K, K * N, M * N
+    eb = _elem_bytes(C)
+    with _timed("gemm", 8 * batch * M * N * K, eb * batch * (sA + sB + sC)):
+        st = _gemm_call(lib, batch, M, N, K, A, lda, opA, B, ldb, opB, C, sA, sB, sC, alpha, beta,
+                        mode)
+    _lib.check(st, "gemm")
+
+
+def _gemm_call(lib, batch, M, N, K, A, lda, opA, B, ldb, opB, C, sA, sB, sC, alpha, beta, mode):
     if C.dtype == torch.complex64:
         st = lib.qf_cgemm_c64(_gemm_mode if mode is None else mode, batch, M, N, K,
                               ctypes.c_void_p(A.data_ptr()), max(lda, 1), sA, opA,
@@ -156,7 +226,7 @@ def gemm_buffer(batch, M, N, K, A, opA, B, opB, C, alpha=1.0, beta=0.0, mode=Non
                                ctypes.c_void_p(C.data_ptr()), max(N, 1), sC,
                                float(np.real(alpha)), float(np.imag(alpha)),
                                float(np.real(beta)), float(np.imag(beta)), stream_handle())
-    _lib.check(st, "gemm")
+    return st
 
 
 # ---------------------------------------------------------------------------
