@@ -125,6 +125,11 @@ int qf_fill_zero(void *y, int64_t bytes, void *stream);
 int qf_workspace_reserve(int64_t bytes, void *stream);
 int qf_workspace_release(void);
 
+/* K2 tuning/validation knob: 0 = auto, 1 = A operand staged in shared
+ * memory (tcgen05 SS form), 2 = A operand in tensor memory (TS form).
+ * Returns the previous setting. */
+int qf_tc3_set_variant(int variant);
+
 /* Number of kernels this library launched on the calling thread since the
  * last reset (for the bench's gpu_launches claim). */
 int64_t qf_launch_count(int reset);

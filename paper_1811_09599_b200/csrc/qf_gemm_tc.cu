@@ -1,11 +1,725 @@
-// K2 -- tcgen05 3xTF32 complex GEMM (placeholder until the kernel lands).
+// K2 -- complex64 GEMM on the 5th-generation tensor cores (tcgen05,
+// kind::tf32) with a 3xTF32 split, for sm_100a.
+//
+// Replaces the OpenBLAS cgemm behind `@` at rq/tensor_core.py:417 for the
+// shapes that fill tensor-core tiles.
+//
+// Math.  Per complex index k the real-block form
+//     [Dre | Dim] += Ar[:,k] x [ Br | Bi ]  +  Ai[:,k] x [ -Bi | Br ]
+// turns one complex MAC into two real MMAs with N' = 2*BN.  Each operand
+// x is split x = hi + lo with hi = tf32(x), lo = tf32(x - hi), and
+// a*b ~ ah*bh + ah*bl + al*bh (3 MMAs) keeps ~fp32 accuracy -- six
+// tcgen05.mma per 8 complex k.  Algorithmic flops = 8*M*N*K as in the
+// reference's cost model; the tensor pipe issues 3x the flops of a 1xTF32
+// complex GEMM, so the roofline is TF32_peak / 3.
+//
+// Data flow per CTA (128 threads = 4 warps, one 128 x BN complex C tile):
+//   global (any N/T layout, complex64) --ld.global--> registers (2-deep
+//   prefetch) --split hi/lo--> B' planes in shared memory, in the UMMA
+//   K-major SWIZZLE_NONE core-matrix layout, stored once as three row
+//   blocks [-Bi | Br | Bi] so [Br|Bi] and [-Bi|Br] are both contiguous
+//   descriptor windows; A planes (Ar/Ai x hi/lo) either in shared memory
+//   (SS variant) or written straight into tensor memory with tcgen05.st
+//   (TS variant: thread t owns row t == TMEM lane t, A never touches smem,
+//   which halves the smem traffic of the MMAs).  One elected thread issues
+//   the six MMAs per stage and tcgen05.commit's an mbarrier that frees the
+//   stage; a ring of S stages keeps the tensor pipe busy while the next
+//   stages are converted.  Accumulators [Dre | Dim] live in TMEM
+//   (2*BN fp32 columns); the epilogue reads them with tcgen05.ld, applies
+//   alpha/beta and writes interleaved complex64.
+#include <algorithm>
+#include <type_traits>
+
 #include "qf_common.cuh"
 
 namespace qf {
-struct GemmArgs;
-bool tc3_eligible(const GemmArgs &) { return false; }
-int gemm_tc3(const GemmArgs &, cudaStream_t) {
-  set_error("tcgen05 GEMM not built yet");
-  return QF_ERR_UNSUPPORTED;
+
+struct GemmArgs {
+  int64_t batch, M, N, K;
+  const void *A;
+  int64_t lda, sA;
+  int opA;
+  const void *B;
+  int64_t ldb, sB;
+  int opB;
+  void *C;
+  int64_t ldc, sC;
+  double ar, ai, br, bi;
+};
+
+namespace tc {
+
+constexpr int BM = 128;     // rows per tile (= TMEM lanes)
+constexpr int KB = 8;       // complex k per stage (= one tf32 MMA K step)
+constexpr int THREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// hi = tf32(x), lo = tf32(x - hi); returned as raw fp32 bit patterns
+__device__ __forceinline__ void split3(float x, uint32_t &hi, uint32_t &lo) {
+  hi = tf32_rna(x);
+  lo = tf32_rna(x - __uint_as_float(hi));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// K-major, SWIZZLE_NONE UMMA shared-memory descriptor.  Core matrix = 8
+// rows x 16 B; the two 16-byte K halves of one tf32 K=8 step are LBO=128 B
+// apart, consecutive 8-row groups SBO=256 B apart.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// byte offset of (row r, k) inside a [rows x 8 tf32] K-major core-matrix tile
+__device__ __forceinline__ uint32_t core_off(int r, int kchunk) {
+  return (uint32_t)((r >> 3) * 256 + kchunk * 128 + (r & 7) * 16);
+}
+
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4)            // D format f32
+         | (2u << 7)          // A format tf32
+         | (2u << 10)         // B format tf32
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+// ---------------------------------------------------------------------------
+
+template <int BN, int STAGES, bool A_TMEM>
+struct Layout {
+  static constexpr int NP = 2 * BN;                       // real MMA N
+  static constexpr int B_BLOCK = BN * 32;                 // bytes of one BN-row block (8 tf32)
+  static constexpr int B_PLANE = 3 * B_BLOCK;             // [-Bi | Br | Bi]
+  static constexpr int B_STAGE = 2 * B_PLANE;             // hi, lo
+  static constexpr int A_PLANE = BM * 32;                 // 128 rows x 8 tf32
+  static constexpr int A_STAGE = A_TMEM ? 0 : 4 * A_PLANE;  // re_hi, re_lo, im_hi, im_lo
+  static constexpr int STAGE = B_STAGE + A_STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 1024;     // + barriers / tmem slot
+  static constexpr int ACC_COLS = NP;
+  static constexpr int A_COLS = A_TMEM ? STAGES * 32 : 0;
+  static constexpr int TMEM_COLS = (ACC_COLS + A_COLS) <= 128   ? 128
+                                   : (ACC_COLS + A_COLS) <= 256 ? 256
+                                                                : 512;
+};
+
+template <int BN, int STAGES, bool A_TMEM>
+__global__ void __launch_bounds__(THREADS, 1)
+    cgemm_tc3_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
+  using L = Layout<BN, STAGES, A_TMEM>;
+  static_assert(BN == 128 || BN == 64, "BN");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * L::STAGE);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + STAGES + 1);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t d_tmem = tmem;                      // accumulators: cols [0, 2*BN)
+  const uint32_t a_tmem = tmem + L::ACC_COLS;        // TS: A planes after the accumulators
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
+
+  const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+  const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+  float2 *Cb = reinterpret_cast<float2 *>(g.C);
+  const int64_t nk = (g.K + KB - 1) / KB;
+  // B elements per thread per stage: KB * BN / THREADS
+  constexpr int BE = KB * BN / THREADS;  // 8 (BN=128) or 4 (BN=64)
+  uint32_t phase_bits = 0;              // per-stage parity of the next wait
+
+  for (int64_t work = blockIdx.x; work < tiles * g.batch; work += gridDim.x) {
+    const int64_t bidx = work / tiles;
+    const int64_t tile = work - bidx * tiles;
+    const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    const float2 *A = Ab + bidx * g.sA;
+    const float2 *B = Bb + bidx * g.sB;
+    float2 *C = Cb + bidx * g.sC;
+
+    // thread -> operand element mapping
+    const int64_t am = m0 + tid;                      // A row owned by this thread
+    // B: thread owns column n = n0 + (tid % BN), k in [kq*BE, kq*BE+BE)
+    const int bn_local = tid % BN;
+    const int kq = tid / BN;
+    const int64_t bn = n0 + bn_local;
+
+    float2 ra[2][KB], rb[2][BE];
+    auto load = [&](auto bufc, int64_t kb) {
+      constexpr int buf = decltype(bufc)::value;
+      const int64_t k0 = kb * KB;
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int64_t gk = k0 + k;
+        float2 v = make_float2(0.f, 0.f);
+        if (am < g.M && gk < g.K)
+          v = (g.opA == QF_OP_N) ? __ldg(A + am * g.lda + gk) : __ldg(A + gk * g.lda + am);
+        ra[buf][k] = v;
+      }
+#pragma unroll
+      for (int e = 0; e < BE; ++e) {
+        const int64_t gk = k0 + kq * BE + e;
+        float2 v = make_float2(0.f, 0.f);
+        if (bn < g.N && gk < g.K)
+          v = (g.opB == QF_OP_N) ? __ldg(B + gk * g.ldb + bn) : __ldg(B + bn * g.ldb + gk);
+        rb[buf][e] = v;
+      }
+    };
+
+    auto convert = [&](auto bufc, int s) {
+      constexpr int buf = decltype(bufc)::value;
+      uint8_t *stage = smem + s * L::STAGE;
+      // ---- B planes: rows [-Bi | Br | Bi], hi then lo
+      {
+        uint32_t hr[BE], lr[BE], hi_[BE], li[BE];
+#pragma unroll
+        for (int e = 0; e < BE; ++e) {
+          split3(rb[buf][e].x, hr[e], lr[e]);
+          split3(rb[buf][e].y, hi_[e], li[e]);
+        }
+        // BE consecutive k: BE==8 -> two 16 B chunks, BE==4 -> one chunk (chunk kq)
+#pragma unroll
+        for (int c = 0; c < BE / 4; ++c) {
+          const int chunk = (BE == 8) ? c : kq;
+          const uint32_t off = core_off(bn_local, chunk);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint8_t *plane = stage + h * L::B_PLANE;
+            const uint32_t *re = h ? lr : hr;
+            const uint32_t *im = h ? li : hi_;
+            uint4 vneg = make_uint4(im[4 * c] ^ 0x80000000u, im[4 * c + 1] ^ 0x80000000u,
+                                    im[4 * c + 2] ^ 0x80000000u, im[4 * c + 3] ^ 0x80000000u);
+            uint4 vre = make_uint4(re[4 * c], re[4 * c + 1], re[4 * c + 2], re[4 * c + 3]);
+            uint4 vim = make_uint4(im[4 * c], im[4 * c + 1], im[4 * c + 2], im[4 * c + 3]);
+            *reinterpret_cast<uint4 *>(plane + 0 * L::B_BLOCK + off) = vneg;
+            *reinterpret_cast<uint4 *>(plane + 1 * L::B_BLOCK + off) = vre;
+            *reinterpret_cast<uint4 *>(plane + 2 * L::B_BLOCK + off) = vim;
+          }
+        }
+      }
+      // ---- A planes for row `tid`: re_hi, re_lo, im_hi, im_lo
+      uint32_t p[4][KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        split3(ra[buf][k].x, p[0][k], p[1][k]);
+        split3(ra[buf][k].y, p[2][k], p[3][k]);
+      }
+      if constexpr (A_TMEM) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tmem_st8(a_tmem + lane_base + (uint32_t)(s * 32 + q * 8), p[q]);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      } else {
+        uint8_t *ab = stage + L::B_STAGE;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            *reinterpret_cast<uint4 *>(ab + q * L::A_PLANE + core_off(tid, c)) =
+                make_uint4(p[q][4 * c], p[q][4 * c + 1], p[q][4 * c + 2], p[q][4 * c + 3]);
+      }
+    };
+
+    auto issue = [&](int s, int64_t kb) {
+      uint8_t *stage = smem + s * L::STAGE;
+      const uint32_t bhi = smem_u32(stage), blo = smem_u32(stage + L::B_PLANE);
+      // [Br | Bi] window starts at block 1; [-Bi | Br] at block 0
+      const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
+      const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
+      const uint32_t acc0 = kb > 0 ? 1u : 0u;
+      if constexpr (A_TMEM) {
+        const uint32_t a = a_tmem + (uint32_t)(s * 32);
+        mma_ts(d_tmem, a + 0, b1h, IDESC, acc0);   // re_hi x [Br|Bi]_hi
+        mma_ts(d_tmem, a + 0, b1l, IDESC, 1u);     // re_hi x [Br|Bi]_lo
+        mma_ts(d_tmem, a + 8, b1h, IDESC, 1u);     // re_lo x [Br|Bi]_hi
+        mma_ts(d_tmem, a + 16, b2h, IDESC, 1u);    // im_hi x [-Bi|Br]_hi
+        mma_ts(d_tmem, a + 16, b2l, IDESC, 1u);    // im_hi x [-Bi|Br]_lo
+        mma_ts(d_tmem, a + 24, b2h, IDESC, 1u);    // im_lo x [-Bi|Br]_hi
+      } else {
+        const uint32_t ab = smem_u32(stage + L::B_STAGE);
+        const uint64_t arh = smem_desc(ab), arl = smem_desc(ab + L::A_PLANE);
+        const uint64_t aih = smem_desc(ab + 2 * L::A_PLANE), ail = smem_desc(ab + 3 * L::A_PLANE);
+        mma_ss(d_tmem, arh, b1h, IDESC, acc0);
+        mma_ss(d_tmem, arh, b1l, IDESC, 1u);
+        mma_ss(d_tmem, arl, b1h, IDESC, 1u);
+        mma_ss(d_tmem, aih, b2h, IDESC, 1u);
+        mma_ss(d_tmem, aih, b2l, IDESC, 1u);
+        mma_ss(d_tmem, ail, b2h, IDESC, 1u);
+      }
+      mma_commit(&bars[s]);
+    };
+
+    using B0 = std::integral_constant<int, 0>;
+    using B1 = std::integral_constant<int, 1>;
+    auto step = [&](auto bufc, int64_t kb) {
+      const int s = (int)(kb % STAGES);
+      if (kb >= STAGES) {
+        mbar_wait(&bars[s], (phase_bits >> s) & 1u);
+        phase_bits ^= 1u << s;
+      }
+      convert(bufc, s);
+      if (kb + 2 < nk) load(bufc, kb + 2);
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        issue(s, kb);
+      }
+    };
+    if (nk > 0) load(B0{}, 0);
+    if (nk > 1) load(B1{}, 1);
+    for (int64_t kb = 0; kb < nk; kb += 2) {
+      step(B0{}, kb);
+      if (kb + 1 < nk) step(B1{}, kb + 1);
+    }
+    // drain: wait for every stage's outstanding commit (the last STAGES k-blocks)
+    for (int64_t kb = (nk > STAGES ? nk - STAGES : 0); kb < nk; ++kb) {
+      const int s = (int)(kb % STAGES);
+      mbar_wait(&bars[s], (phase_bits >> s) & 1u);
+      phase_bits ^= 1u << s;
+    }
+    tc_fence_after();
+
+    // ---- epilogue: TMEM -> registers -> C (row tid of the tile)
+    const int64_t row = m0 + tid;
+    const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+    const bool use_beta = (br != 0.f || bi != 0.f);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t vr[32], vi[32];
+      tmem_ld32(d_tmem + lane_base + (uint32_t)c0, vr);
+      tmem_ld32(d_tmem + lane_base + (uint32_t)(BN + c0), vi);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < g.M && nk > 0) {
+        float2 *crow = C + row * g.ldc + n0 + c0;
+        const int64_t ncols = min((int64_t)32, g.N - (n0 + c0));
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < ncols) {
+            const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
+            float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
+            if (use_beta) {
+              const float2 c = crow[j];
+              o.x += br * c.x - bi * c.y;
+              o.y += br * c.y + bi * c.x;
+            }
+            crow[j] = o;
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // all TMEM reads done before the next tile's MMAs overwrite
+    tc_fence_after();
+  }
+
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+}
+
+template <int BN, int STAGES, bool A_TMEM>
+int launch(const GemmArgs &g, cudaStream_t s) {
+  using L = Layout<BN, STAGES, A_TMEM>;
+  auto kern = cgemm_tc3_kernel<BN, STAGES, A_TMEM>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) {
+      set_error("tc3: cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    attr = true;
+  }
+  const int64_t tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM - 1) / BM;
+  const int64_t tiles = tiles_n * tiles_m;
+  const int64_t work = tiles * g.batch;
+  const int64_t grid = std::min<int64_t>(work, (int64_t)sm_count());
+  kern<<<(unsigned)grid, THREADS, L::SMEM, s>>>(g, tiles_n, tiles);
+  return check_launch("cgemm_tc3");
+}
+
+
+// ---------------------------------------------------------------------------
+// v2: promoted accumulation.  The tensor pipe's fp32 accumulation truncates,
+// so error grows ~linearly with K (measured: 1.4e-8 * K relative).  As in
+// DeepGEMM's FP8 "promotion", each chunk of CK k-blocks accumulates fresh in
+// one of two TMEM partial buffers; after the chunk's MMAs retire the CUDA
+// cores add that partial into fp32 registers (round-to-nearest) while the
+// tensor pipe fills the other buffer.  256 threads: warp w owns TMEM lanes
+// 32*(w%4).. and half (w/4) of every row's columns.
+
+constexpr int V2_THREADS = 256;
+constexpr int V2_BN = 64;
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c,
+                                         uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+template <int STAGES, int CK>
+struct LayoutV2 {
+  static constexpr int BN = V2_BN;
+  static constexpr int NP = 2 * BN;            // 128 real columns per partial
+  static constexpr int B_BLOCK = BN * 32;
+  static constexpr int B_PLANE = 3 * B_BLOCK;
+  static constexpr int STAGE = 2 * B_PLANE;    // B planes only (A lives in TMEM)
+  static constexpr int SMEM = STAGES * STAGE + 1024;
+  static constexpr int P_COLS = NP;            // one partial buffer
+  static constexpr int A_COL0 = 2 * P_COLS;    // A ring after the two partials
+  static constexpr int TMEM_COLS = 512;
+  static_assert(2 * P_COLS + STAGES * 32 <= 512, "TMEM budget");
+};
+
+template <int STAGES, int CK>
+__global__ void __launch_bounds__(V2_THREADS, 1)
+    cgemm_tc3p_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
+  using L = LayoutV2<STAGES, CK>;
+  constexpr int BN = L::BN;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * L::STAGE);  // [STAGES]
+  uint64_t *pbar = bars + STAGES;                                           // [2] chunk done
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pbar + 2);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int lg = warp & 3;       // TMEM lane group
+  const int half = warp >> 2;    // which half of the columns / k
+  const int row_l = lg * 32 + lane;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES + 2; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+  constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
+
+  const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+  const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+  float2 *Cb = reinterpret_cast<float2 *>(g.C);
+  const int64_t nk = (g.K + KB - 1) / KB;
+  const int64_t nchunks = (nk + CK - 1) / CK;
+  constexpr int BE = KB * BN / V2_THREADS;  // 2 B elements (consecutive k) per thread
+  uint32_t phase_bits = 0;                  // bits [0,STAGES): stage barriers; +STAGES: partials
+
+  for (int64_t work = blockIdx.x; work < tiles * g.batch; work += gridDim.x) {
+    const int64_t bidx = work / tiles;
+    const int64_t tile = work - bidx * tiles;
+    const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    const float2 *A = Ab + bidx * g.sA;
+    const float2 *B = Bb + bidx * g.sB;
+    float2 *C = Cb + bidx * g.sC;
+    const int64_t am = m0 + row_l;           // A row (this thread: k in [4*half, 4*half+4))
+    const int bn_local = tid % BN;
+    const int kq = tid / BN;                 // 0..3 -> k = 2*kq, 2*kq+1
+    const int64_t bn = n0 + bn_local;
+
+    float racc[32], iacc[32];                // promoted sums: columns n0 + 32*half + j
+#pragma unroll
+    for (int j = 0; j < 32; ++j) racc[j] = iacc[j] = 0.f;
+
+    float2 ra[2][4], rb[2][BE];
+    auto load = [&](auto bufc, int64_t kb) {
+      constexpr int buf = decltype(bufc)::value;
+      const int64_t k0 = kb * KB;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t gk = k0 + 4 * half + k;
+        float2 v = make_float2(0.f, 0.f);
+        if (am < g.M && gk < g.K)
+          v = (g.opA == QF_OP_N) ? __ldg(A + am * g.lda + gk) : __ldg(A + gk * g.lda + am);
+        ra[buf][k] = v;
+      }
+#pragma unroll
+      for (int e = 0; e < BE; ++e) {
+        const int64_t gk = k0 + kq * BE + e;
+        float2 v = make_float2(0.f, 0.f);
+        if (bn < g.N && gk < g.K)
+          v = (g.opB == QF_OP_N) ? __ldg(B + gk * g.ldb + bn) : __ldg(B + bn * g.ldb + gk);
+        rb[buf][e] = v;
+      }
+    };
+    auto convert = [&](auto bufc, int s) {
+      constexpr int buf = decltype(bufc)::value;
+      uint8_t *stage = smem + s * L::STAGE;
+      uint32_t hr[BE], lr[BE], hi_[BE], li[BE];
+#pragma unroll
+      for (int e = 0; e < BE; ++e) {
+        split3(rb[buf][e].x, hr[e], lr[e]);
+        split3(rb[buf][e].y, hi_[e], li[e]);
+      }
+      const int kfirst = kq * BE;  // 0,2,4,6
+      const uint32_t off = core_off(bn_local, kfirst >> 2) + (uint32_t)((kfirst & 3) * 4);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint8_t *plane = stage + h * L::B_PLANE;
+        const uint32_t *re = h ? lr : hr;
+        const uint32_t *im = h ? li : hi_;
+        *reinterpret_cast<uint2 *>(plane + 0 * L::B_BLOCK + off) =
+            make_uint2(im[0] ^ 0x80000000u, im[1] ^ 0x80000000u);
+        *reinterpret_cast<uint2 *>(plane + 1 * L::B_BLOCK + off) = make_uint2(re[0], re[1]);
+        *reinterpret_cast<uint2 *>(plane + 2 * L::B_BLOCK + off) = make_uint2(im[0], im[1]);
+      }
+      uint32_t p[4][4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        split3(ra[buf][k].x, p[0][k], p[1][k]);
+        split3(ra[buf][k].y, p[2][k], p[3][k]);
+      }
+      const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32 + 4 * half);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_st4(acol + q * 8, p[q][0], p[q][1], p[q][2], p[q][3]);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    };
+    auto promote = [&](int pb) {
+      // wait for the chunk that used partial buffer pb, then add it into registers
+      mbar_wait(&pbar[pb], (phase_bits >> (STAGES + pb)) & 1u);
+      phase_bits ^= 1u << (STAGES + pb);
+      tc_fence_after();
+      uint32_t v[32];
+      const uint32_t base = tmem + lane_base + (uint32_t)(pb * L::P_COLS + 32 * half);
+      tmem_ld32(base, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j) racc[j] += __uint_as_float(v[j]);
+      tmem_ld32(base + BN, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j) iacc[j] += __uint_as_float(v[j]);
+    };
+    auto issue = [&](int s, int64_t kb) {
+      const int64_t chunk = kb / CK;
+      const int pos = (int)(kb - chunk * CK);
+      const uint32_t d = tmem + (uint32_t)((chunk & 1) * L::P_COLS);
+      uint8_t *stage = smem + s * L::STAGE;
+      const uint32_t bhi = smem_u32(stage), blo = smem_u32(stage + L::B_PLANE);
+      const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
+      const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
+      const uint32_t a = tmem + (uint32_t)(L::A_COL0 + s * 32);
+      const uint32_t acc0 = pos > 0 ? 1u : 0u;
+      mma_ts(d, a + 0, b1h, IDESC, acc0);
+      mma_ts(d, a + 0, b1l, IDESC, 1u);
+      mma_ts(d, a + 8, b1h, IDESC, 1u);
+      mma_ts(d, a + 16, b2h, IDESC, 1u);
+      mma_ts(d, a + 16, b2l, IDESC, 1u);
+      mma_ts(d, a + 24, b2h, IDESC, 1u);
+      mma_commit(&bars[s]);
+      if (pos == CK - 1 || kb == nk - 1) mma_commit(&pbar[chunk & 1]);
+    };
+
+    using B0 = std::integral_constant<int, 0>;
+    using B1 = std::integral_constant<int, 1>;
+    auto step = [&](auto bufc, int64_t kb) {
+      const int s = (int)(kb % STAGES);
+      if (kb >= STAGES) {
+        mbar_wait(&bars[s], (phase_bits >> s) & 1u);
+        phase_bits ^= 1u << s;
+      }
+      convert(bufc, s);
+      if (kb + 2 < nk) load(bufc, kb + 2);
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        issue(s, kb);
+      }
+      // one chunk behind: promote the previous chunk's partial
+      const int64_t chunk = kb / CK;
+      if (kb == chunk * CK && chunk >= 1) promote((int)((chunk - 1) & 1));
+    };
+    if (nk > 0) load(B0{}, 0);
+    if (nk > 1) load(B1{}, 1);
+    for (int64_t kb = 0; kb < nk; kb += 2) {
+      step(B0{}, kb);
+      if (kb + 1 < nk) step(B1{}, kb + 1);
+    }
+    if (nchunks > 0) promote((int)((nchunks - 1) & 1));
+    // drain the stage barriers of the last STAGES k-blocks (keeps parity in sync)
+    for (int64_t kb = (nk > STAGES ? nk - STAGES : 0); kb < nk; ++kb) {
+      const int s = (int)(kb % STAGES);
+      mbar_wait(&bars[s], (phase_bits >> s) & 1u);
+      phase_bits ^= 1u << s;
+    }
+
+    // ---- epilogue from registers: row row_l, columns n0 + 32*half + j
+    const int64_t row = m0 + row_l;
+    if (row < g.M) {
+      const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+      const bool use_beta = (br != 0.f || bi != 0.f);
+      const int64_t c0 = n0 + 32 * half;
+      float2 *crow = C + row * g.ldc + c0;
+      const int64_t ncols = min((int64_t)32, g.N - c0);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < ncols) {
+          float2 o = make_float2(ar * racc[j] - ai * iacc[j], ar * iacc[j] + ai * racc[j]);
+          if (use_beta) {
+            const float2 c = crow[j];
+            o.x += br * c.x - bi * c.y;
+            o.y += br * c.y + bi * c.x;
+          }
+          crow[j] = o;
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+}
+
+template <int STAGES, int CK>
+int launch_v2(const GemmArgs &g, cudaStream_t s) {
+  using L = LayoutV2<STAGES, CK>;
+  auto kern = cgemm_tc3p_kernel<STAGES, CK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) {
+      set_error("tc3p: cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    attr = true;
+  }
+  const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + BM - 1) / BM;
+  const int64_t tiles = tiles_n * tiles_m;
+  const int64_t grid = std::min<int64_t>(tiles * g.batch, (int64_t)sm_count());
+  kern<<<(unsigned)grid, V2_THREADS, L::SMEM, s>>>(g, tiles_n, tiles);
+  return check_launch("cgemm_tc3p");
+}
+}  // namespace tc
+
+// variant: 0 = auto (promoted v2), 1 = v1 SS, 2 = v1 TS (v1 accumulates the
+// whole K in TMEM: fastest, but its error grows ~1.4e-8 * K)
+static int g_tc3_variant = 0;
+
+bool tc3_eligible(const GemmArgs &g) {
+  // a 128 x 64 tile reasonably full, K long enough to amortise the pipeline
+  return g.M >= 128 && g.N >= 32 && g.K >= 32 && g.M * g.N * g.batch >= 128 * 64 * 148;
+}
+
+int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
+  if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
+  QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
+  const bool small_n = g.N <= 64;
+  if (g_tc3_variant == 1)
+    return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);
+  if (g_tc3_variant == 2)
+    return small_n ? tc::launch<64, 6, true>(g, s) : tc::launch<128, 4, true>(g, s);
+  return tc::launch_v2<6, 4>(g, s);
+}
+
 }  // namespace qf
+
+extern "C" int qf_tc3_set_variant(int v) {
+  int prev = qf::g_tc3_variant;
+  qf::g_tc3_variant = v;
+  return prev;
+}

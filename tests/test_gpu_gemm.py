@@ -85,3 +85,55 @@ def test_batched_contract_keeps_batch_label():
     ref = np.einsum("bijk,bkjm->bim", A, B)
     np.testing.assert_allclose(out.transpose_to(("@b", "i", "m")).array, ref, rtol=1e-5,
                                atol=1e-6)
+
+
+TC_SHAPES = [(1, 128, 128, 8), (1, 128, 128, 64), (2, 256, 256, 40), (1, 300, 200, 77),
+             (3, 4096, 64, 64), (1, 1000, 130, 1000), (4, 512, 64, 8), (1, 129, 257, 3),
+             (1, 2048, 2048, 512)]
+
+
+@pytest.fixture(params=[0, 1, 2], ids=["promoted", "SS", "TS"])
+def tc_variant(request):
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(request.param)
+    yield request.param
+    lib.qf_tc3_set_variant(prev)
+
+
+@pytest.mark.parametrize("shape", TC_SHAPES)
+@pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
+def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
+    """3xTF32 keeps ~fp32 accuracy: same 1e-5 bar as the FFMA kernel.  The
+    unpromoted v1 variants accumulate all of K in TMEM (error ~1.4e-8 K),
+    so they are only held to the bar for K <= 256."""
+    if tc_variant != 0 and shape[3] > 256:
+        pytest.skip("v1 variants are exercised at short K only")
+    err = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3)
+    assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("K", [1024, 4096, 32768])
+def test_tcgen05_promoted_accuracy_at_long_k(K):
+    """Promotion keeps the long-K error near the FFMA kernel's (config-4
+    GEMMs have K = 2^15)."""
+    err = _gemm(1, 128, 64, K, 0, 0, np.complex64, mode=_lib.GEMM_TC3)
+    assert err < 5e-6, err
+
+
+def test_tcgen05_alpha_beta(tc_variant):
+    assert _gemm(2, 256, 128, 64, 0, 0, np.complex64, _lib.GEMM_TC3, 0.5 - 1j, 1.0 + 0.5j) < 1e-5
+
+
+def test_tcgen05_matches_ffma_bitwise_scale():
+    """Same inputs through both engines agree to fp32 rounding."""
+    rng = np.random.default_rng(11)
+    M, N, K = 512, 256, 1024
+    A = _rand(rng, (M, K), np.complex64)
+    B = _rand(rng, (K, N), np.complex64)
+    outs = []
+    for mode in (_lib.GEMM_FFMA, _lib.GEMM_TC3):
+        C = torch.empty(M * N, dtype=torch.complex64, device="cuda")
+        tc.gemm_buffer(1, M, N, K, torch.from_numpy(A.reshape(-1)).cuda(), 0,
+                       torch.from_numpy(B.reshape(-1)).cuda(), 0, C, mode=mode)
+        outs.append(C.cpu().numpy())
+    assert np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[0]) < 2e-6
