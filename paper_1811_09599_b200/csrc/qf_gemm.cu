@@ -286,6 +286,87 @@ __global__ void cgemm_skinny_reduce(const __grid_constant__ GemmArgs g, int P, i
   *C = o;
 }
 
+// ---------------------------------------------------------------------------
+// small-KxN streaming kernel: K*N <= SKN_MAX complex (B[b] fits in smem).
+// The memory-bound shapes of region growth -- GEMVs against a cut-sliced
+// site (n = 1), k = 8 / n = 8 bond contractions -- stream A once, coalesced,
+// through shared memory and write C rows coalesced; B[b] is staged once per
+// work item.  One work item = (batch entry, block of rows).
+
+constexpr int SKN_THREADS = 256;
+constexpr int SKN_MAX = 4096;      // complex entries of B held in smem
+constexpr int SKN_A_MAX = 4096;    // complex entries of the staged A block
+
+template <typename R>
+__global__ void __launch_bounds__(SKN_THREADS)
+    cgemm_smallkn_kernel(const __grid_constant__ GemmArgs g, int rm, int64_t blocks_m) {
+  using V = typename C2<R>::T;
+  extern __shared__ __align__(16) unsigned char skn_smem[];
+  const int K = (int)g.K, N = (int)g.N;
+  const int bpitch = N + ((N % 2 == 0) ? 1 : 0);
+  const int apitch = K + ((K % 2 == 0) ? 1 : 0);
+  V *Bs = reinterpret_cast<V *>(skn_smem);
+  V *As = Bs + (size_t)K * bpitch;
+  const int tid = threadIdx.x;
+  const R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
+  const bool use_beta = (br != R(0) || bi != R(0));
+  int64_t cur_b = -1;
+  for (int64_t item = blockIdx.x; item < g.batch * blocks_m; item += gridDim.x) {
+    const int64_t b = item / blocks_m;
+    const int64_t m0 = (item - b * blocks_m) * rm;
+    const int rows = (int)min((int64_t)rm, g.M - m0);
+    __syncthreads();  // previous item done with smem
+    if (b != cur_b) {
+      const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+      for (int i = tid; i < K * N; i += SKN_THREADS) {
+        int k, n;
+        if (g.opB == QF_OP_N) {
+          k = i / N;
+          n = i - k * N;
+          Bs[k * bpitch + n] = B[(int64_t)k * g.ldb + n];
+        } else {
+          n = i / K;
+          k = i - n * K;
+          Bs[k * bpitch + n] = B[(int64_t)n * g.ldb + k];
+        }
+      }
+      cur_b = b;
+    }
+    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    for (int i = tid; i < rows * K; i += SKN_THREADS) {
+      int m, k;
+      if (g.opA == QF_OP_N) {
+        m = i / K;
+        k = i - m * K;
+        As[m * apitch + k] = A[(m0 + m) * g.lda + k];
+      } else {
+        k = i / rows;
+        m = i - k * rows;
+        As[m * apitch + k] = A[(int64_t)k * g.lda + m0 + m];
+      }
+    }
+    __syncthreads();
+    V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
+    for (int o = tid; o < rows * N; o += SKN_THREADS) {
+      const int m = o / N, n = o - m * N;
+      V acc = {R(0), R(0)};
+      const V *arow = As + m * apitch;
+#pragma unroll 8
+      for (int k = 0; k < K; ++k) cfma(acc, arow[k], Bs[k * bpitch + n]);
+      V out;
+      out.x = ar * acc.x - ai * acc.y;
+      out.y = ar * acc.y + ai * acc.x;
+      V *cp = C + (m0 + m) * g.ldc + n;
+      if (use_beta) {
+        const V c = *cp;
+        out.x += br * c.x - bi * c.y;
+        out.y += br * c.y + bi * c.x;
+      }
+      *cp = out;
+    }
+  }
+}
+
 template <typename R>
 __global__ void cgemm_scale_kernel(const __grid_constant__ GemmArgs g) {
   // K == 0: C = beta * C
@@ -316,6 +397,33 @@ int validate(const GemmArgs &g) {
   QF_REQUIRE(g.lda >= std::max<int64_t>(1, g.opA == QF_OP_N ? g.K : g.M), "gemm: lda too small");
   QF_REQUIRE(g.ldb >= std::max<int64_t>(1, g.opB == QF_OP_N ? g.N : g.K), "gemm: ldb too small");
   return QF_OK;
+}
+
+bool smallkn_eligible(const GemmArgs &g) {
+  // B[b] fits in smem and one of the contracted/output widths is narrow:
+  // these shapes are HBM-bound and the 64x64 tile wastes most of its work
+  return g.K * g.N <= SKN_MAX && (g.N <= 16 || g.K <= 16) && g.K >= 1;
+}
+
+template <typename R>
+int gemm_smallkn(const GemmArgs &g, cudaStream_t s) {
+  using V = typename C2<R>::T;
+  const int K = (int)g.K, N = (int)g.N;
+  const int bpitch = N + ((N % 2 == 0) ? 1 : 0), apitch = K + ((K % 2 == 0) ? 1 : 0);
+  int rm = (int)std::min<int64_t>(g.M, std::max(1, SKN_A_MAX / apitch));
+  // enough work items to fill the machine when the batch is small
+  int64_t blocks_m = (g.M + rm - 1) / rm;
+  size_t smem = ((size_t)K * bpitch + (size_t)rm * apitch) * sizeof(V);
+  static thread_local bool attr[2] = {false, false};
+  auto kern = cgemm_smallkn_kernel<R>;
+  if (!attr[sizeof(R) == 8]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    attr[sizeof(R) == 8] = true;
+  }
+  int64_t items = g.batch * blocks_m;
+  int64_t grid = std::min<int64_t>(items, (int64_t)sm_count() * 6);
+  kern<<<(unsigned)grid, SKN_THREADS, smem, s>>>(g, rm, blocks_m);
+  return check_launch("cgemm_smallkn");
 }
 
 template <typename R>
@@ -351,6 +459,7 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
                                                                            ws);
     return check_launch("cgemm_skinny_reduce");
   }
+  if (smallkn_eligible(g)) return gemm_smallkn<R>(g, s);
   int64_t tiles_n = (g.N + TBN - 1) / TBN, tiles_m = (g.M + TBM - 1) / TBM;
   int64_t tiles = tiles_n * tiles_m;
   int64_t work = tiles * g.batch;

@@ -105,11 +105,12 @@ class KernelTimer:
         _timer = self._prev
         return False
 
-    def summary(self) -> dict:
+    def summary(self, detail: bool = False) -> dict:
         torch.cuda.synchronize()
         out: dict = {}
-        for kind, a, b, flops, nbytes in self.records:
-            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "flops": 0, "bytes": 0})
+        for kind, a, b, flops, nbytes, *rest in self.records:
+            key = f"{kind} {rest[0]}" if detail and rest and rest[0] else kind
+            d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0, "bytes": 0})
             d["launches"] += 1
             d["ms"] += a.elapsed_time(b)
             d["flops"] += flops
@@ -121,10 +122,10 @@ _timer: Optional[KernelTimer] = None
 
 
 class _timed:
-    __slots__ = ("kind", "flops", "nbytes", "ev")
+    __slots__ = ("kind", "flops", "nbytes", "ev", "detail")
 
-    def __init__(self, kind, flops=0, nbytes=0):
-        self.kind, self.flops, self.nbytes = kind, flops, nbytes
+    def __init__(self, kind, flops=0, nbytes=0, detail=""):
+        self.kind, self.flops, self.nbytes, self.detail = kind, flops, nbytes, detail
 
     def __enter__(self):
         if _timer is not None:
@@ -136,7 +137,7 @@ class _timed:
         if _timer is not None:
             end = torch.cuda.Event(enable_timing=True)
             end.record()
-            _timer.records.append((self.kind, self.ev, end, self.flops, self.nbytes))
+            _timer.records.append((self.kind, self.ev, end, self.flops, self.nbytes, self.detail))
         return False
 
 
@@ -149,7 +150,8 @@ def permute_buffer(src, dims: Sequence[int], perm: Sequence[int], out=None):
     n = math.prod(dims)
     if out is None:
         out = device_buffer(n, src.dtype, src.device)
-    with _timed("permute", 0, 2 * n * _elem_bytes(src)):
+    with _timed("permute", 0, 2 * n * _elem_bytes(src),
+                f"dims{tuple(dims)} perm{tuple(perm)}" if _timer else ""):
         st = _lib.load().qf_permute(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                     len(dims), _lib.dims_array(dims), _lib.perm_array(perm),
                                     _elem_bytes(src), stream_handle())
@@ -205,7 +207,8 @@ def gemm_buffer(batch, M, N, K, A, opA, B, opB, C, alpha=1.0, beta=0.0, mode=Non
     lib = _lib.load()
     sA, sB, sC = M * K, K * N, M * N
     eb = _elem_bytes(C)
-    with _timed("gemm", 8 * batch * M * N * K, eb * batch * (sA + sB + sC)):
+    with _timed("gemm", 8 * batch * M * N * K, eb * batch * (sA + sB + sC),
+                f"b{batch} m{M} n{N} k{K} {'NT'[opA]}{'NT'[opB]}" if _timer else ""):
         st = _gemm_call(lib, batch, M, N, K, A, lda, opA, B, ldb, opB, C, sA, sB, sC, alpha, beta,
                         mode)
     _lib.check(st, "gemm")
@@ -240,7 +243,7 @@ class Tensor:
     uploaded once.  `.array` downloads a numpy copy (API compatibility with
     the reference's numpy-backed Tensor)."""
 
-    __slots__ = ("labels", "data", "dims")
+    __slots__ = ("labels", "data", "dims", "_layouts")
 
     def __init__(self, labels: Sequence[str], array, dims: Optional[Sequence[int]] = None):
         labels = tuple(labels)
@@ -265,6 +268,7 @@ class Tensor:
         self.labels = labels
         self.data = data
         self.dims = dims
+        self._layouts = None  # memoised transposes (labels -> Tensor)
 
     @property
     def size(self) -> int:
@@ -309,11 +313,19 @@ class Tensor:
         labels = tuple(labels)
         if labels == self.labels:
             return self
+        if self._layouts is not None and labels in self._layouts:
+            return self._layouts[labels]
         if sorted(labels) != sorted(self.labels):
             raise ValueError(f"{labels} is not a permutation of {self.labels}")
         perm = [self.labels.index(l) for l in labels]
         out = permute_buffer(self.data, self.dims, perm)
-        return Tensor(labels, out, tuple(self.dims[p] for p in perm))
+        t = Tensor(labels, out, tuple(self.dims[p] for p in perm))
+        # an intermediate reused across paths (reuse=global/outer steps) is
+        # permuted once, not once per path; the copy dies with its source
+        if self._layouts is None:
+            self._layouts = {}
+        self._layouts[labels] = t
+        return t
 
     def scalar(self) -> complex:
         if self.labels:

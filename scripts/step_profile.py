@@ -1,0 +1,21 @@
+"""Per-launch breakdown of one config-2 step (KernelTimer, CUDA events)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1811_09599_b200 as qf
+from paper_1811_09599_b200 import tensor_core as tc
+mode = sys.argv[1] if len(sys.argv) > 1 else "auto"
+nb = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+qf.set_gemm_mode(mode)
+lat = qf.Lattice.named("grid:5x5"); circ = qf.generate_rqc(lat, "1+24+1", 0)
+eng = qf.AmplitudeEngine(circ, qf.grid_plan(lat, n_cuts=1))
+rng = np.random.Generator(np.random.PCG64(0))
+outs = [format(int(v), "025b") for v in rng.integers(0, 2 ** 25, size=nb)]
+for _ in range(2): eng.amplitudes(0, outs)
+with tc.KernelTimer() as kt:
+    eng.amplitudes(0, outs)
+s = kt.summary(detail=True)
+tot = sum(d["ms"] for d in s.values())
+print(f"mode={mode} batch={nb} total kernel ms {tot:.2f}")
+for k, d in sorted(s.items(), key=lambda x: -x[1]["ms"])[:40]:
+    print(f"{d['ms']:8.3f} ms {d['launches']:3d}x  {d['bytes']/d['ms']/1e6:7.0f} GB/s {d['flops']/d['ms']/1e9:6.1f} TF/s  {k}")
