@@ -367,6 +367,108 @@ __global__ void __launch_bounds__(SKN_THREADS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// batched GEMV family: N <= 4 output columns, A in N layout (rows contiguous
+// along K).  One warp per row group: lanes stride K with coalesced loads,
+// 4 rows in flight per warp, butterfly reduction.  B[b] (K x N) is read
+// through the read-only path (small, L1/L2 resident).
+
+constexpr int GV_THREADS = 256;
+
+template <typename R, int NC>
+__global__ void __launch_bounds__(GV_THREADS)
+    cgemv_rows_kernel(const __grid_constant__ GemmArgs g, int64_t rows_per_item,
+                      int64_t items_per_b) {
+  using V = typename C2<R>::T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
+  const bool use_beta = (br != R(0) || bi != R(0));
+  for (int64_t item = blockIdx.x; item < g.batch * items_per_b; item += gridDim.x) {
+    const int64_t b = item / items_per_b;
+    const int64_t r0 = (item - b * items_per_b) * rows_per_item;
+    const int64_t r1 = min(g.M, r0 + rows_per_item);
+    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+    V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
+    for (int64_t m = r0 + warp * 4; m < r1; m += (GV_THREADS / 32) * 4) {
+      V acc[4][NC];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[r][c] = V{R(0), R(0)};
+      for (int64_t k = lane; k < g.K; k += 32) {
+        V x[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          x[c] = (g.opB == QF_OP_N) ? __ldg(B + k * g.ldb + c) : __ldg(B + c * g.ldb + k);
+        V a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          a[r] = (m + r < r1) ? __ldg(A + (m + r) * g.lda + k) : V{R(0), R(0)};
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) cfma(acc[r][c], a[r], x[c]);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            acc[r][c].x += __shfl_xor_sync(0xffffffffu, acc[r][c].x, o);
+            acc[r][c].y += __shfl_xor_sync(0xffffffffu, acc[r][c].y, o);
+          }
+      if (lane < 4 * NC) {
+        const int r = lane / NC, c = lane % NC;
+        if (m + r < r1) {
+          V v = acc[0][0];
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc)
+              if (rr == r && cc == c) v = acc[rr][cc];
+          V out;
+          out.x = ar * v.x - ai * v.y;
+          out.y = ar * v.y + ai * v.x;
+          V *cp = C + (m + r) * g.ldc + c;
+          if (use_beta) {
+            const V cv = *cp;
+            out.x += br * cv.x - bi * cv.y;
+            out.y += br * cv.y + bi * cv.x;
+          }
+          *cp = out;
+        }
+      }
+    }
+  }
+}
+
+bool gemv_eligible(const GemmArgs &g) {
+  return g.N <= 4 && g.opA == QF_OP_N && g.K >= 32 && g.M >= 32;
+}
+
+template <typename R, int NC>
+int gemv_launch(const GemmArgs &g, cudaStream_t s) {
+  // ~8 row groups per warp per item; enough items to fill 148 SMs x 8 CTAs
+  const int64_t rows_per_item = std::max<int64_t>(32, std::min<int64_t>(g.M, 256));
+  const int64_t items_per_b = (g.M + rows_per_item - 1) / rows_per_item;
+  const int64_t items = g.batch * items_per_b;
+  const int64_t grid = std::min<int64_t>(items, (int64_t)sm_count() * 8);
+  cgemv_rows_kernel<R, NC><<<(unsigned)grid, GV_THREADS, 0, s>>>(g, rows_per_item, items_per_b);
+  return check_launch("cgemv_rows");
+}
+
+template <typename R>
+int gemm_gemv(const GemmArgs &g, cudaStream_t s) {
+  switch (g.N) {
+    case 1: return gemv_launch<R, 1>(g, s);
+    case 2: return gemv_launch<R, 2>(g, s);
+    case 3: return gemv_launch<R, 3>(g, s);
+    default: return gemv_launch<R, 4>(g, s);
+  }
+}
+
 template <typename R>
 __global__ void cgemm_scale_kernel(const __grid_constant__ GemmArgs g) {
   // K == 0: C = beta * C
@@ -459,6 +561,7 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
                                                                            ws);
     return check_launch("cgemm_skinny_reduce");
   }
+  if (gemv_eligible(g)) return gemm_gemv<R>(g, s);
   if (smallkn_eligible(g)) return gemm_smallkn<R>(g, s);
   int64_t tiles_n = (g.N + TBN - 1) / TBN, tiles_m = (g.M + TBM - 1) / TBM;
   int64_t tiles = tiles_n * tiles_m;

@@ -35,7 +35,8 @@ def _gemm(batch, M, N, K, opA, opB, dt, mode=None, alpha=1.0, beta=0.0, seed=0):
 
 SHAPES = [(1, 64, 64, 64), (3, 100, 37, 70), (2, 4096, 64, 64), (1, 1, 1, 4096),
           (4, 1, 64, 20000), (1, 64, 1, 5000), (1, 257, 129, 33), (5, 7, 5, 3), (1, 8, 8, 0),
-          (1, 512, 512, 256)]
+          (1, 512, 512, 256), (3, 1000, 1, 64), (2, 4096, 3, 100), (1, 77, 4, 33),
+          (16, 4096, 1, 64), (2, 300, 2, 1000)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -92,7 +93,7 @@ TC_SHAPES = [(1, 128, 128, 8), (1, 128, 128, 64), (2, 256, 256, 40), (1, 300, 20
              (1, 2048, 2048, 512)]
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["promoted", "SS", "TS"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["stream", "SS", "TS", "promoted-v2"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -106,7 +107,7 @@ def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
     """3xTF32 keeps ~fp32 accuracy: same 1e-5 bar as the FFMA kernel.  The
     unpromoted v1 variants accumulate all of K in TMEM (error ~1.4e-8 K),
     so they are only held to the bar for K <= 256."""
-    if tc_variant != 0 and shape[3] > 256:
+    if tc_variant in (1, 2) and shape[3] > 256:
         pytest.skip("v1 variants are exercised at short K only")
     err = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3)
     assert err < 1e-5, err
