@@ -1000,6 +1000,298 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
                  "r"(L::TMEM_COLS));
 }
 
+// warp-specialised twin: 8 converter warps + 1 MMA-issue warp, per-stage
+// `full` mbarriers instead of a block barrier per k-block
+template <int STAGES, int CK, int RAW>
+__global__ void __launch_bounds__(V2_THREADS + 32, 1)
+    cgemm_tc3w_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
+  using L = LayoutV3<STAGES, CK, RAW>;
+  constexpr int BN = L::BN;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
+  uint64_t *pbar = bars + STAGES;                                    // [2] chunk done
+  uint64_t *full = pbar + 2;                                         // [STAGES] stage converted
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + STAGES);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int lg = warp & 3, half = warp >> 2;
+  const int row_l = lg * 32 + lane;              // A row / TMEM lane of this thread
+  // B mapping: two threads share one 16-byte core-matrix row segment, so a
+  // 16-lane phase writes 8 rows x 16 B = 128 contiguous bytes (no conflicts)
+  const int b_kp = tid & 1;                      // which k pair inside a 4-k chunk
+  const int b_n = (tid >> 1) & (BN - 1);         // B column (row of B')
+  const int b_chunk = tid >> 7;                  // k 0-3 or 4-7
+  const int b_k = b_chunk * 4 + b_kp * 2;        // first of the thread's two k
+
+  if (tid == 0) {
+    for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], V2_THREADS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+  constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
+  const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 32;
+  const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * 16;
+  const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
+
+  const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+  const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+  float2 *Cb = reinterpret_cast<float2 *>(g.C);
+  const uint32_t nk = (uint32_t)((g.K + KB - 1) / KB);
+  const bool k_tail = (g.K % KB) != 0;
+  const int64_t total_work = tiles * g.batch;
+  const bool a_vec = (g.opA == QF_OP_N) && (g.lda % 2 == 0) && (g.sA % 2 == 0);
+  const bool b_vec = (g.opB == QF_OP_T) && (g.ldb % 2 == 0) && (g.sB % 2 == 0);
+  const int64_t a_kstride = (g.opA == QF_OP_N) ? 1 : g.lda;   // elements between consecutive k
+  const int64_t b_kstride = (g.opB == QF_OP_N) ? g.ldb : 1;
+
+  // ---- fetch cursor: incremental source pointers, set up once per tile
+  int64_t f_work = blockIdx.x;
+  uint32_t f_kb = 0;
+  const float2 *fa = Ab, *fb = Bb;
+  bool fa_ok = false, fb_ok = false;
+  auto fetch_setup = [&]() {
+    if (f_work >= total_work) return;
+    const int64_t bidx = f_work / tiles;
+    const int64_t tile = f_work - bidx * tiles;
+    const int64_t am = (tile / tiles_n) * BM + row_l;
+    const int64_t bn = (tile % tiles_n) * BN + b_n;
+    fa_ok = am < g.M;
+    fb_ok = bn < g.N;
+    const float2 *A = Ab + bidx * g.sA;
+    const float2 *B = Bb + bidx * g.sB;
+    fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+    fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
+    if (!fa_ok) fa = Ab;
+    if (!fb_ok) fb = Bb;
+  };
+  auto fetch = [&](uint32_t slot) {
+    if (f_work < total_work) {
+      const uint32_t da = rawa0 + slot * L::RAWA_SLOT, db = rawb0 + slot * L::RAWB_SLOT;
+      if (!(k_tail && f_kb == nk - 1)) {
+        if (a_vec) {
+          cp_async16(da, fa, fa_ok);
+          cp_async16(da + 16, fa + 2, fa_ok);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cp_async8(da + 8 * k, fa + k * a_kstride, fa_ok);
+        }
+        if (b_vec) {
+          cp_async16(db, fb, fb_ok);
+        } else {
+          cp_async8(db, fb, fb_ok);
+          cp_async8(db + 8, fb + b_kstride, fb_ok);
+        }
+      } else {  // ragged last k-block: per-element predicates
+        const int64_t k0 = (int64_t)f_kb * KB;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool ok = fa_ok && k0 + 4 * half + k < g.K;
+          cp_async8(da + 8 * k, ok ? fa + k * a_kstride : Ab, ok);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = fb_ok && k0 + b_k + e < g.K;
+          cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
+        }
+      }
+      if (fa_ok) fa += KB * a_kstride;
+      if (fb_ok) fb += KB * b_kstride;
+      if (++f_kb == nk) {
+        f_kb = 0;
+        f_work += gridDim.x;
+        fetch_setup();
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // uniform group count
+  };
+
+  if (warp == V2_THREADS / 32) {
+    // ===== MMA issuer: one elected thread walks the same k-block sequence
+    if (lane == 0) {
+      uint32_t qm = 0;
+      for (int64_t work = blockIdx.x; work < total_work; work += gridDim.x) {
+        for (uint32_t kb = 0; kb < nk; ++kb, ++qm) {
+          const uint32_t s = qm & (STAGES - 1);
+          mbar_wait(&full[s], (qm >> L::LOG_STAGES) & 1u);
+          tc_fence_after();
+          const uint32_t pos = kb & (CK - 1);
+          const uint32_t chunk = kb >> L::LOG_CK;
+          const uint32_t d = tmem + (chunk & 1u) * (uint32_t)L::P_COLS;
+          uint8_t *stage = smem + s * L::STAGE;
+          const uint32_t bhi = smem_u32(stage), blo = smem_u32(stage + L::B_PLANE);
+          const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
+          const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
+          const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
+          const uint32_t acc0 = pos > 0 ? 1u : 0u;
+          mma_ts(d, a + 0, b1h, IDESC, acc0);
+          mma_ts(d, a + 0, b1l, IDESC, 1u);
+          mma_ts(d, a + 8, b1h, IDESC, 1u);
+          mma_ts(d, a + 16, b2h, IDESC, 1u);
+          mma_ts(d, a + 16, b2l, IDESC, 1u);
+          mma_ts(d, a + 24, b2h, IDESC, 1u);
+          mma_commit(&bars[s]);
+          if (pos == CK - 1 || kb == nk - 1) mma_commit(&pbar[chunk & 1u]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+  uint32_t q = 0;            // k-blocks consumed by this CTA (drives every ring)
+  uint32_t pwaits[2] = {0, 0};
+  fetch_setup();
+  for (int i = 0; i < RAW - 1; ++i) fetch((uint32_t)i);
+
+  for (int64_t work = blockIdx.x; work < total_work; work += gridDim.x) {
+    const int64_t bidx = work / tiles;
+    const int64_t tile = work - bidx * tiles;
+    const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    float2 *C = Cb + bidx * g.sC;
+    float racc[32], iacc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) racc[j] = iacc[j] = 0.f;
+
+    auto promote = [&](int pb) {
+      mbar_wait(&pbar[pb], pwaits[pb] & 1u);
+      ++pwaits[pb];
+      tc_fence_after();
+      uint32_t v[32];
+      const uint32_t base = tmem + lane_base + (uint32_t)(pb * L::P_COLS + 32 * half);
+      tmem_ld32(base, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j) racc[j] += __uint_as_float(v[j]);
+      tmem_ld32(base + BN, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 32; ++j) iacc[j] += __uint_as_float(v[j]);
+    };
+
+    for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+      fetch((q + RAW - 1) & (RAW - 1));
+      asm volatile("cp.async.wait_group %0;" ::"n"(RAW - 1) : "memory");
+      const uint32_t s = q & (STAGES - 1);
+      if (q >= STAGES) mbar_wait(&bars[s], ((q >> L::LOG_STAGES) + 1) & 1u);
+      const uint32_t slot = q & (RAW - 1);
+      // ---- convert this thread's own bytes
+      const float4 a01 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
+                                                            slot * L::RAWA_SLOT + tid * 32);
+      const float4 a23 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
+                                                            slot * L::RAWA_SLOT + tid * 32 + 16);
+      const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
+                                                           slot * L::RAWB_SLOT + tid * 16);
+      {
+        uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
+        split_fast(bb.x, hr0, lr0);
+        split_fast(bb.y, hi0, li0);
+        split_fast(bb.z, hr1, lr1);
+        split_fast(bb.w, hi1, li1);
+        uint8_t *stage = smem + s * L::STAGE;
+        uint8_t *ph = stage, *pl = stage + L::B_PLANE;
+        *reinterpret_cast<uint2 *>(ph + 0 * L::B_BLOCK + boff) =
+            make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
+        *reinterpret_cast<uint2 *>(ph + 1 * L::B_BLOCK + boff) = make_uint2(hr0, hr1);
+        *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
+        *reinterpret_cast<uint2 *>(pl + 0 * L::B_BLOCK + boff) =
+            make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
+        *reinterpret_cast<uint2 *>(pl + 1 * L::B_BLOCK + boff) = make_uint2(lr0, lr1);
+        *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(li0, li1);
+      }
+      {
+        uint32_t rh[4], rl[4], ih[4], il[4];
+        split_fast(a01.x, rh[0], rl[0]);
+        split_fast(a01.y, ih[0], il[0]);
+        split_fast(a01.z, rh[1], rl[1]);
+        split_fast(a01.w, ih[1], il[1]);
+        split_fast(a23.x, rh[2], rl[2]);
+        split_fast(a23.y, ih[2], il[2]);
+        split_fast(a23.z, rh[3], rl[3]);
+        split_fast(a23.w, ih[3], il[3]);
+        const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32 + 4 * half);
+        tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+        tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+        tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+        tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+      const uint32_t pos = kb & (CK - 1);
+      const uint32_t chunk = kb >> L::LOG_CK;
+      if (pos == 0 && kb > 0) promote((int)((chunk - 1) & 1u));
+    }
+    if (nk > 0) promote((int)(((nk - 1) >> L::LOG_CK) & 1u));
+
+    const int64_t row = m0 + row_l;
+    if (row < g.M) {
+      const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+      const bool use_beta = (br != 0.f || bi != 0.f);
+      const int64_t c0 = n0 + 32 * half;
+      float2 *crow = C + row * g.ldc + c0;
+      const int64_t ncols = min((int64_t)32, g.N - c0);
+      if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && (((uintptr_t)crow) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2)
+          *reinterpret_cast<float4 *>(crow + j) =
+              make_float4(racc[j], iacc[j], racc[j + 1], iacc[j + 1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < ncols) {
+            float2 o = make_float2(ar * racc[j] - ai * iacc[j], ar * iacc[j] + ai * racc[j]);
+            if (use_beta) {
+              const float2 c = crow[j];
+              o.x += br * c.x - bi * c.y;
+              o.y += br * c.y + bi * c.x;
+            }
+            crow[j] = o;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }  // converter warps
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+}
+
+template <int STAGES, int CK, int RAW>
+int launch_ws(const GemmArgs &g, cudaStream_t s) {
+  using L = LayoutV3<STAGES, CK, RAW>;
+  auto kern = cgemm_tc3w_kernel<STAGES, CK, RAW>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) {
+      set_error("tc3w: cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    attr = true;
+  }
+  const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + BM - 1) / BM;
+  const int64_t tiles = tiles_n * tiles_m;
+  const int64_t grid = std::min<int64_t>(tiles * g.batch, (int64_t)sm_count());
+  kern<<<(unsigned)grid, V2_THREADS + 32, L::SMEM, s>>>(g, tiles_n, tiles);
+  return check_launch("cgemm_tc3w");
+}
+
 template <int STAGES, int CK, int RAW>
 int launch_v3(const GemmArgs &g, cudaStream_t s) {
   using L = LayoutV3<STAGES, CK, RAW>;
@@ -1024,7 +1316,8 @@ int launch_v3(const GemmArgs &g, cudaStream_t s) {
 
 // variant: 0 = auto (v3: promoted + cp.async stream), 1 = v1 SS, 2 = v1 TS
 // (v1 accumulates the whole K in TMEM: its error grows ~1.4e-8 * K),
-// 3 = v2 (promoted, register prefetch)
+// 3 = v2 (promoted, register prefetch), 4 = v3 stream (block barrier per
+// k-block); default = warp-specialised stream
 static int g_tc3_variant = 0;
 
 bool tc3_eligible(const GemmArgs &g) {
@@ -1041,7 +1334,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 2)
     return small_n ? tc::launch<64, 6, true>(g, s) : tc::launch<128, 4, true>(g, s);
   if (g_tc3_variant == 3) return tc::launch_v2<6, 4>(g, s);
-  return tc::launch_v3<4, 4, 8>(g, s);
+  if (g_tc3_variant == 4) return tc::launch_v3<4, 4, 8>(g, s);
+  return tc::launch_ws<8, 4, 8>(g, s);
 }
 
 }  // namespace qf
