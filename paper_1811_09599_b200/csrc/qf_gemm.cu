@@ -297,9 +297,142 @@ constexpr int SKN_THREADS = 256;
 constexpr int SKN_MAX = 4096;      // complex entries of B held in smem
 constexpr int SKN_A_MAX = 4096;    // complex entries of the staged A block
 
+__device__ __forceinline__ void skn_cp_async(void *smem_dst, const void *gsrc, int bytes) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+// Pipelined: each CTA owns a contiguous range of work items (batch-major, so
+// B[b] is restaged rarely); the A block of item j+1 streams into the other
+// smem buffer with cp.async while item j is computed and written.
+template <typename R, int NG>
+__global__ void __launch_bounds__(SKN_THREADS)
+    cgemm_smallkn_kernel(const __grid_constant__ GemmArgs g, int rm, int64_t blocks_m,
+                         int apitch, int bpitch, int64_t items_per_cta) {
+  using V = typename C2<R>::T;
+  extern __shared__ __align__(16) unsigned char skn_smem[];
+  const int K = (int)g.K, N = (int)g.N;
+  V *Bs = reinterpret_cast<V *>(skn_smem);
+  V *As0 = Bs + (((size_t)K * bpitch + 1) & ~(size_t)1);
+  V *Asb[2] = {As0, As0 + (size_t)rm * apitch};
+  const int tid = threadIdx.x;
+  const R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
+  const bool use_beta = (br != R(0) || bi != R(0));
+  const int64_t total = g.batch * blocks_m;
+  const int64_t it0 = blockIdx.x * items_per_cta;
+  const int64_t it1 = min(total, it0 + items_per_cta);
+  if (it0 >= it1) return;
+  // 16-byte copies when rows are contiguous K-runs of even length (pairs stay in a row)
+  const bool vec = sizeof(V) == 8 && g.opA == QF_OP_N && (K % 2 == 0) && (g.lda % 2 == 0) &&
+                   (g.sA % 2 == 0) && (apitch % 2 == 0);
+
+  auto issue = [&](int64_t item, int buf) {
+    const int64_t b = item / blocks_m;
+    const int64_t m0 = (item - b * blocks_m) * rm;
+    const int rows = (int)min((int64_t)rm, g.M - m0);
+    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    V *As = Asb[buf];
+    if (vec) {
+      const int pairs = rows * (K / 2);
+      for (int i = tid; i < pairs; i += SKN_THREADS) {
+        const int m = i / (K / 2), k = (i - m * (K / 2)) * 2;
+        skn_cp_async(As + m * apitch + k, A + (m0 + m) * g.lda + k, 16);
+      }
+    } else if (g.opA == QF_OP_N) {
+      for (int i = tid; i < rows * K; i += SKN_THREADS) {
+        const int m = i / K, k = i - m * K;
+        skn_cp_async(As + m * apitch + k, A + (m0 + m) * g.lda + k, sizeof(V));
+      }
+    } else {
+      for (int i = tid; i < rows * K; i += SKN_THREADS) {
+        const int k = i / rows, m = i - k * rows;
+        skn_cp_async(As + m * apitch + k, A + (int64_t)k * g.lda + m0 + m, sizeof(V));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto stage_b = [&](int64_t b) {
+    const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+    for (int i = tid; i < K * N; i += SKN_THREADS) {
+      int k, n;
+      if (g.opB == QF_OP_N) {
+        k = i / N;
+        n = i - k * N;
+        Bs[k * bpitch + n] = B[(int64_t)k * g.ldb + n];
+      } else {
+        n = i / K;
+        k = i - n * K;
+        Bs[k * bpitch + n] = B[(int64_t)n * g.ldb + k];
+      }
+    }
+  };
+
+  int64_t cur_b = it0 / blocks_m;
+  stage_b(cur_b);
+  issue(it0, 0);
+  for (int64_t item = it0; item < it1; ++item) {
+    const int buf = (int)((item - it0) & 1);
+    const int64_t b = item / blocks_m;
+    const int64_t m0 = (item - b * blocks_m) * rm;
+    const int rows = (int)min((int64_t)rm, g.M - m0);
+    if (item + 1 < it1 && (item + 1) / blocks_m == b) {
+      issue(item + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // A block (and B stage) visible to every thread
+    const V *As = Asb[buf];
+    V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
+    // register blocking: a thread computes NG consecutive columns of one row,
+    // reading its A row once; B reads are warp-wide broadcasts
+    const int groups = (N + NG - 1) / NG;
+    for (int o = tid; o < rows * groups; o += SKN_THREADS) {
+      const int m = o / groups, n0 = (o - m * groups) * NG;
+      V acc[NG];
+#pragma unroll
+      for (int j = 0; j < NG; ++j) acc[j] = V{R(0), R(0)};
+      const V *arow = As + m * apitch;
+      const V *bcol = Bs + n0;
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const V a = arow[k];
+#pragma unroll
+        for (int j = 0; j < NG; ++j)
+          if (n0 + j < N) cfma(acc[j], a, bcol[k * bpitch + j]);
+      }
+      V *cp = C + (m0 + m) * g.ldc + n0;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) {
+        if (n0 + j < N) {
+          V out;
+          out.x = ar * acc[j].x - ai * acc[j].y;
+          out.y = ar * acc[j].y + ai * acc[j].x;
+          if (use_beta) {
+            const V c = cp[j];
+            out.x += br * c.x - bi * c.y;
+            out.y += br * c.y + bi * c.x;
+          }
+          cp[j] = out;
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` and Bs free
+    if (item + 1 < it1 && (item + 1) / blocks_m != b) {  // next batch entry: restage B, refill
+      cur_b = (item + 1) / blocks_m;
+      stage_b(cur_b);
+      issue(item + 1, buf ^ 1);
+    }
+  }
+}
+
+// single-buffer twin for short K (<= 16): more CTAs per SM beat pipelining
 template <typename R>
 __global__ void __launch_bounds__(SKN_THREADS)
-    cgemm_smallkn_kernel(const __grid_constant__ GemmArgs g, int rm, int64_t blocks_m) {
+    cgemm_smallkn_simple_kernel(const __grid_constant__ GemmArgs g, int rm, int64_t blocks_m) {
   using V = typename C2<R>::T;
   extern __shared__ __align__(16) unsigned char skn_smem[];
   const int K = (int)g.K, N = (int)g.N;
@@ -508,23 +641,45 @@ bool smallkn_eligible(const GemmArgs &g) {
 }
 
 template <typename R>
-int gemm_smallkn(const GemmArgs &g, cudaStream_t s) {
+int gemm_smallkn_simple(const GemmArgs &g, cudaStream_t s) {
   using V = typename C2<R>::T;
   const int K = (int)g.K, N = (int)g.N;
   const int bpitch = N + ((N % 2 == 0) ? 1 : 0), apitch = K + ((K % 2 == 0) ? 1 : 0);
   int rm = (int)std::min<int64_t>(g.M, std::max(1, SKN_A_MAX / apitch));
-  // enough work items to fill the machine when the batch is small
   int64_t blocks_m = (g.M + rm - 1) / rm;
   size_t smem = ((size_t)K * bpitch + (size_t)rm * apitch) * sizeof(V);
-  static thread_local bool attr[2] = {false, false};
-  auto kern = cgemm_smallkn_kernel<R>;
-  if (!attr[sizeof(R) == 8]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    attr[sizeof(R) == 8] = true;
-  }
+  auto kern = cgemm_smallkn_simple_kernel<R>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   int64_t items = g.batch * blocks_m;
   int64_t grid = std::min<int64_t>(items, (int64_t)sm_count() * 6);
   kern<<<(unsigned)grid, SKN_THREADS, smem, s>>>(g, rm, blocks_m);
+  return check_launch("cgemm_smallkn_simple");
+}
+
+template <typename R>
+int gemm_smallkn(const GemmArgs &g, cudaStream_t s) {
+  using V = typename C2<R>::T;
+  const int K = (int)g.K, N = (int)g.N;
+  if (K <= 16) return gemm_smallkn_simple<R>(g, s);
+  const int bpitch = N + ((N % 2 == 0) ? 1 : 0);
+  const int apitch = (K % 2 == 0) ? K + 2 : K + 1;  // even pitch keeps 16-byte pairs aligned
+  int rm = (int)std::min<int64_t>(g.M, std::max(1, SKN_A_MAX / apitch));
+  const int64_t blocks_m = (g.M + rm - 1) / rm;
+  const size_t smem = ((((size_t)K * bpitch + 1) & ~(size_t)1) + 2 * (size_t)rm * apitch) * sizeof(V);
+  // short K: one output per thread (warp spans a row: A broadcast, B
+  // conflict-free); long K: a thread keeps up to 8 columns of its row so the
+  // A row is read from smem once
+  auto kern = (N < 2) ? cgemm_smallkn_kernel<R, 1>
+              : N >= 8           ? cgemm_smallkn_kernel<R, 8>
+              : N >= 4           ? cgemm_smallkn_kernel<R, 4>
+                                 : cgemm_smallkn_kernel<R, 2>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  const int64_t items = g.batch * blocks_m;
+  const int per_sm = std::max(1, std::min(4, (int)((200 * 1024) / (smem + 2048))));
+  const int64_t grid = std::min<int64_t>(items, (int64_t)sm_count() * per_sm);
+  const int64_t per_cta = (items + grid - 1) / grid;
+  const int64_t grid2 = (items + per_cta - 1) / per_cta;
+  kern<<<(unsigned)grid2, SKN_THREADS, smem, s>>>(g, rm, blocks_m, apitch, bpitch, per_cta);
   return check_launch("cgemm_smallkn");
 }
 

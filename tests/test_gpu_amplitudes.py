@@ -170,3 +170,29 @@ def test_nonzero_input_and_bristlecone72_fold(golden):
         ()))
     net = eng.base_net(0)
     assert sorted(net.tensors) == [s for s in range(72) if s not in (0, 71)]
+
+
+def test_slice_late_is_transparent(golden):
+    """Slice-late execution (cut bonds left open in steps whose cut
+    dependence enters only through their own site tensors) gives the same
+    amplitudes and the same reference flop count as slicing early."""
+    case = next(c for c in golden["amplitudes"] if c["name"] == "config2_c64")
+    circ = qf.parse_circuit(golden["circuits"][case["circuit"]])
+    plan = qf.parse_plan(golden["plans"][case["plan"]])
+    eng = qf.AmplitudeEngine(circ, plan)
+    outs = case["out_bits"][:16]
+    bits = np.array([[int(c) for c in o] for o in outs], dtype=np.int32)
+    net = eng.base_net(0).fix_outputs_batch(bits, tuple(range(circ.n)))
+    res = {}
+    for late in (True, False):
+        ex = qf.PlanExecutor(net, plan, slice_late=late)
+        if late:
+            assert set(ex.late) == {"A", "B"}
+        tot = None
+        for p in qf.enumerate_paths(ex.cut_dims):
+            r = ex.run(p).data.clone()
+            tot = r if tot is None else tot + r
+        res[late] = (tot.cpu().numpy(), ex.flops)
+    assert rel_l2(res[True][0], res[False][0]) < 1e-6
+    assert res[True][1] == res[False][1] == case["flops"]
+    assert rel_l2(res[True][0], golden_amps(case)[:16]) < 1e-4
