@@ -784,7 +784,9 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
   constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
-  const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 32;
+  // A slot = two 16-byte lanes per thread, each lane contiguous across threads,
+  // so the 128-bit accesses of a quarter warp hit 8 distinct bank groups
+  const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 16;
   const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * 16;
   const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
 
@@ -825,10 +827,11 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
       if (!(k_tail && f_kb == nk - 1)) {
         if (a_vec) {
           cp_async16(da, fa, fa_ok);
-          cp_async16(da + 16, fa + 2, fa_ok);
+          cp_async16(da + V2_THREADS * 16, fa + 2, fa_ok);
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) cp_async8(da + 8 * k, fa + k * a_kstride, fa_ok);
+          for (int k = 0; k < 4; ++k)
+            cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, fa + k * a_kstride, fa_ok);
         }
         if (b_vec) {
           cp_async16(db, fb, fb_ok);
@@ -841,7 +844,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const bool ok = fa_ok && k0 + 4 * half + k < g.K;
-          cp_async8(da + 8 * k, ok ? fa + k * a_kstride : Ab, ok);
+          cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -898,9 +901,9 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
       const uint32_t slot = q & (RAW - 1);
       // ---- convert this thread's own bytes
       const float4 a01 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
-                                                            slot * L::RAWA_SLOT + tid * 32);
-      const float4 a23 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
-                                                            slot * L::RAWA_SLOT + tid * 32 + 16);
+                                                            slot * L::RAWA_SLOT + tid * 16);
+      const float4 a23 = *reinterpret_cast<const float4 *>(
+          smem + L::RAWA_OFF + slot * L::RAWA_SLOT + V2_THREADS * 16 + tid * 16);
       const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
                                                            slot * L::RAWB_SLOT + tid * 16);
       {
@@ -1040,7 +1043,9 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
   constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
-  const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 32;
+  // A slot = two 16-byte lanes per thread, each lane contiguous across threads,
+  // so the 128-bit accesses of a quarter warp hit 8 distinct bank groups
+  const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 16;
   const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * 16;
   const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
 
@@ -1081,10 +1086,11 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       if (!(k_tail && f_kb == nk - 1)) {
         if (a_vec) {
           cp_async16(da, fa, fa_ok);
-          cp_async16(da + 16, fa + 2, fa_ok);
+          cp_async16(da + V2_THREADS * 16, fa + 2, fa_ok);
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) cp_async8(da + 8 * k, fa + k * a_kstride, fa_ok);
+          for (int k = 0; k < 4; ++k)
+            cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, fa + k * a_kstride, fa_ok);
         }
         if (b_vec) {
           cp_async16(db, fb, fb_ok);
@@ -1097,7 +1103,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const bool ok = fa_ok && k0 + 4 * half + k < g.K;
-          cp_async8(da + 8 * k, ok ? fa + k * a_kstride : Ab, ok);
+          cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -1236,9 +1242,9 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       const uint32_t slot = q & (RAW - 1);
       // ---- convert this thread's own bytes
       const float4 a01 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
-                                                            slot * L::RAWA_SLOT + tid * 32);
-      const float4 a23 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
-                                                            slot * L::RAWA_SLOT + tid * 32 + 16);
+                                                            slot * L::RAWA_SLOT + tid * 16);
+      const float4 a23 = *reinterpret_cast<const float4 *>(
+          smem + L::RAWA_OFF + slot * L::RAWA_SLOT + V2_THREADS * 16 + tid * 16);
       const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
                                                            slot * L::RAWB_SLOT + tid * 16);
       {
