@@ -29,6 +29,7 @@
 //   alpha/beta and writes interleaved complex64.
 #include <algorithm>
 #include <type_traits>
+#include <utility>
 
 #include "qf_common.cuh"
 
@@ -1388,6 +1389,364 @@ int launch_v3(const GemmArgs &g, cudaStream_t s) {
   return check_launch("cgemm_tc3s");
 }
 
+
+// ---------------------------------------------------------------------------
+// "reg" variant: 8 warps (255-register budget), operands prefetched D
+// k-blocks ahead straight into registers (no raw shared-memory ring: that
+// ring was ~40% of the kernel's shared-memory traffic), per-stage `full`
+// mbarriers, and warp 0's elected lane issues the MMAs after waiting on them.
+
+template <int STAGES, int CK, int D>
+struct LayoutR {
+  static_assert((STAGES & (STAGES - 1)) == 0 && (CK & (CK - 1)) == 0, "powers of two");
+  static constexpr int BN = V2_BN;
+  static constexpr int NP = 2 * BN;
+  static constexpr int B_BLOCK = BN * 32;
+  static constexpr int B_PLANE = 3 * B_BLOCK;
+  static constexpr int STAGE = 2 * B_PLANE;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int SMEM = BAR_OFF + 1024;
+  static constexpr int P_COLS = NP;
+  static constexpr int A_COL0 = 2 * P_COLS;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int LOG_STAGES = STAGES == 2 ? 1 : STAGES == 4 ? 2 : 3;
+  static constexpr int LOG_CK = CK == 1 ? 0 : CK == 2 ? 1 : CK == 4 ? 2 : CK == 8 ? 3 : 4;
+  static_assert(2 * P_COLS + STAGES * 32 <= 512, "TMEM budget");
+};
+
+template <int STAGES, int CK, int D, bool SHORTK>
+__global__ void __launch_bounds__(V2_THREADS, 1)
+    cgemm_tc3r_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
+  using L = LayoutR<STAGES, CK, D>;
+  constexpr int BN = L::BN;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
+  uint64_t *pbar = bars + STAGES;                                    // [2] partial done
+  uint64_t *full = pbar + 2;                                         // [STAGES] converted
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + STAGES);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int lg = warp & 3, half = warp >> 2;
+  const int row_l = lg * 32 + lane;
+  const int b_kp = tid & 1;
+  const int b_n = (tid >> 1) & (BN - 1);
+  const int b_chunk = tid >> 7;
+  const int b_k = b_chunk * 4 + b_kp * 2;
+
+  if (tid == 0) {
+    for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], V2_THREADS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+  constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
+  const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
+
+  const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+  const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+  float2 *Cb = reinterpret_cast<float2 *>(g.C);
+  const uint32_t nk = (uint32_t)((g.K + KB - 1) / KB);
+  const bool k_tail = (g.K % KB) != 0;
+  const int64_t total_work = tiles * g.batch;
+  const bool a_vec = (g.opA == QF_OP_N) && (g.lda % 2 == 0) && (g.sA % 2 == 0);
+  const bool b_vec = (g.opB == QF_OP_T) && (g.ldb % 2 == 0) && (g.sB % 2 == 0);
+  const int64_t a_kstride = (g.opA == QF_OP_N) ? 1 : g.lda;
+  const int64_t b_kstride = (g.opB == QF_OP_N) ? g.ldb : 1;
+
+  // ---- fetch cursor (register prefetch D k-blocks ahead)
+  int64_t f_work = blockIdx.x;
+  uint32_t f_kb = 0;
+  const float2 *fa = Ab, *fb = Bb;
+  bool fa_ok = false, fb_ok = false;
+  auto fetch_setup = [&]() {
+    if (f_work >= total_work) return;
+    const int64_t bidx = f_work / tiles;
+    const int64_t tile = f_work - bidx * tiles;
+    const int64_t am = (tile / tiles_n) * BM + row_l;
+    const int64_t bn = (tile % tiles_n) * BN + b_n;
+    fa_ok = am < g.M;
+    fb_ok = bn < g.N;
+    const float2 *A = Ab + bidx * g.sA;
+    const float2 *B = Bb + bidx * g.sB;
+    fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+    fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
+    if (!fa_ok) fa = Ab;
+    if (!fb_ok) fb = Bb;
+  };
+  float4 ra0[D], ra1[D], rb[D];
+  auto fetch = [&](auto dc) {
+    constexpr int d = decltype(dc)::value;
+    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    ra0[d] = z;
+    ra1[d] = z;
+    rb[d] = z;
+    if (f_work < total_work) {
+      if (!(k_tail && f_kb == nk - 1)) {
+        if (fa_ok) {
+          if (a_vec) {
+            ra0[d] = __ldg(reinterpret_cast<const float4 *>(fa));
+            ra1[d] = __ldg(reinterpret_cast<const float4 *>(fa + 2));
+          } else {
+            const float2 x0 = __ldg(fa), x1 = __ldg(fa + a_kstride), x2 = __ldg(fa + 2 * a_kstride),
+                         x3 = __ldg(fa + 3 * a_kstride);
+            ra0[d] = make_float4(x0.x, x0.y, x1.x, x1.y);
+            ra1[d] = make_float4(x2.x, x2.y, x3.x, x3.y);
+          }
+        }
+        if (fb_ok) {
+          if (b_vec) {
+            rb[d] = __ldg(reinterpret_cast<const float4 *>(fb));
+          } else {
+            const float2 y0 = __ldg(fb), y1 = __ldg(fb + b_kstride);
+            rb[d] = make_float4(y0.x, y0.y, y1.x, y1.y);
+          }
+        }
+      } else {
+        const int64_t k0 = (int64_t)f_kb * KB;
+        float2 x[4] = {}, y[2] = {};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (fa_ok && k0 + 4 * half + k < g.K) x[k] = __ldg(fa + k * a_kstride);
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (fb_ok && k0 + b_k + e < g.K) y[e] = __ldg(fb + e * b_kstride);
+        ra0[d] = make_float4(x[0].x, x[0].y, x[1].x, x[1].y);
+        ra1[d] = make_float4(x[2].x, x[2].y, x[3].x, x[3].y);
+        rb[d] = make_float4(y[0].x, y[0].y, y[1].x, y[1].y);
+      }
+      if (fa_ok) fa += KB * a_kstride;
+      if (fb_ok) fb += KB * b_kstride;
+      if (++f_kb == nk) {
+        f_kb = 0;
+        f_work += gridDim.x;
+        fetch_setup();
+      }
+    }
+  };
+
+  fetch_setup();
+  // prologue: D k-blocks in flight
+  [&]<int... I>(std::integer_sequence<int, I...>) {
+    (fetch(std::integral_constant<int, I>{}), ...);
+  }(std::make_integer_sequence<int, D>{});
+
+  uint32_t q = 0, qm_tile = 0;
+  uint32_t pwaits[2] = {0, 0};
+  const uint32_t nch = (nk + CK - 1) >> L::LOG_CK;
+  uint32_t tcount = 0;
+  bool have_prev = false;
+  int prev_pb = 0;
+  int64_t prev_m0 = 0, prev_n0 = 0;
+  float2 *prev_C = nullptr;
+  float racc[32], iacc[32];
+
+  auto wait_partial = [&](int pb) {
+    mbar_wait(&pbar[pb], pwaits[pb] & 1u);
+    ++pwaits[pb];
+    tc_fence_after();
+  };
+  auto promote = [&](int pb) {
+    wait_partial(pb);
+    uint32_t v[32];
+    const uint32_t base = tmem + lane_base + (uint32_t)(pb * L::P_COLS + 32 * half);
+    tmem_ld32(base, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) racc[j] += __uint_as_float(v[j]);
+    tmem_ld32(base + BN, v);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) iacc[j] += __uint_as_float(v[j]);
+  };
+  auto store_c = [&](int64_t em0, int64_t en0, float2 *eC, const float *xr, const float *xi) {
+    const int64_t row = em0 + row_l;
+    if (row >= g.M) return;
+    const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+    const bool use_beta = (br != 0.f || bi != 0.f);
+    const int64_t c0 = en0 + 32 * half;
+    float2 *crow = eC + row * g.ldc + c0;
+    const int64_t ncols = min((int64_t)32, g.N - c0);
+    if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && (((uintptr_t)crow) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 2)
+        *reinterpret_cast<float4 *>(crow + j) = make_float4(xr[j], xi[j], xr[j + 1], xi[j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < ncols) {
+          float2 o = make_float2(ar * xr[j] - ai * xi[j], ar * xi[j] + ai * xr[j]);
+          if (use_beta) {
+            const float2 c = crow[j];
+            o.x += br * c.x - bi * c.y;
+            o.y += br * c.y + bi * c.x;
+          }
+          crow[j] = o;
+        }
+      }
+    }
+  };
+  auto tmem_epilogue = [&](int pb, int64_t em0, int64_t en0, float2 *eC) {
+    wait_partial(pb);
+    uint32_t vr[32], vi[32];
+    const uint32_t base = tmem + lane_base + (uint32_t)(pb * L::P_COLS + 32 * half);
+    tmem_ld32(base, vr);
+    tmem_ld32(base + BN, vi);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    store_c(em0, en0, eC, reinterpret_cast<const float *>(vr), reinterpret_cast<const float *>(vi));
+    tc_fence_before();
+  };
+
+  // one k-block: convert register buffer d, refill it, signal, maybe issue
+  auto kstep = [&](auto dc, uint32_t kb, uint32_t mma_chunk) {
+    constexpr int d = decltype(dc)::value;
+    const uint32_t s = q & (STAGES - 1);
+    if (q >= STAGES) mbar_wait(&bars[s], ((q >> L::LOG_STAGES) + 1) & 1u);
+    {
+      uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
+      split_fast(rb[d].x, hr0, lr0);
+      split_fast(rb[d].y, hi0, li0);
+      split_fast(rb[d].z, hr1, lr1);
+      split_fast(rb[d].w, hi1, li1);
+      uint8_t *ph = smem + s * L::STAGE, *pl = ph + L::B_PLANE;
+      *reinterpret_cast<uint2 *>(ph + boff) = make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
+      *reinterpret_cast<uint2 *>(ph + L::B_BLOCK + boff) = make_uint2(hr0, hr1);
+      *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
+      *reinterpret_cast<uint2 *>(pl + boff) = make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
+      *reinterpret_cast<uint2 *>(pl + L::B_BLOCK + boff) = make_uint2(lr0, lr1);
+      *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(li0, li1);
+    }
+    {
+      uint32_t rh[4], rl[4], ih[4], il[4];
+      split_fast(ra0[d].x, rh[0], rl[0]);
+      split_fast(ra0[d].y, ih[0], il[0]);
+      split_fast(ra0[d].z, rh[1], rl[1]);
+      split_fast(ra0[d].w, ih[1], il[1]);
+      split_fast(ra1[d].x, rh[2], rl[2]);
+      split_fast(ra1[d].y, ih[2], il[2]);
+      split_fast(ra1[d].z, rh[3], rl[3]);
+      split_fast(ra1[d].w, ih[3], il[3]);
+      const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32 + 4 * half);
+      tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+      tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+      tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+      tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+    }
+    fetch(dc);  // refill this register buffer D k-blocks ahead
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    fence_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+    if (warp == 0) {
+      if (lane == 0) {
+        mbar_wait(&full[s], (q >> L::LOG_STAGES) & 1u);
+        tc_fence_after();
+        const uint32_t pos = SHORTK ? kb : (kb & (CK - 1));
+        const uint32_t d_t = tmem + (mma_chunk & 1u) * (uint32_t)L::P_COLS;
+        const uint32_t bhi = smem_u32(smem + s * L::STAGE), blo = bhi + L::B_PLANE;
+        const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
+        const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
+        const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
+        const uint32_t acc0 = pos > 0 ? 1u : 0u;
+        mma_ts(d_t, a + 0, b1h, IDESC, acc0);
+        mma_ts(d_t, a + 0, b1l, IDESC, 1u);
+        mma_ts(d_t, a + 8, b1h, IDESC, 1u);
+        mma_ts(d_t, a + 16, b2h, IDESC, 1u);
+        mma_ts(d_t, a + 16, b2l, IDESC, 1u);
+        mma_ts(d_t, a + 24, b2h, IDESC, 1u);
+        mma_commit(&bars[s]);
+        if (SHORTK ? kb == nk - 1 : (pos == CK - 1 || kb == nk - 1)) mma_commit(&pbar[mma_chunk & 1u]);
+      }
+      __syncwarp();
+    }
+    ++q;
+  };
+
+  for (int64_t work = blockIdx.x; work < total_work; work += gridDim.x, ++tcount) {
+    const int64_t bidx = work / tiles;
+    const int64_t tile = work - bidx * tiles;
+    const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
+    float2 *C = Cb + bidx * g.sC;
+    if (!SHORTK) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) racc[j] = iacc[j] = 0.f;
+    }
+    uint32_t kb = 0;
+    auto one = [&](auto dc) {
+      const uint32_t chunk = SHORTK ? tcount : (kb >> L::LOG_CK);
+      kstep(dc, kb, chunk);
+      if constexpr (SHORTK) {
+        if (kb == 0 && have_prev) {
+          tmem_epilogue(prev_pb, prev_m0, prev_n0, prev_C);
+          have_prev = false;
+        }
+      } else {
+        if ((kb & (CK - 1)) == 0 && kb > 0) promote((int)(((kb >> L::LOG_CK) - 1) & 1u));
+      }
+      ++kb;
+    };
+    // the register buffer index must be static: walk k-blocks D at a time,
+    // continuing the ring position q (mod D) across tiles
+    while (kb < nk) {
+      [&]<int... I>(std::integer_sequence<int, I...>) {
+        (((q % D) == (uint32_t)I && kb < nk ? (one(std::integral_constant<int, I>{}), 0) : 0), ...);
+      }(std::make_integer_sequence<int, D>{});
+    }
+    if constexpr (SHORTK) {
+      have_prev = nk > 0;
+      prev_pb = (int)(tcount & 1u);
+      prev_m0 = m0;
+      prev_n0 = n0;
+      prev_C = C;
+    } else {
+      if (nk > 0) {
+        promote((int)(((nk - 1) >> L::LOG_CK) & 1u));
+        store_c(m0, n0, C, racc, iacc);
+      }
+    }
+  }
+  if constexpr (SHORTK) {
+    if (have_prev) tmem_epilogue(prev_pb, prev_m0, prev_n0, prev_C);
+  }
+  (void)qm_tile;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+}
+
+template <int STAGES, int CK, int D, bool SHORTK>
+int launch_reg(const GemmArgs &g, cudaStream_t s) {
+  using L = LayoutR<STAGES, CK, D>;
+  auto kern = cgemm_tc3r_kernel<STAGES, CK, D, SHORTK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) {
+      set_error("tc3r: cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    attr = true;
+  }
+  const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + BM - 1) / BM;
+  const int64_t tiles = tiles_n * tiles_m;
+  const int64_t grid = std::min<int64_t>(tiles * g.batch, (int64_t)sm_count());
+  kern<<<(unsigned)grid, V2_THREADS, L::SMEM, s>>>(g, tiles_n, tiles);
+  return check_launch("cgemm_tc3r");
+}
+
 }  // namespace tc
 
 // variant: 0 = auto (v3: promoted + cp.async stream), 1 = v1 SS, 2 = v1 TS
@@ -1411,6 +1770,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return small_n ? tc::launch<64, 6, true>(g, s) : tc::launch<128, 4, true>(g, s);
   if (g_tc3_variant == 3) return tc::launch_v2<6, 4>(g, s);
   if (g_tc3_variant == 4) return tc::launch_v3<4, 4, 8>(g, s);
+  if (g_tc3_variant == 5)
+    return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
   // double-buffered TMEM accumulators with a deferred epilogue
   if (g.K <= 256) return tc::launch_ws<8, 4, 8, true>(g, s);
