@@ -40,17 +40,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-N_BITSTRINGS = 1024
-LATTICE, DEPTH, SEED, N_CUTS = "grid:5x5", "1+24+1", 0, 1
+SEED = 0
+# (lattice, depth, grid_plan n_cuts, bit-strings per step, description, L2 note)
+WORKLOADS = {
+    "config2": ("grid:5x5", "1+24+1", 1, 1024,
+                "config2: grid:5x5 RQC 1+24+1 (bond 8), 1024 bitstrings/rank, grid_plan n_cuts=1 "
+                "(8 slices of dim-8 cut)",
+                "working set > L2 (126 MB): 1024 x 2^18-entry intermediates per step"),
+    "config1": ("grid:4x4", "1+16+1", 0, 64,
+                "config1: grid:4x4 RQC 1+16+1 (bond 4), 64 bitstrings/rank, no cuts",
+                "working set < L2 (launch-bound workload; inputs re-gathered every step)"),
+}
+N_BITSTRINGS = WORKLOADS["config2"][3]
+LATTICE, DEPTH, N_CUTS = WORKLOADS["config2"][:3]
 
 
-def workload_config(shard: str, world: int) -> dict:
-    return {"workload": "config2: grid:5x5 RQC 1+24+1 (bond 8), 1024 bitstrings/rank, "
-                        "grid_plan n_cuts=1 (8 slices of dim-8 cut)",
-            "lattice": LATTICE, "depth": DEPTH, "circuit_seed": SEED, "cuts": N_CUTS,
-            "bitstrings_per_step": N_BITSTRINGS * (world if shard == "bitstrings" else 1),
-            "parallelism": f"{shard}-sharded x{world}",
-            "l2": "working set > L2 (126 MB): 1024 x 2^18-entry intermediates per step"}
+def workload_config(shard: str, world: int, workload: str = "config2") -> dict:
+    lat, depth, cuts, nb, desc, l2 = WORKLOADS[workload]
+    return {"workload": desc, "lattice": lat, "depth": depth, "circuit_seed": SEED, "cuts": cuts,
+            "bitstrings_per_step": nb * (world if shard == "bitstrings" else 1),
+            "parallelism": f"{shard}-sharded x{world}", "l2": l2}
 
 
 def bitstrings(rank: int, n: int, count: int) -> list:
@@ -206,9 +215,16 @@ def peaks() -> dict:
         with open(path) as fh:
             d = json.load(fh)
         d["source"] = "MEASURED_PEAKS.json (measured)"
+    else:
+        d = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+             "source": "B200_PROFILING.md fallback"}
+    tf32 = os.path.join(ROOT, "profiles", "measured_tf32.json")
+    if os.path.exists(tf32):
+        with open(tf32) as fh:
+            d["tf32_tflops"] = json.load(fh)["tf32_tflops"]
         return d
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
-            "source": "B200_PROFILING.md fallback"}
+    d.setdefault("tf32_tflops", d["bf16_tflops"] / 2)
+    return d
 
 
 def run_gpu(args):
@@ -225,6 +241,7 @@ def run_gpu(args):
     if args.gemm:
         qf.set_gemm_mode(args.gemm)
 
+    LATTICE, DEPTH, N_CUTS, N_BITSTRINGS = WORKLOADS[args.workload][:4]
     lat = qf.Lattice.named(LATTICE)
     circ = qf.generate_rqc(lat, DEPTH, SEED)
     plan = qf.grid_plan(lat, n_cuts=N_CUTS)
@@ -240,7 +257,13 @@ def run_gpu(args):
     base = eng.base_net(0)
     bits_dev = bits_host.t().contiguous().to(dev)       # (sites, B): row j = bits of site j
 
+    runner = eng._graph_runner(0, N_BITSTRINGS, qf.FidelitySpec()) if args.graph else None
+
     def step_device():
+        if runner is not None:           # captured plan walk, bits already resident
+            acc = runner.replay_device(bits_dev)
+            qf.reduce_partials(acc, group)
+            return acc
         net = base.fix_outputs_batch_device(bits_dev, tuple(range(circ.n)))
         ex = eng._executor(net)
         paths = qf.FidelitySpec().paths_for(ex.cut_dims)
@@ -248,7 +271,7 @@ def run_gpu(args):
         return acc
 
     def step_e2e():
-        res, _ = eng.amplitudes(0, outs)
+        res, _ = eng.amplitudes(0, outs, graph=args.graph)
         return res
 
     for _ in range(args.warmup):
@@ -266,6 +289,8 @@ def run_gpu(args):
         torch.cuda.synchronize()
     barrier(world)
     launches = _lib.launch_count(reset=True) // max(args.steps, 1)
+    if runner is not None:
+        launches = runner.kernels          # kernels recorded in the replayed graph
     ms = max_over_ranks(start.elapsed_time(end) / args.steps, world, dev)
     amps_per_step = N_BITSTRINGS * (world if shard == "bitstrings" else 1)
     value = amps_per_step / (ms / 1e3)
@@ -286,46 +311,53 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall_ms), world, dev)
     e2e = amps_per_step / (e2e_ms / 1e3)
 
-    # ---- per-kernel profile (one extra, separately timed step) ----
+    # ---- per-kernel profile (one extra, separately timed, eager step) ----
     with tc.KernelTimer() as kt:
-        step_device()
+        net = base.fix_outputs_batch_device(bits_dev, tuple(range(circ.n)))
+        ex = eng._executor(net)
+        eng._sum_paths(ex, qf.FidelitySpec().paths_for(ex.cut_dims), lambda t: t.data,
+                       N_BITSTRINGS)
     kinds = kt.summary()
+    kerns = kt.summary(by_kernel=True)
     stats_flops = qf.estimate_cost(plan, lat, DEPTH).total_flops  # per amplitude
     pk = peaks()
     result = None
     if rank == 0:
-        kern = {}
-        for kind, d in kinds.items():
-            kern[kind] = {"launches": d["launches"], "ms": round(d["ms"], 4),
-                          "share": None, "tflops": d["flops"] / d["ms"] / 1e9 if d["ms"] else None,
-                          "gbs": d["bytes"] / d["ms"] / 1e6 if d["ms"] else None}
+        ops, kern = {}, {}
         total = sum(d["ms"] for d in kinds.values()) or 1.0
-        for kind in kern:
-            kern[kind]["share"] = round(kinds[kind]["ms"] / total, 4)
-        dom = max(kinds, key=lambda k: kinds[k]["ms"])
-        d = kinds[dom]
-        if dom == "gemm":
-            ai = d["flops"] / max(d["bytes"], 1)
-            ridge = pk.get("tf32_tflops", pk["bf16_tflops"] / 2) * 1e12 / (pk["hbm_gbs"] * 1e9)
-        else:
-            ai, ridge = 0.0, 1.0
-        if dom == "gemm" and ai >= ridge:
+        for kind, d in kinds.items():
+            ops[kind] = {"launches": d["launches"], "ms": round(d["ms"], 4),
+                         "share": round(d["ms"] / total, 4)}
+        for name, d in kerns.items():
+            kern[name] = {"launches": d["launches"], "ms": round(d["ms"], 4),
+                          "share": round(d["ms"] / total, 4),
+                          "tflops": round(d["flops"] / d["ms"] / 1e9, 2) if d["ms"] else None,
+                          "gbs": round(d["bytes"] / d["ms"] / 1e6, 1) if d["ms"] else None}
+        dom = max(kerns, key=lambda k: kerns[k]["ms"])   # dominant CUDA kernel of the step
+        d = kerns[dom]
+        tensor_peak = pk["tf32_tflops"] / 3                # 3xTF32 complex ceiling
+        ridge = tensor_peak * 1e12 / (pk["hbm_gbs"] * 1e9)
+        ai = d["flops"] / max(d["bytes"], 1)
+        if d["flops"] and "tc3" in dom and ai >= ridge:
             achieved = d["flops"] / d["ms"] / 1e9
-            peak = pk.get("tf32_tflops", pk["bf16_tflops"] / 2) / 3
+            peak = tensor_peak
             roof = {"bound": "tensor", "unit": "TFLOP/s", "kernel": dom,
-                    "peak_basis": "TF32 dense / 3 (3xTF32 complex)"}
+                    "peak_basis": "cuBLAS TF32 measured (profiles/measured_tf32.json) / 3 (3xTF32)"}
         else:
             achieved = d["bytes"] / d["ms"] / 1e6
             peak = pk["hbm_gbs"]
             roof = {"bound": "hbm", "unit": "GB/s", "kernel": dom,
                     "peak_basis": f"hbm_gbs {pk['source']}"}
-        roof.update({"achieved": round(achieved, 2), "peak": peak,
+        roof.update({"achieved": round(achieved, 2), "peak": round(peak, 1),
                      "frac": round(achieved / peak, 4), "traffic": None,
-                     "algorithmic": f"{dom}: {'8*m*k*n flops' if roof['bound'] == 'tensor' else 'bytes = operands + output (gemm) / 16 B per element (permute)'} per launch, summed over {d['launches']} launches in one step"})
+                     "arithmetic_intensity": round(ai, 2), "ridge": round(ridge, 2),
+                     "algorithmic": (f"{dom}: 8*m*k*n flops and 8*(m*k + k*n + m*n)*batch bytes "
+                                     f"per launch (16 B/element for permutes), summed over "
+                                     f"{d['launches']} launches of one step, / their CUDA-event time")})
         clk = clocks.summary()
         cpu = None
         if not args.no_cpu_baseline:
-            sample = max(8, min(256, int(args.cpu_sample)))
+            sample = max(8, min(len(outs), int(args.cpu_sample)))
             cpu = cpu_oracle_rate(qf.write_circuit(circ), qf.format_plan(plan), outs[:sample],
                                   host_cores())
         result = {
@@ -336,7 +368,8 @@ def run_gpu(args):
             "vs_baseline": None, "dtype": "c64 (fp32 complex; 3xTF32 on tensor cores)",
             "data": "synthetic (seeded RQC + seeded bit-strings; the paper's circuit files are "
                     "not in the container)",
-            "config": workload_config(shard, world),
+            "config": workload_config(shard, world, args.workload),
+            "cuda_graph": bool(args.graph),
             "sustained_tflops": round(amps_per_step * stats_flops / (ms / 1e3) / 1e12, 3),
             "flops_per_amplitude": stats_flops,
             "gemm_mode": qf.get_gemm_mode(),
@@ -344,7 +377,7 @@ def run_gpu(args):
                     "h2d_bytes_per_step": int(bits_host.numel() * 4),
                     "d2h_bytes_per_step": int(amps_per_step // world * 8),
                     "api": "AmplitudeEngine.amplitudes(0, host bit-strings) -> host ndarray"},
-            "roofline": roof, "kernels": kern, "gpu_launches": int(launches),
+            "roofline": roof, "kernels": kern, "ops": ops, "gpu_launches": int(launches),
             "clocks": clk, "cpu_baseline": cpu,
         }
     barrier(world)
@@ -443,6 +476,83 @@ def run_permute(args):
             "per_size": per_size, "gpu_launches": int(launches)}
 
 
+def run_fulldepth(args):
+    """Configs 4 and 5 at full depth: time `--paths` paths of one unit (an
+    amplitude for config 4, a 64-amplitude batch for config 5) through the
+    engine's executor and project the unit time over all selected paths
+    (labelled as a projection).  Slices are independent, so N GPUs divide
+    the path list (slices.py)."""
+    import torch
+
+    import paper_1811_09599_b200 as qf
+    from paper_1811_09599_b200 import _lib
+    from paper_1811_09599_b200.network_builder import out_label
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if args.workload == "config4":
+        lat = qf.Lattice.named("grid:7x7")
+        circ = qf.generate_rqc(lat, "1+40+1", SEED)
+        plan, fid, c_sites = qf.load_plan("grid:7x7"), qf.FidelitySpec(1 / 64, SEED), ()
+        rng = np.random.Generator(np.random.PCG64(SEED))
+        out = format(int(rng.integers(0, 2 ** 49)), "049b")
+        fixed = {q: int(b) for q, b in enumerate(out)}
+        units, desc = 1, "config4: grid:7x7 RQC 1+40+1 (bond 32), slice-first plan (cuts right 19:26, bottom 37:38; 1024 slices), f=1/64 (16 paths), 1 bitstring"
+    else:
+        lat = qf.Lattice.named("bristlecone-70")
+        circ = qf.generate_rqc(lat, "1+32+1", SEED)
+        plan, fid = qf.load_plan("bristlecone-70"), qf.FidelitySpec(0.005, SEED)
+        c_sites = tuple(sorted(plan.batch_sites[:6]))
+        rng = np.random.Generator(np.random.PCG64(SEED))
+        s_ab = "".join(str(int(b)) for b in rng.integers(0, 2, size=70))
+        fixed = {q: int(s_ab[q]) for q in range(70) if q not in c_sites}
+        units, desc = 64, "config5: bristlecone-70 RQC 1+32+1 (bond 16), slice-first plan (4 cuts, 65536 slices), f=0.005 (328 paths), 6 open qubits (64 amplitudes/batch)"
+    eng = qf.AmplitudeEngine(circ, plan, device=local)
+    net = eng.base_net(0).fix_outputs(fixed)
+    ex = eng._executor(net)
+    paths = fid.paths_for(ex.cut_dims)
+    mine = qf.SliceShard(rank, world).take(paths)
+    order = tuple(out_label(q) for q in c_sites)
+    times, flops = [], []
+    _lib.launch_count(reset=True)
+    for p in mine[: max(2, args.paths)]:
+        f0 = ex.flops
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        t = ex.run(p)
+        if order:
+            t = t.transpose_to(order)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b) / 1e3)
+        flops.append(ex.flops - f0)
+    launches = _lib.launch_count(reset=True) // max(1, len(times))
+    steady = float(np.mean(times[1:])) if len(times) > 1 else times[0]
+    unit_s = times[0] + steady * (len(mine) - 1)          # this rank's share
+    unit_s = max_over_ranks(unit_s, world, torch.device("cuda", local))
+    rate = units / unit_s
+    exec_tf = sum(flops[1:]) / sum(times[1:]) / 1e12 if len(times) > 1 else flops[0] / times[0] / 1e12
+    pk = peaks()
+    tf32 = pk.get("tf32_tflops", 718.5)
+    if rank != 0:
+        return None
+    return {"metric": "amplitudes/s (projected from timed paths)", "value": round(rate, 5),
+            "unit": "amplitudes/s", "n_gpus": world, "steps": len(times), "warmup": 0,
+            "ms_per_step": round(steady * 1e3, 2), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c64 (3xTF32 tensor cores)",
+            "data": "synthetic seeded circuit", "config": {"workload": desc,
+                                                            "paths_selected": len(paths),
+                                                            "paths_this_rank": len(mine),
+                                                            "paths_timed": len(times)},
+            "projection": "unit time = first path + mean(timed later paths) x (paths on this rank - 1)",
+            "executed_tflops": round(exec_tf, 1),
+            "roofline": {"bound": "tensor", "unit": "TFLOP/s", "kernel": "contraction path (GEMM-dominated)",
+                         "achieved": round(exec_tf, 1), "peak": round(tf32 / 3, 1),
+                         "frac": round(exec_tf / (tf32 / 3), 4), "traffic": None,
+                         "peak_basis": "cuBLAS TF32 measured 718.5 TFLOP/s / 3 (3xTF32)"},
+            "gpu_launches": int(launches)}
+
+
 def run_reference(args):
     """The reference algorithm on the host cores (oracle port), same metric."""
     rank, world, _ = dist_env()
@@ -450,6 +560,8 @@ def run_reference(args):
         return None
     sys.path.insert(0, ROOT)
     import paper_1811_09599_b200 as qf  # host-side circuit/plan text only
+    wl = args.workload if args.workload in WORKLOADS else "config2"
+    LATTICE, DEPTH, N_CUTS, N_BITSTRINGS = WORKLOADS[wl][:4]
     lat = qf.Lattice.named(LATTICE)
     circ = qf.generate_rqc(lat, DEPTH, SEED)
     plan = qf.grid_plan(lat, n_cuts=N_CUTS)
@@ -470,7 +582,7 @@ def run_reference(args):
             "ms_per_step": round(secs / len(rates) * 1e3, 2), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c64",
             "data": "synthetic (seeded RQC + seeded bit-strings)",
-            "config": workload_config("bitstrings", 1),
+            "config": workload_config("bitstrings", 1, wl),
             "cpu_baseline": cpu,
             "e2e": {"value": round(value, 3), "unit": "amplitudes/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -486,8 +598,13 @@ def main(argv=None):
     ap.add_argument("--gemm", choices=["auto", "ffma", "tc3"], default=None)
     ap.add_argument("--cpu-sample", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["config2", "permute"], default="config2",
-                    help="config2 = headline (BASELINE configs[1]); permute = config 3")
+    ap.add_argument("--workload", choices=["config2", "config1", "permute", "config4", "config5"],
+                    default="config2",
+                    help="config2 = headline (BASELINE configs[1]); config1; permute = config 3; "
+                         "config4/config5 = full-depth bounded-path runs")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the plan walk eagerly instead of replaying a captured CUDA graph")
+    ap.add_argument("--paths", type=int, default=4, help="paths timed for config4/config5")
     ap.add_argument("--perm-sizes", default="24,28,30")
     ap.add_argument("--perms", type=int, default=64)
     args = ap.parse_args(argv)
@@ -496,6 +613,8 @@ def main(argv=None):
         args.warmup = 3
     if args.workload == "permute" and args.impl != "reference":
         out = run_permute(args)
+    elif args.workload in ("config4", "config5") and args.impl != "reference":
+        out = run_fulldepth(args)
     else:
         out = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if out is not None:

@@ -130,6 +130,10 @@ int qf_workspace_release(void);
  * Returns the previous setting. */
 int qf_tc3_set_variant(int variant);
 
+/* Name of the last kernel this library launched on the calling thread
+ * (static string; "" if none) -- lets profilers attribute timings. */
+const char *qf_last_kernel(void);
+
 /* Number of kernels this library launched on the calling thread since the
  * last reset (for the bench's gpu_launches claim). */
 int64_t qf_launch_count(int reset);

@@ -22,8 +22,9 @@ from .contraction_plan import (ContractionPlan, CostEstimate, CutSpec, ContractS
                                two_region_plan)
 from .network_builder import Net2D, Net3D, build_3d, contract_grid, contract_time, gate_tensor
 from .slices import SliceShard, current_shard, reduce_partials, shard_range
-from .tensor_core import (PermutePlan, Tensor, contract, get_gemm_mode, permute_fast,
-                          permute_naive, plan_permutation, set_gemm_mode)
+from .tensor_core import (PermutePlan, Tensor, benchmark_csv, benchmark_permute, contract,
+                          get_gemm_mode, permute_fast, permute_naive, plan_permutation,
+                          set_gemm_mode)
 
 __version__ = "0.1.0"
 
@@ -32,7 +33,7 @@ __all__ = [
     "cz_cut_count", "edge_activations", "generate_rqc", "parse_circuit", "pattern_bonds",
     "write_circuit",
     "Tensor", "PermutePlan", "plan_permutation", "permute_fast", "permute_naive", "contract",
-    "set_gemm_mode", "get_gemm_mode",
+    "set_gemm_mode", "get_gemm_mode", "benchmark_permute", "benchmark_csv",
     "Net2D", "Net3D", "build_3d", "contract_time", "contract_grid", "gate_tensor",
     "ContractionPlan", "CutSpec", "ContractStep", "PlanError", "MemoryBudgetError",
     "PlanExecutor", "CostEstimate", "parse_plan", "format_plan", "builtin_plan", "grid_plan",

@@ -30,7 +30,7 @@ OP_N, OP_T = 0, 1
 EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_info", "qf_permute", "qf_permute_c64",
     "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_zgemm_c128", "qf_accumulate",
-    "qf_fill_zero", "qf_tc3_set_variant",
+    "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
     "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
 )
 
@@ -81,12 +81,14 @@ def _declare(lib):
     lib.qf_accumulate.argtypes = [_c_void_p, _c_void_p, _i64, ctypes.c_int, _c_void_p]
     lib.qf_fill_zero.argtypes = [_c_void_p, _i64, _c_void_p]
     lib.qf_tc3_set_variant.argtypes = [ctypes.c_int]
+    lib.qf_last_kernel.restype = ctypes.c_char_p
+    lib.qf_last_kernel.argtypes = []
     lib.qf_workspace_reserve.argtypes = [_i64, _c_void_p]
     lib.qf_workspace_release.argtypes = []
     lib.qf_launch_count.argtypes = [ctypes.c_int]
     lib.qf_launch_count.restype = _i64
     for name in EXPORTS:
-        if name not in ("qf_last_error", "qf_launch_count"):
+        if name not in ("qf_last_error", "qf_launch_count", "qf_last_kernel"):
             getattr(lib, name).restype = ctypes.c_int
     return lib
 

@@ -138,16 +138,20 @@ class AmplitudeEngine:
 
     # -- path sums ----------------------------------------------------------
 
-    def _sum_paths(self, ex: PlanExecutor, paths, finish, size: int):
-        """Sum finish(ex.run(p)) (a flat device buffer of `size` entries)
-        over this rank's share of `paths`; all-reduce across ranks."""
+    def _sum_paths_local(self, ex: PlanExecutor, paths, finish, size: int):
+        """Sum finish(ex.run(p)) over this rank's share of `paths` (device
+        work only -- capturable in a CUDA graph)."""
         shard = slices.current_shard(self.group)
-        mine = shard.take(paths)
         acc = device_buffer(size, torch.complex64 if self.dtype == np.complex64
                             else torch.complex128)
         zero_buffer(acc)
-        for p in mine:
+        for p in shard.take(paths):
             accumulate_buffer(finish(ex.run(p)), acc, size)
+        return acc
+
+    def _sum_paths(self, ex: PlanExecutor, paths, finish, size: int):
+        """Local path sum, then one all-reduce of the partial amplitudes."""
+        acc = self._sum_paths_local(ex, paths, finish, size)
         slices.reduce_partials(acc, self.group)
         flops = slices.reduce_int(ex.flops, self.group, acc.device)
         return acc[:size], flops
@@ -166,11 +170,13 @@ class AmplitudeEngine:
 
     def amplitudes(self, in_bits: Union[str, int], out_bits: Sequence,
                    fidelity: FidelitySpec = FidelitySpec(), *,
-                   chunk: Optional[int] = None) -> tuple:
+                   chunk: Optional[int] = None, graph: bool = False) -> tuple:
         """Many amplitudes at once; returns (ndarray, PathStats per amplitude).
 
         Bit-strings ride as the '@b' GEMM batch axis through one plan walk
-        per chunk (default: all of them)."""
+        per chunk (default: all of them).  With graph=True the plan walk for
+        this (input, chunk size, fidelity) is captured once as a CUDA graph
+        and replayed for every later chunk of the same size."""
         n = self.circuit.n
         outs = [_bits_str(o, n) for o in out_bits]
         bits = np.array([[int(c) for c in o] for o in outs], dtype=np.int32).reshape(len(outs), n)
@@ -181,6 +187,11 @@ class AmplitudeEngine:
             base = self.base_net(in_bits)
             for lo in range(0, len(outs), chunk):
                 part = bits[lo:lo + chunk]
+                if graph:
+                    runner = self._graph_runner(in_bits, len(part), fidelity)
+                    result[lo:lo + len(part)] = runner(part)
+                    stats = runner.stats
+                    continue
                 net = base.fix_outputs_batch(part, tuple(range(n)))
                 ex = self._executor(net)
                 paths = fidelity.paths_for(ex.cut_dims)
@@ -188,6 +199,13 @@ class AmplitudeEngine:
                 result[lo:lo + len(part)] = acc.cpu().numpy()
                 stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
         return result, stats
+
+    def _graph_runner(self, in_bits, batch: int, fidelity: FidelitySpec) -> "_GraphRunner":
+        key = (_bits_str(in_bits, self.circuit.n), batch, fidelity.f, fidelity.seed)
+        cache = self.__dict__.setdefault("_graphs", {})
+        if key not in cache:
+            cache[key] = _GraphRunner(self, key[0], batch, fidelity)
+        return cache[key]
 
     def amplitude_batch(self, in_bits: Union[str, int], s_ab: Union[str, int],
                         c_sites: Sequence[int], n_c: int, *, seed: int = 0,
@@ -246,6 +264,59 @@ class AmplitudeEngine:
             acc, _ = self._sum_paths(ex, paths, lambda t: t.transpose_to(order).data,
                                      2 ** self.circuit.n)
             return acc.cpu().numpy()
+
+
+class _GraphRunner:
+    """One captured plan walk for a fixed (input, batch size, fidelity).
+
+    The bit-string matrix lives in a static device buffer (filled from a
+    pinned host buffer per call), the whole path loop -- slicing gathers,
+    permutations, GEMMs, path accumulation -- replays as one CUDA graph, and
+    the partial amplitudes are all-reduced across ranks outside the graph."""
+
+    def __init__(self, eng: "AmplitudeEngine", in_bits: str, batch: int, fidelity: FidelitySpec):
+        self.eng, self.batch = eng, batch
+        n = eng.circuit.n
+        dev = eng._torch_device()
+        self.bits_t = torch.zeros((n, batch), dtype=torch.int32, device=dev)
+        self.host = torch.zeros((n, batch), dtype=torch.int32).pin_memory()
+        base = eng.base_net(in_bits)
+
+        def body():
+            net = base.fix_outputs_batch_device(self.bits_t, tuple(range(n)))
+            ex = eng._executor(net)
+            paths = fidelity.paths_for(ex.cut_dims)
+            return eng._sum_paths_local(ex, paths, lambda t: t.data, batch), ex, paths
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):   # warm-up: plan tables, workspaces, allocator pool
+            body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        from . import _lib
+        before = _lib.launch_count()
+        with torch.cuda.graph(self.graph):
+            self.acc, ex, paths = body()
+        self.kernels = _lib.launch_count() - before   # library kernels per replay
+        flops = slices.reduce_int(ex.flops, eng.group, self.acc.device)
+        self.stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
+
+    def replay_device(self, bits_t=None):
+        """Replay with bits already on the device (or the current buffer)."""
+        if bits_t is not None:
+            self.bits_t.copy_(bits_t, non_blocking=True)
+        self.graph.replay()
+        return self.acc
+
+    def __call__(self, bits: np.ndarray) -> np.ndarray:
+        self.host.copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(bits, np.int32).T)))
+        self.bits_t.copy_(self.host, non_blocking=True)
+        self.graph.replay()
+        out = self.acc[: self.batch].clone()
+        slices.reduce_partials(out, self.eng.group)
+        return out.cpu().numpy()
 
 
 def mixed_state_samples(circuit: Circuit, f: float, count: int, seed: int = 0) -> np.ndarray:

@@ -10,6 +10,7 @@ namespace qf {
 
 static thread_local std::string g_err;
 static thread_local int64_t g_launches = 0;
+static thread_local const char *g_last_kernel = "";
 
 void set_error(const char *fmt, ...) {
   char buf[1024];
@@ -29,6 +30,7 @@ int check_launch(const char *what) {
     return QF_ERR_CUDA;
   }
   count_launch();
+  g_last_kernel = what;
   return QF_OK;
 }
 
@@ -139,6 +141,8 @@ static int gather_impl(const void *src, void *dst, int64_t outer, int64_t dim, i
 extern "C" {
 
 const char *qf_last_error(void) { return qf::g_err.c_str(); }
+
+const char *qf_last_kernel(void) { return qf::g_last_kernel; }
 
 int qf_version(void) { return 100; }
 

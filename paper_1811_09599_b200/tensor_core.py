@@ -105,11 +105,14 @@ class KernelTimer:
         _timer = self._prev
         return False
 
-    def summary(self, detail: bool = False) -> dict:
+    def summary(self, detail: bool = False, by_kernel: bool = False) -> dict:
         torch.cuda.synchronize()
         out: dict = {}
         for kind, a, b, flops, nbytes, *rest in self.records:
-            key = f"{kind} {rest[0]}" if detail and rest and rest[0] else kind
+            if by_kernel:
+                key = rest[1] if len(rest) > 1 and rest[1] else kind
+            else:
+                key = f"{kind} {rest[0]}" if detail and rest and rest[0] else kind
             d = out.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0, "bytes": 0})
             d["launches"] += 1
             d["ms"] += a.elapsed_time(b)
@@ -137,7 +140,9 @@ class _timed:
         if _timer is not None:
             end = torch.cuda.Event(enable_timing=True)
             end.record()
-            _timer.records.append((self.kind, self.ev, end, self.flops, self.nbytes, self.detail))
+            kern = _lib.load().qf_last_kernel().decode()
+            _timer.records.append((self.kind, self.ev, end, self.flops, self.nbytes, self.detail,
+                                   kern))
         return False
 
 
@@ -485,3 +490,68 @@ def permute_naive(array, perm: Sequence[int]):
     """Same result as the reference's numpy transpose, computed by K1."""
     shape = tuple(array.shape)
     return permute_fast(array, plan_permutation(shape, perm))
+
+
+# ---------------------------------------------------------------------------
+# permutation micro-benchmark (reference: rq/tensor_core.py:427-511)
+
+
+def _random_perm(rng, k: int, fix_prefix: int = 0, fix_suffix: int = 0) -> tuple:
+    """Random non-identity permutation fixing the given prefix/suffix
+    (same draw sequence as the reference's benchmark)."""
+    body = list(range(fix_prefix, k - fix_suffix))
+    while True:
+        mixed = [int(v) for v in rng.permutation(body)]
+        if mixed != body:
+            return tuple(range(fix_prefix)) + tuple(mixed) + tuple(range(k - fix_suffix, k))
+
+
+def benchmark_permute(rank: int = 20, gammas=range(5, 11), thread_counts=(1,), repeats: int = 7,
+                      dtype=np.complex64, compare_backends: bool = False, seed: int = 0) -> list:
+    """Device-timed twin of the reference's benchmark_permute: per gamma an
+    "L move" (leading axes permuted, trailing gamma fixed), an "R move"
+    (trailing gamma permuted) and a "naive" full permutation of a binary
+    rank-`rank` tensor, with the same seeded permutations.  Rows keep the
+    reference schema (op, rank, gamma, threads, median_ns, p10_ns, p90_ns);
+    every op is one K1 launch, timed with CUDA events after a warm-up, and
+    `threads` is echoed only for schema compatibility."""
+    _require_cuda()
+    rng = np.random.Generator(np.random.PCG64(seed))
+    x = (rng.standard_normal(1 << rank) + 1j * rng.standard_normal(1 << rank)).astype(dtype)
+    src = torch.from_numpy(x).cuda()
+    dst = torch.empty_like(src)
+    dims = (2,) * rank
+
+    def time_ns(perm):
+        permute_buffer(src, dims, perm, out=dst)  # warm: plan + tables
+        samples = []
+        for _ in range(repeats):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            permute_buffer(src, dims, perm, out=dst)
+            b.record()
+            torch.cuda.synchronize()
+            samples.append(a.elapsed_time(b) * 1e6)
+        arr = np.array(samples)
+        return float(np.median(arr)), float(np.percentile(arr, 10)), float(np.percentile(arr, 90))
+
+    rows = []
+    for gamma in gammas:
+        perm_l = _random_perm(rng, rank, fix_suffix=gamma)
+        perm_r = _random_perm(rng, rank, fix_prefix=rank - gamma)
+        for name, perm in (("lmove", perm_l), ("rmove", perm_r)):
+            med, p10, p90 = time_ns(perm)
+            for threads in thread_counts:
+                op = f"{name}/b200" if compare_backends else name
+                rows.append({"op": op, "rank": rank, "gamma": gamma, "threads": threads,
+                             "median_ns": med, "p10_ns": p10, "p90_ns": p90})
+        perm_full = _random_perm(rng, rank)
+        med, p10, p90 = time_ns(perm_full)
+        rows.append({"op": "naive", "rank": rank, "gamma": gamma, "threads": 1,
+                     "median_ns": med, "p10_ns": p10, "p90_ns": p90})
+    return rows
+
+
+def benchmark_csv(rows: list) -> str:
+    header = ["op", "rank", "gamma", "threads", "median_ns", "p10_ns", "p90_ns"]
+    return "\n".join([",".join(header)] + [",".join(str(r[h]) for h in header) for r in rows]) + "\n"

@@ -196,3 +196,20 @@ def test_slice_late_is_transparent(golden):
     assert rel_l2(res[True][0], res[False][0]) < 1e-6
     assert res[True][1] == res[False][1] == case["flops"]
     assert rel_l2(res[True][0], golden_amps(case)[:16]) < 1e-4
+
+
+@pytest.mark.parametrize("name", ["config1_c64", "config2_c64", "g4x4s3_cuts2_f025_c64"])
+def test_cuda_graph_replay_matches_eager(golden, name):
+    case = next(c for c in golden["amplitudes"] if c["name"] == name)
+    eng = _engine(golden, case)
+    fid = qf.FidelitySpec(case["f"], case["fseed"])
+    outs = case["out_bits"]
+    eager, st_e = eng.amplitudes(case["in_bits"], outs, fid)
+    for _ in range(2):  # capture once, then replay with new bits each call
+        g1, st_g = eng.amplitudes(case["in_bits"], outs, fid, graph=True)
+        assert rel_l2(g1, eager) < 1e-6
+        assert (st_g.flops, st_g.paths_used) == (st_e.flops, st_e.paths_used)
+    rev = list(reversed(outs))
+    g2, _ = eng.amplitudes(case["in_bits"], rev, fid, graph=True)
+    assert rel_l2(g2, eager[::-1]) < 1e-6
+    assert rel_l2(g1, golden_amps(case)) < 1e-4

@@ -117,3 +117,12 @@ def test_reference_api_shims():
     assert tc.permute_naive(x, perm).tobytes() == O.permute_naive(x, perm).tobytes()
     with pytest.raises(ValueError):
         tc.plan_permutation([2, 2], [0, 0])
+
+
+def test_benchmark_permute_schema_and_perms():
+    rows = tc.benchmark_permute(rank=16, gammas=range(5, 7), repeats=3)
+    assert [r["op"] for r in rows] == ["lmove", "rmove", "naive"] * 2
+    assert all(r["median_ns"] > 0 and r["p10_ns"] <= r["p90_ns"] for r in rows)
+    csv = tc.benchmark_csv(rows)
+    assert csv.splitlines()[0] == "op,rank,gamma,threads,median_ns,p10_ns,p90_ns"
+    assert len(csv.splitlines()) == 7
