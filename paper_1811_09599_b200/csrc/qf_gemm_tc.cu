@@ -1747,6 +1747,376 @@ int launch_reg(const GemmArgs &g, cudaStream_t s) {
   return check_launch("cgemm_tc3r");
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs computes a 256 x 64
+// complex tile with M=256 MMAs issued by the leader.  Each CTA keeps its 128
+// A rows in its own TMEM and HALF of every B' window in its own smem (CTA0:
+// Br and -Bi, CTA1: Bi and Br at the same offsets, so the pair's windows are
+// [Br|Bi] and [-Bi|Br]), which halves each SM's B conversion and the tensor
+// core's shared-memory reads.  Converters of both CTAs arrive on the leader's
+// `full` barrier; MMA completions multicast to both CTAs' barriers.
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ts2(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit2(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int STAGES, int CK, int RAW>
+struct LayoutP2 {
+  static constexpr int BN = V2_BN;
+  static constexpr int NP = 2 * BN;                 // 128: the pair's MMA N
+  static constexpr int B_BLOCK = BN * 32;           // one BN-row tf32 block
+  static constexpr int STAGE = 4 * B_BLOCK;         // (X, Y) x (hi, lo)
+  static constexpr int RAWA_SLOT = V2_THREADS * 32;
+  static constexpr int RAWB_SLOT = V2_THREADS * 16;
+  static constexpr int RAWA_OFF = STAGES * STAGE;
+  static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
+  static constexpr int BAR_OFF = RAWB_OFF + RAW * RAWB_SLOT;
+  static constexpr int SMEM = BAR_OFF + 1024;
+  static constexpr int P_COLS = NP;                 // accumulator columns per partial
+  static constexpr int A_COL0 = 2 * P_COLS;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int LOG_STAGES = STAGES == 2 ? 1 : STAGES == 4 ? 2 : 3;
+  static constexpr int LOG_CK = CK == 1 ? 0 : CK == 2 ? 1 : CK == 4 ? 2 : CK == 8 ? 3 : 4;
+  static_assert(2 * P_COLS + STAGES * 32 <= 512, "TMEM budget");
+};
+
+template <int STAGES, int CK, int RAW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS + 32, 1)
+    cgemm_tc3pair_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
+  using L = LayoutP2<STAGES, CK, RAW>;
+  constexpr int BN = L::BN;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
+  uint64_t *pbar = bars + STAGES;                                    // [2] partial done
+  uint64_t *full = pbar + 2;                                         // [STAGES] (leader) converted
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + STAGES);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int lg = warp & 3, half = warp >> 2;
+  const int row_l = lg * 32 + lane;
+  const int b_kp = tid & 1;
+  const int b_n = (tid >> 1) & (BN - 1);
+  const int b_chunk = tid >> 7;
+  const int b_k = b_chunk * 4 + b_kp * 2;
+  const uint32_t crank = cluster_rank();
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (tid == 0) {
+    for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], 2 * (V2_THREADS / 32));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits + TMEM allocation visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+  constexpr uint32_t IDESC = idesc_tf32(2 * BM, L::NP);
+  const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 16;
+  const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * 16;
+  const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
+
+  const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+  const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+  float2 *Cb = reinterpret_cast<float2 *>(g.C);
+  const uint32_t nk = (uint32_t)((g.K + KB - 1) / KB);
+  const bool k_tail = (g.K % KB) != 0;
+  const int64_t total_work = tiles * g.batch;   // 256 x BN tiles
+  const bool a_vec = (g.opA == QF_OP_N) && (g.lda % 2 == 0) && (g.sA % 2 == 0);
+  const bool b_vec = (g.opB == QF_OP_T) && (g.ldb % 2 == 0) && (g.sB % 2 == 0);
+  const int64_t a_kstride = (g.opA == QF_OP_N) ? 1 : g.lda;
+  const int64_t b_kstride = (g.opB == QF_OP_N) ? g.ldb : 1;
+
+  if (warp == V2_THREADS / 32) {
+    // ===== MMA issuer (leader CTA only)
+    if (crank == 0 && lane == 0) {
+      uint32_t qm = 0;
+      for (int64_t work = pair; work < total_work; work += npairs) {
+        for (uint32_t kb = 0; kb < nk; ++kb, ++qm) {
+          const uint32_t s = qm & (STAGES - 1);
+          mbar_wait(&full[s], (qm >> L::LOG_STAGES) & 1u);
+          tc_fence_after();
+          const uint32_t pos = kb & (CK - 1);
+          const uint32_t chunk = kb >> L::LOG_CK;
+          const uint32_t d = tmem + (chunk & 1u) * (uint32_t)L::P_COLS;
+          const uint32_t st = smem_u32(smem + s * L::STAGE);
+          // stage layout: [X_hi | Y_hi | X_lo | Y_lo]; X = window [Br|Bi], Y = [-Bi|Br]
+          const uint64_t xh = smem_desc(st), yh = smem_desc(st + L::B_BLOCK);
+          const uint64_t xl = smem_desc(st + 2 * L::B_BLOCK), yl = smem_desc(st + 3 * L::B_BLOCK);
+          const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
+          const uint32_t acc0 = pos > 0 ? 1u : 0u;
+          mma_ts2(d, a + 0, xh, IDESC, acc0);
+          mma_ts2(d, a + 0, xl, IDESC, 1u);
+          mma_ts2(d, a + 8, xh, IDESC, 1u);
+          mma_ts2(d, a + 16, yh, IDESC, 1u);
+          mma_ts2(d, a + 16, yl, IDESC, 1u);
+          mma_ts2(d, a + 24, yh, IDESC, 1u);
+          mma_commit2(&bars[s]);
+          if (pos == CK - 1 || kb == nk - 1) mma_commit2(&pbar[chunk & 1u]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== converter warps (both CTAs)
+    int64_t f_work = pair;
+    uint32_t f_kb = 0;
+    const float2 *fa = Ab, *fb = Bb;
+    bool fa_ok = false, fb_ok = false;
+    auto fetch_setup = [&]() {
+      if (f_work >= total_work) return;
+      const int64_t bidx = f_work / tiles;
+      const int64_t tile = f_work - bidx * tiles;
+      const int64_t am = (tile / tiles_n) * (2 * BM) + crank * BM + row_l;
+      const int64_t bn = (tile % tiles_n) * BN + b_n;
+      fa_ok = am < g.M;
+      fb_ok = bn < g.N;
+      const float2 *A = Ab + bidx * g.sA;
+      const float2 *B = Bb + bidx * g.sB;
+      fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+      fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
+      if (!fa_ok) fa = Ab;
+      if (!fb_ok) fb = Bb;
+    };
+    auto fetch = [&](uint32_t slot) {
+      if (f_work < total_work) {
+        const uint32_t da = rawa0 + slot * L::RAWA_SLOT, db = rawb0 + slot * L::RAWB_SLOT;
+        if (!(k_tail && f_kb == nk - 1)) {
+          if (a_vec) {
+            cp_async16(da, fa, fa_ok);
+            cp_async16(da + V2_THREADS * 16, fa + 2, fa_ok);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, fa + k * a_kstride, fa_ok);
+          }
+          if (b_vec) {
+            cp_async16(db, fb, fb_ok);
+          } else {
+            cp_async8(db, fb, fb_ok);
+            cp_async8(db + 8, fb + b_kstride, fb_ok);
+          }
+        } else {
+          const int64_t k0 = (int64_t)f_kb * KB;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool ok = fa_ok && k0 + 4 * half + k < g.K;
+            cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = fb_ok && k0 + b_k + e < g.K;
+            cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
+          }
+        }
+        if (fa_ok) fa += KB * a_kstride;
+        if (fb_ok) fb += KB * b_kstride;
+        if (++f_kb == nk) {
+          f_kb = 0;
+          f_work += npairs;
+          fetch_setup();
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    uint32_t q = 0;
+    uint32_t pwaits[2] = {0, 0};
+    const uint32_t full_leader = map_to_rank(smem_u32(full), 0);
+    fetch_setup();
+    for (int i = 0; i < RAW - 1; ++i) fetch((uint32_t)i);
+
+    for (int64_t work = pair; work < total_work; work += npairs) {
+      const int64_t bidx = work / tiles;
+      const int64_t tile = work - bidx * tiles;
+      const int64_t m0 = (tile / tiles_n) * (2 * BM) + crank * BM, n0 = (tile % tiles_n) * BN;
+      float2 *C = Cb + bidx * g.sC;
+      float racc[32], iacc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) racc[j] = iacc[j] = 0.f;
+      auto promote = [&](int pb) {
+        mbar_wait(&pbar[pb], pwaits[pb] & 1u);
+        ++pwaits[pb];
+        tc_fence_after();
+        uint32_t v[32];
+        const uint32_t base = tmem + lane_base + (uint32_t)(pb * L::P_COLS + 32 * half);
+        tmem_ld32(base, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) racc[j] += __uint_as_float(v[j]);
+        tmem_ld32(base + BN, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) iacc[j] += __uint_as_float(v[j]);
+      };
+      for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+        fetch((q + RAW - 1) & (RAW - 1));
+        asm volatile("cp.async.wait_group %0;" ::"n"(RAW - 1) : "memory");
+        const uint32_t s = q & (STAGES - 1);
+        if (q >= STAGES) mbar_wait(&bars[s], ((q >> L::LOG_STAGES) + 1) & 1u);
+        const uint32_t slot = q & (RAW - 1);
+        const float4 a01 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
+                                                              slot * L::RAWA_SLOT + tid * 16);
+        const float4 a23 = *reinterpret_cast<const float4 *>(
+            smem + L::RAWA_OFF + slot * L::RAWA_SLOT + V2_THREADS * 16 + tid * 16);
+        const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
+                                                             slot * L::RAWB_SLOT + tid * 16);
+        {
+          uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
+          split_fast(bb.x, hr0, lr0);
+          split_fast(bb.y, hi0, li0);
+          split_fast(bb.z, hr1, lr1);
+          split_fast(bb.w, hi1, li1);
+          uint8_t *stage = smem + s * L::STAGE;
+          // CTA0: X = Br, Y = -Bi      CTA1: X = Bi, Y = Br
+          uint2 xh, yh, xl, yl;
+          if (crank == 0) {
+            xh = make_uint2(hr0, hr1);
+            yh = make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
+            xl = make_uint2(lr0, lr1);
+            yl = make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
+          } else {
+            xh = make_uint2(hi0, hi1);
+            yh = make_uint2(hr0, hr1);
+            xl = make_uint2(li0, li1);
+            yl = make_uint2(lr0, lr1);
+          }
+          *reinterpret_cast<uint2 *>(stage + boff) = xh;
+          *reinterpret_cast<uint2 *>(stage + L::B_BLOCK + boff) = yh;
+          *reinterpret_cast<uint2 *>(stage + 2 * L::B_BLOCK + boff) = xl;
+          *reinterpret_cast<uint2 *>(stage + 3 * L::B_BLOCK + boff) = yl;
+        }
+        {
+          uint32_t rh[4], rl[4], ih[4], il[4];
+          split_fast(a01.x, rh[0], rl[0]);
+          split_fast(a01.y, ih[0], il[0]);
+          split_fast(a01.z, rh[1], rl[1]);
+          split_fast(a01.w, ih[1], il[1]);
+          split_fast(a23.x, rh[2], rl[2]);
+          split_fast(a23.y, ih[2], il[2]);
+          split_fast(a23.z, rh[3], rl[3]);
+          split_fast(a23.w, ih[3], il[3]);
+          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32 + 4 * half);
+          tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+          tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+          tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+          tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          // plain (CTA-scope release) remote arrive, as CUTLASS's 2-SM pipelines
+          // do: the data it publishes is read by the tensor core through the
+          // async proxy (fenced above), not by the leader's threads
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(
+                           full_leader + (uint32_t)(s * 8))
+                       : "memory");
+        const uint32_t pos = kb & (CK - 1);
+        const uint32_t chunk = kb >> L::LOG_CK;
+        if (pos == 0 && kb > 0) promote((int)((chunk - 1) & 1u));
+      }
+      if (nk > 0) promote((int)(((nk - 1) >> L::LOG_CK) & 1u));
+      const int64_t row = m0 + row_l;
+      if (row < g.M) {
+        const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+        const bool use_beta = (br != 0.f || bi != 0.f);
+        const int64_t c0 = n0 + 32 * half;
+        float2 *crow = C + row * g.ldc + c0;
+        const int64_t ncols = min((int64_t)32, g.N - c0);
+        if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && (((uintptr_t)crow) & 15) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            *reinterpret_cast<float4 *>(crow + j) =
+                make_float4(racc[j], iacc[j], racc[j + 1], iacc[j + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j < ncols) {
+              float2 o = make_float2(ar * racc[j] - ai * iacc[j], ar * iacc[j] + ai * racc[j]);
+              if (use_beta) {
+                const float2 c = crow[j];
+                o.x += br * c.x - bi * c.y;
+                o.y += br * c.y + bi * c.x;
+              }
+              crow[j] = o;
+            }
+          }
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // the leader's MMAs read this CTA's smem/TMEM until here
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+}
+
+template <int STAGES, int CK, int RAW>
+int launch_pair(const GemmArgs &g, cudaStream_t s) {
+  using L = LayoutP2<STAGES, CK, RAW>;
+  auto kern = cgemm_tc3pair_kernel<STAGES, CK, RAW>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) {
+      set_error("tc3pair: cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    attr = true;
+  }
+  const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + 2 * BM - 1) / (2 * BM);
+  const int64_t tiles = tiles_n * tiles_m;
+  const int64_t pairs = std::min<int64_t>(tiles * g.batch, (int64_t)sm_count() / 2);
+  kern<<<(unsigned)(2 * pairs), V2_THREADS + 32, L::SMEM, s>>>(g, tiles_n, tiles);
+  return check_launch("cgemm_tc3pair");
+}
+
 }  // namespace tc
 
 // variant: 0 = auto (v3: promoted + cp.async stream), 1 = v1 SS, 2 = v1 TS
@@ -1770,6 +2140,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return small_n ? tc::launch<64, 6, true>(g, s) : tc::launch<128, 4, true>(g, s);
   if (g_tc3_variant == 3) return tc::launch_v2<6, 4>(g, s);
   if (g_tc3_variant == 4) return tc::launch_v3<4, 4, 8>(g, s);
+  if (g_tc3_variant == 6) return tc::launch_pair<8, 4, 8>(g, s);
   if (g_tc3_variant == 5)
     return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
