@@ -100,6 +100,21 @@ int qf_cgemm_c64(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
                  float alpha_re, float alpha_im, float beta_re, float beta_im,
                  void *stream);
 
+/*
+ * Gathered-A twin of qf_cgemm_c64: the permutation of A is fused into the
+ * GEMM's operand fetch instead of a separate transpose pass.
+ *   A(b, r, k) = A + b*strideA + a_roff[r] + a_coff[k]   (complex elements)
+ * a_roff: DEVICE int32[M], a_coff: DEVICE int32[K] (row-major offsets of the
+ * free and summed index groups inside one batch entry; entries < 2^31).
+ * Replaces the permute-then-`@` pair of rq/tensor_core.py:411-417.
+ */
+int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
+                        const void *A, int64_t strideA, const int32_t *a_roff,
+                        const int32_t *a_coff, const void *B, int64_t ldb, int64_t strideB,
+                        int opB, void *C, int64_t ldc, int64_t strideC,
+                        float alpha_re, float alpha_im, float beta_re, float beta_im,
+                        void *stream);
+
 /* complex128 twin (FFMA/DFMA only), for dtype=complex128 engines. */
 int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
                   const void *A, int64_t lda, int64_t strideA, int opA,

@@ -29,7 +29,8 @@ OP_N, OP_T = 0, 1
 # every exported symbol declared in include/qflex_b200.h
 EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_info", "qf_permute", "qf_permute_c64",
-    "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_zgemm_c128", "qf_accumulate",
+    "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_cgemm_c64_gather", "qf_zgemm_c128",
+    "qf_accumulate",
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
     "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
 )
@@ -72,6 +73,12 @@ def _declare(lib):
                                  _c_void_p, _i64, _i64,
                                  ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                  _c_void_p]
+    lib.qf_cgemm_c64_gather.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64,
+                                        _c_void_p, _i64, _c_void_p, _c_void_p,
+                                        _c_void_p, _i64, _i64, ctypes.c_int,
+                                        _c_void_p, _i64, _i64,
+                                        ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                        ctypes.c_float, _c_void_p]
     lib.qf_zgemm_c128.argtypes = [_i64, _i64, _i64, _i64,
                                   _c_void_p, _i64, _i64, ctypes.c_int,
                                   _c_void_p, _i64, _i64, ctypes.c_int,

@@ -26,6 +26,30 @@ void *workspace(int64_t bytes, cudaStream_t stream, int *status);
 
 int sm_count();
 
+// Strided-batched complex GEMM arguments (all engines).  When a_roff/a_coff
+// are set, A is GATHERED: A(b, r, k) = A + b*sA + a_roff[r] + a_coff[k]
+// (element offsets; opA/lda ignored) -- the operand permutation is fused
+// into the GEMM's operand fetch instead of a separate transpose pass.
+struct GemmArgs {
+  int64_t batch, M, N, K;
+  const void *A;
+  int64_t lda, sA;
+  int opA;
+  const void *B;
+  int64_t ldb, sB;
+  int opB;
+  void *C;
+  int64_t ldc, sC;
+  double ar, ai, br, bi;
+  const int32_t *a_roff = nullptr;
+  const int32_t *a_coff = nullptr;
+};
+
+__device__ __forceinline__ int64_t a_offset(const GemmArgs &g, int64_t r, int64_t k) {
+  if (g.a_roff) return (int64_t)g.a_roff[r] + g.a_coff[k];
+  return g.opA == QF_OP_N ? r * g.lda + k : k * g.lda + r;
+}
+
 }  // namespace qf
 
 #define QF_REQUIRE(cond, ...)                 \

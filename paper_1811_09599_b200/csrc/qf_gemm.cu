@@ -40,18 +40,6 @@ __device__ __forceinline__ void cfma(V &acc, const V &a, const V &b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
-struct GemmArgs {
-  int64_t batch, M, N, K;
-  const void *A;
-  int64_t lda, sA;
-  int opA;
-  const void *B;
-  int64_t ldb, sB;
-  int opB;
-  void *C;
-  int64_t ldc, sC;
-  double ar, ai, br, bi;
-};
 
 // ---------------------------------------------------------------------------
 // tiled SIMT kernel
@@ -112,7 +100,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
         }
         int64_t gm = m0 + m, gk = k0 + k;
         V v = zero;
-        if (gm < g.M && gk < g.K) v = (g.opA == QF_OP_N) ? A[gm * g.lda + gk] : A[gk * g.lda + gm];
+        if (gm < g.M && gk < g.K) v = A[a_offset(g, gm, gk)];
         ra[r] = v;
         int n;
         if (g.opB == QF_OP_N) {
@@ -223,14 +211,16 @@ __global__ void __launch_bounds__(STHREADS)
   if (p < P) {
     int64_t m = p / g.N, n = p % g.N;
     int64_t k0 = split * kchunk, k1 = min(g.K, k0 + kchunk);
-    const V *ap = (g.opA == QF_OP_N) ? A + m * g.lda : A + m;
+    // gathered A: the K offsets come from a table; otherwise a fixed stride
+    const bool gat = g.a_roff != nullptr;
+    const V *ap = gat ? A + g.a_roff[m] : ((g.opA == QF_OP_N) ? A + m * g.lda : A + m);
     int64_t as = (g.opA == QF_OP_N) ? 1 : g.lda;
     const V *bp = (g.opB == QF_OP_N) ? B + n : B + n * g.ldb;
     int64_t bs = (g.opB == QF_OP_N) ? g.ldb : 1;
     int64_t k = k0 + kl;
     // 4-way unrolled for memory-level parallelism
     V acc2 = {R(0), R(0)};
-    for (; k + 3 * KL < k1; k += 4 * KL) {
+    for (; !gat && k + 3 * KL < k1; k += 4 * KL) {
       V a0 = ap[k * as], a1 = ap[(k + KL) * as], a2 = ap[(k + 2 * KL) * as],
         a3 = ap[(k + 3 * KL) * as];
       V b0 = bp[k * bs], b1 = bp[(k + KL) * bs], b2 = bp[(k + 2 * KL) * bs],
@@ -240,7 +230,7 @@ __global__ void __launch_bounds__(STHREADS)
       cfma(acc, a2, b2);
       cfma(acc2, a3, b3);
     }
-    for (; k < k1; k += KL) cfma(acc, ap[k * as], bp[k * bs]);
+    for (; k < k1; k += KL) cfma(acc, gat ? ap[g.a_coff[k]] : ap[k * as], bp[k * bs]);
     acc.x += acc2.x;
     acc.y += acc2.y;
   }
@@ -335,7 +325,21 @@ __global__ void __launch_bounds__(SKN_THREADS)
     const int rows = (int)min((int64_t)rm, g.M - m0);
     const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
     V *As = Asb[buf];
-    if (vec) {
+    if (g.a_roff) {
+      // walk the index group that holds A's stride-1 label fastest (coalesced)
+      const bool m_fast = rows > 1 && g.a_roff[m0 + 1] - g.a_roff[m0] == 1;
+      for (int i = tid; i < rows * K; i += SKN_THREADS) {
+        int m, k;
+        if (m_fast) {
+          k = i / rows;
+          m = i - k * rows;
+        } else {
+          m = i / K;
+          k = i - m * K;
+        }
+        skn_cp_async(As + m * apitch + k, A + g.a_roff[m0 + m] + g.a_coff[k], sizeof(V));
+      }
+    } else if (vec) {
       const int pairs = rows * (K / 2);
       for (int i = tid; i < pairs; i += SKN_THREADS) {
         const int m = i / (K / 2), k = (i - m * (K / 2)) * 2;
@@ -468,7 +472,16 @@ __global__ void __launch_bounds__(SKN_THREADS)
     const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
     for (int i = tid; i < rows * K; i += SKN_THREADS) {
       int m, k;
-      if (g.opA == QF_OP_N) {
+      if (g.a_roff) {
+        if (rows > 1 && g.a_roff[m0 + 1] - g.a_roff[m0] == 1) {  // stride-1 label is a row label
+          k = i / rows;
+          m = i - k * rows;
+        } else {
+          m = i / K;
+          k = i - m * K;
+        }
+        As[m * apitch + k] = A[g.a_roff[m0 + m] + g.a_coff[k]];
+      } else if (g.opA == QF_OP_N) {
         m = i / K;
         k = i - m * K;
         As[m * apitch + k] = A[(m0 + m) * g.lda + k];
@@ -537,7 +550,7 @@ __global__ void __launch_bounds__(GV_THREADS)
         V a[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
-          a[r] = (m + r < r1) ? __ldg(A + (m + r) * g.lda + k) : V{R(0), R(0)};
+          a[r] = (m + r < r1) ? __ldg(A + a_offset(g, m + r, k)) : V{R(0), R(0)};
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -578,7 +591,7 @@ __global__ void __launch_bounds__(GV_THREADS)
 }
 
 bool gemv_eligible(const GemmArgs &g) {
-  return g.N <= 4 && g.opA == QF_OP_N && g.K >= 32 && g.M >= 32;
+  return g.N <= 4 && (g.opA == QF_OP_N || g.a_roff) && g.K >= 32 && g.M >= 32;
 }
 
 template <typename R, int NC>
@@ -729,6 +742,7 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
 // from qf_gemm_tc.cu
 int gemm_tc3(const GemmArgs &g, cudaStream_t s);
 bool tc3_eligible(const GemmArgs &g);
+bool tc3_gather_ok(const GemmArgs &g);
 
 }  // namespace qf
 
@@ -746,6 +760,23 @@ int qf_cgemm_c64(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const
   if (mode == QF_GEMM_TC3) return qf::gemm_tc3(g, s);
   if (mode == QF_GEMM_AUTO && qf::tc3_eligible(g)) return qf::gemm_tc3(g, s);
   QF_REQUIRE(mode == QF_GEMM_AUTO || mode == QF_GEMM_FFMA, "gemm: unknown mode %d", mode);
+  return qf::gemm_simt<float>(g, s);
+}
+
+int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                        int64_t strideA, const int32_t *a_roff, const int32_t *a_coff,
+                        const void *B, int64_t ldb, int64_t strideB, int opB, void *C, int64_t ldc,
+                        int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                        float beta_im, void *stream) {
+  QF_REQUIRE(a_roff != nullptr && a_coff != nullptr, "gather gemm: offset tables are NULL");
+  qf::GemmArgs g{batch, M, N, K, A, std::max<int64_t>(K, 1), strideA, QF_OP_N, B, ldb, strideB,
+                 opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff};
+  int st = qf::validate(g);
+  if (st != QF_OK) return st;
+  cudaStream_t s = qf::as_stream(stream);
+  if ((mode == QF_GEMM_AUTO && qf::tc3_eligible(g)) || mode == QF_GEMM_TC3) {
+    if (qf::tc3_gather_ok(g)) return qf::gemm_tc3(g, s);
+  }
   return qf::gemm_simt<float>(g, s);
 }
 

@@ -35,18 +35,6 @@
 
 namespace qf {
 
-struct GemmArgs {
-  int64_t batch, M, N, K;
-  const void *A;
-  int64_t lda, sA;
-  int opA;
-  const void *B;
-  int64_t ldb, sB;
-  int opB;
-  void *C;
-  int64_t ldc, sC;
-  double ar, ai, br, bi;
-};
 
 namespace tc {
 
@@ -729,7 +717,9 @@ struct LayoutV3 {
   static constexpr int RAWA_OFF = STAGES * STAGE;
   static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
   static constexpr int BAR_OFF = RAWB_OFF + RAW * RAWB_SLOT;
-  static constexpr int SMEM = BAR_OFF + 1024;
+  static constexpr int COFF_OFF = BAR_OFF + 1024;           // gathered-A K offsets (int32)
+  static constexpr int COFF_MAX = 4096;
+  static constexpr int SMEM = COFF_OFF + 4 * COFF_MAX;
   static constexpr int P_COLS = NP;
   static constexpr int A_COL0 = 2 * P_COLS;
   static constexpr int TMEM_COLS = 512;
@@ -1038,6 +1028,10 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
                  "r"(L::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  const bool gat = g.a_roff != nullptr;
+  int32_t *s_coff = reinterpret_cast<int32_t *>(smem + L::COFF_OFF);
+  if (gat)
+    for (int i = tid; i < (int)g.K; i += blockDim.x) s_coff[i] = g.a_coff[i];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1076,7 +1070,8 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     fb_ok = bn < g.N;
     const float2 *A = Ab + bidx * g.sA;
     const float2 *B = Bb + bidx * g.sB;
-    fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+    fa = gat ? A + g.a_roff[fa_ok ? am : 0]
+             : ((g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am);
     fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
     if (!fa_ok) fa = Ab;
     if (!fb_ok) fb = Bb;
@@ -1084,8 +1079,17 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
   auto fetch = [&](uint32_t slot) {
     if (f_work < total_work) {
       const uint32_t da = rawa0 + slot * L::RAWA_SLOT, db = rawb0 + slot * L::RAWB_SLOT;
+      if (gat) {  // A row base + per-k offsets from the staged table
+        const int64_t k0 = (int64_t)f_kb * KB + 4 * half;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const bool ok = fa_ok && k0 + k < g.K;
+          cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + s_coff[k0 + k] : Ab, ok);
+        }
+      }
       if (!(k_tail && f_kb == nk - 1)) {
-        if (a_vec) {
+        if (gat) {
+        } else if (a_vec) {
           cp_async16(da, fa, fa_ok);
           cp_async16(da + V2_THREADS * 16, fa + 2, fa_ok);
         } else {
@@ -1103,6 +1107,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
         const int64_t k0 = (int64_t)f_kb * KB;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+          if (gat) break;
           const bool ok = fa_ok && k0 + 4 * half + k < g.K;
           cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
         }
@@ -1112,7 +1117,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
           cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
         }
       }
-      if (fa_ok) fa += KB * a_kstride;
+      if (fa_ok && !gat) fa += KB * a_kstride;
       if (fb_ok) fb += KB * b_kstride;
       if (++f_kb == nk) {
         f_kb = 0;
@@ -2125,6 +2130,8 @@ int launch_pair(const GemmArgs &g, cudaStream_t s) {
 // k-block); default = warp-specialised stream
 static int g_tc3_variant = 0;
 
+bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
+
 bool tc3_eligible(const GemmArgs &g) {
   // a 128 x 64 tile reasonably full, K long enough to amortise the pipeline
   return g.M >= 128 && g.N >= 32 && g.K >= 32 && g.M * g.N * g.batch >= 128 * 64 * 148;
@@ -2134,6 +2141,10 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
   QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
   const bool small_n = g.N <= 64;
+  if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
+    QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
+    return g.K <= 256 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_ws<8, 4, 8, false>(g, s);
+  }
   if (g_tc3_variant == 1)
     return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);
   if (g_tc3_variant == 2)

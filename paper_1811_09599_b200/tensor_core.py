@@ -47,6 +47,17 @@ if torch is not None:
     _TORCH_OF = {np.dtype(np.complex64): torch.complex64, np.dtype(np.complex128): torch.complex128}
     _NP_OF = {torch.complex64: np.dtype(np.complex64), torch.complex128: np.dtype(np.complex128)}
 
+# fuse the big operand's permutation into the GEMM operand fetch (gathered A)
+_gather_enabled = True
+
+
+def set_gather(enabled: bool) -> bool:
+    """Enable/disable gathered-A GEMMs in `contract`; returns the previous value."""
+    global _gather_enabled
+    prev, _gather_enabled = _gather_enabled, bool(enabled)
+    return prev
+
+
 # GEMM engine for contractions: "auto" (tcgen05 3xTF32 where it pays), "ffma", "tc3"
 _GEMM_MODES = {"auto": _lib.GEMM_AUTO, "ffma": _lib.GEMM_FFMA, "tc3": _lib.GEMM_TC3}
 _gemm_mode = _lib.GEMM_AUTO
@@ -219,6 +230,53 @@ def gemm_buffer(batch, M, N, K, A, opA, B, opB, C, alpha=1.0, beta=0.0, mode=Non
     _lib.check(st, "gemm")
 
 
+_GATHER_TABLES: dict = {}
+
+
+def _gather_tables(dims, labels, rows, cols, device):
+    """Device int32 offset tables of a tensor's free (`rows`) and summed
+    (`cols`) label groups inside one batch entry (memoised per layout)."""
+    key = (tuple(dims), tuple(labels), tuple(rows), tuple(cols), str(device))
+    hit = _GATHER_TABLES.get(key)
+    if hit is not None:
+        return hit
+    stride = {}
+    acc = 1
+    for l, d in zip(reversed(labels), reversed(dims)):
+        stride[l] = acc
+        acc *= d
+    dim = dict(zip(labels, dims))
+
+    def table(group):
+        off = np.zeros(1, dtype=np.int64)
+        for l in group:
+            off = (off[:, None] + np.arange(dim[l], dtype=np.int64)[None, :] * stride[l]).reshape(-1)
+        return torch.from_numpy(off.astype(np.int32)).to(device)
+
+    hit = (table(rows), table(cols))
+    if len(_GATHER_TABLES) > 512:
+        _GATHER_TABLES.clear()
+    _GATHER_TABLES[key] = hit
+    return hit
+
+
+def gemm_gather_buffer(batch, M, N, K, A, sA, roff, coff, B, opB, C, mode=None):
+    """C[b] = A_gathered[b] @ op(B[b]) (complex64): the big operand is read
+    through offset tables instead of being transposed first."""
+    ldb = N if opB == _lib.OP_N else K
+    lib = _lib.load()
+    with _timed("gemm", 8 * batch * M * N * K, 8 * batch * (M * K + K * N + M * N),
+                f"b{batch} m{M} n{N} k{K} G{'NT'[opB]}" if _timer else ""):
+        st = lib.qf_cgemm_c64_gather(_gemm_mode if mode is None else mode, batch, M, N, K,
+                                     ctypes.c_void_p(A.data_ptr()), sA,
+                                     ctypes.c_void_p(roff.data_ptr()),
+                                     ctypes.c_void_p(coff.data_ptr()),
+                                     ctypes.c_void_p(B.data_ptr()), max(ldb, 1), K * N, opB,
+                                     ctypes.c_void_p(C.data_ptr()), max(N, 1), M * N,
+                                     1.0, 0.0, 0.0, 0.0, stream_handle())
+    _lib.check(st, "gemm_gather")
+
+
 def _gemm_call(lib, batch, M, N, K, A, lda, opA, B, ldb, opB, C, sA, sB, sC, alpha, beta, mode):
     if C.dtype == torch.complex64:
         st = lib.qf_cgemm_c64(_gemm_mode if mode is None else mode, batch, M, N, K,
@@ -384,6 +442,10 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     (rq/tensor_core.py:396-419) with the batch axis in front."""
     if a.data.dtype != b.data.dtype:
         raise ValueError(f"dtype mismatch: {a.dtype} vs {b.dtype}")
+    if b.size > a.size:
+        # the big operand goes first (its layout decides the GEMM); the output
+        # is then [batch, b_free, a_free] -- labels carry the order
+        a, b = b, a
     bset, aset = set(b.labels), set(a.labels)
     batch = [l for l in a.labels if l in bset and _is_batch(l)]
     shared_a = [l for l in a.labels if l in bset and not _is_batch(l)]
@@ -407,14 +469,25 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
             return t, _lib.OP_T
         return t.transpose_to(n_layout), _lib.OP_N
 
-    A, opA = operand(a, a_free, True)      # N: [batch][M][K], T: [batch][K][M]
-    B, opB = operand(b, b_free, False)     # N: [batch][K][N], T: [batch][N][K]
     bt = math.prod(a.dim_of(l) for l in batch)
     m = math.prod(a.dim_of(l) for l in a_free)
     k = math.prod(a.dim_of(l) for l in k_order)
     n = math.prod(b.dim_of(l) for l in b_free)
     out = device_buffer(bt * m * n, a.data.dtype, a.data.device)
-    gemm_buffer(bt, m, n, k, A.data, opA, B.data, opB, out)
+    B, opB = operand(b, b_free, False)     # N: [batch][K][N], T: [batch][N][K]
+    a_n = batch + a_free + k_order
+    a_t = batch + k_order + a_free
+    entry = a.size // max(bt, 1)
+    if (list(a.labels) not in (a_n, a_t) and a.data.dtype == torch.complex64
+            and list(a.labels[:len(batch)]) == batch and entry >= 4096 and entry < 2 ** 31
+            and m <= 2 ** 22 and k <= 4096 and _gather_enabled):
+        # fuse the big operand's permutation into the GEMM fetch
+        nb = len(batch)
+        roff, coff = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order, a.data.device)
+        gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out)
+    else:
+        A, opA = operand(a, a_free, True)  # N: [batch][M][K], T: [batch][K][M]
+        gemm_buffer(bt, m, n, k, A.data, opA, B.data, opB, out)
     labels = tuple(batch + a_free + b_free)
     dims = tuple(a.dim_of(l) for l in batch + a_free) + tuple(b.dim_of(l) for l in b_free)
     return Tensor(labels, out, dims)
