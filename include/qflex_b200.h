@@ -145,6 +145,11 @@ int qf_workspace_release(void);
  * Returns the previous setting. */
 int qf_tc3_set_variant(int variant);
 
+/* K3 tuning/validation knob for memory-bound small K x N shapes: 0 = auto
+ * (row-block streaming for N <= 16, shared-memory staged otherwise), 1 =
+ * staged kernels only, 2 = row-block kernel only.  Returns the previous one. */
+int qf_small_engine(int engine);
+
 /* Name of the last kernel this library launched on the calling thread
  * (static string; "" if none) -- lets profilers attribute timings. */
 const char *qf_last_kernel(void);

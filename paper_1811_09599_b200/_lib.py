@@ -32,6 +32,7 @@ EXPORTS = (
     "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_cgemm_c64_gather", "qf_zgemm_c128",
     "qf_accumulate",
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
+    "qf_small_engine",
     "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
 )
 
@@ -88,6 +89,7 @@ def _declare(lib):
     lib.qf_accumulate.argtypes = [_c_void_p, _c_void_p, _i64, ctypes.c_int, _c_void_p]
     lib.qf_fill_zero.argtypes = [_c_void_p, _i64, _c_void_p]
     lib.qf_tc3_set_variant.argtypes = [ctypes.c_int]
+    lib.qf_small_engine.argtypes = [ctypes.c_int]
     lib.qf_last_kernel.restype = ctypes.c_char_p
     lib.qf_last_kernel.argtypes = []
     lib.qf_workspace_reserve.argtypes = [_i64, _c_void_p]

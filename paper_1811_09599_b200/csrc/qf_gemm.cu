@@ -513,6 +513,123 @@ __global__ void __launch_bounds__(SKN_THREADS)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// row-block streaming kernel for the small K x N shapes (K*N <= 4096 and one
+// of K, N <= 16): B[b] is staged in smem once per batch entry; each thread
+// owns (row, group of 8 output columns) and streams its A row in chunks of 8
+// k straight into registers (N, T or gathered layout), so every A byte is
+// read once with no shared-memory round trip and C is written with 16-byte
+// stores.  A CTA walks a contiguous range of (batch, row-block) items.
+
+constexpr int RB_THREADS = 256;
+constexpr int RB_NG = 8;
+
+template <typename R>
+__global__ void __launch_bounds__(RB_THREADS)
+    cgemm_rowblock_kernel(const __grid_constant__ GemmArgs g, int rows_per_item,
+                          int64_t items_per_b, int64_t items_per_cta) {
+  using V = typename C2<R>::T;
+  extern __shared__ __align__(16) unsigned char rb_smem[];
+  V *Bs = reinterpret_cast<V *>(rb_smem);
+  const int K = (int)g.K, N = (int)g.N;
+  const int groups = (N + RB_NG - 1) / RB_NG;
+  const int tid = threadIdx.x;
+  const R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
+  const bool use_beta = (br != R(0) || bi != R(0));
+  const int64_t total = g.batch * items_per_b;
+  const int64_t it0 = blockIdx.x * items_per_cta, it1 = min(total, it0 + items_per_cta);
+  int64_t cur_b = -1;
+  for (int64_t item = it0; item < it1; ++item) {
+    const int64_t b = item / items_per_b;
+    const int64_t r0 = (item - b * items_per_b) * rows_per_item;
+    const int rows = (int)min((int64_t)rows_per_item, g.M - r0);
+    if (b != cur_b) {
+      __syncthreads();
+      const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+      for (int i = tid; i < K * N; i += RB_THREADS) {
+        int k, n;
+        if (g.opB == QF_OP_N) {
+          k = i / N;
+          n = i - k * N;
+          Bs[k * N + n] = B[(int64_t)k * g.ldb + n];
+        } else {
+          n = i / K;
+          k = i - n * K;
+          Bs[k * N + n] = B[(int64_t)n * g.ldb + k];
+        }
+      }
+      cur_b = b;
+      __syncthreads();
+    }
+    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
+    for (int task = tid; task < rows * groups; task += RB_THREADS) {
+      const int r = task / groups, cg = task - r * groups;
+      const int64_t row = r0 + r;
+      const int n0 = cg * RB_NG;
+      V acc[RB_NG];
+#pragma unroll
+      for (int j = 0; j < RB_NG; ++j) acc[j] = V{R(0), R(0)};
+      const V *arow = g.a_roff ? A + g.a_roff[row]
+                               : (g.opA == QF_OP_N ? A + row * g.lda : A + row);
+      for (int k0 = 0; k0 < K; k0 += 8) {
+        V a[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = k0 + j;
+          a[j] = V{R(0), R(0)};
+          if (k < K)
+            a[j] = g.a_roff ? __ldg(arow + g.a_coff[k])
+                            : (g.opA == QF_OP_N ? __ldg(arow + k) : __ldg(arow + (int64_t)k * g.lda));
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (k0 + j < K) {
+            const V *bk = Bs + (k0 + j) * N + n0;
+#pragma unroll
+            for (int c = 0; c < RB_NG; ++c)
+              if (n0 + c < N) cfma(acc[c], a[j], bk[c]);
+          }
+        }
+      }
+      V *cp = C + row * g.ldc + n0;
+#pragma unroll
+      for (int c = 0; c < RB_NG; ++c) {
+        if (n0 + c < N) {
+          V o;
+          o.x = ar * acc[c].x - ai * acc[c].y;
+          o.y = ar * acc[c].y + ai * acc[c].x;
+          if (use_beta) {
+            const V cv = cp[c];
+            o.x += br * cv.x - bi * cv.y;
+            o.y += br * cv.y + bi * cv.x;
+          }
+          cp[c] = o;
+        }
+      }
+    }
+  }
+}
+
+template <typename R>
+int gemm_rowblock(const GemmArgs &g, cudaStream_t s) {
+  using V = typename C2<R>::T;
+  const int groups = (int)((g.N + RB_NG - 1) / RB_NG);
+  // ~8 row-groups of work per thread per item; items fill the machine
+  int rows_per_item = (int)std::max<int64_t>(1, std::min<int64_t>(g.M, 8 * RB_THREADS / groups));
+  const int64_t items_per_b = (g.M + rows_per_item - 1) / rows_per_item;
+  const int64_t items = g.batch * items_per_b;
+  const int64_t ctas = std::min<int64_t>(items, (int64_t)sm_count() * 8);
+  const int64_t per_cta = (items + ctas - 1) / ctas;
+  const int64_t grid = (items + per_cta - 1) / per_cta;
+  const size_t smem = (size_t)g.K * g.N * sizeof(V);
+  auto kern = cgemm_rowblock_kernel<R>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  kern<<<(unsigned)grid, RB_THREADS, smem, s>>>(g, rows_per_item, items_per_b, per_cta);
+  return check_launch("cgemm_rowblock");
+}
+
 // ---------------------------------------------------------------------------
 // batched GEMV family: N <= 4 output columns, A in N layout (rows contiguous
 // along K).  One warp per row group: lanes stride K with coalesced loads,
@@ -647,6 +764,10 @@ int validate(const GemmArgs &g) {
   return QF_OK;
 }
 
+// 0 = auto (row-block streaming for N <= 16, smem-staged otherwise),
+// 1 = smem-staged kernels only, 2 = row-block kernel only
+static int g_small_engine = 0;
+
 bool smallkn_eligible(const GemmArgs &g) {
   // B[b] fits in smem and one of the contracted/output widths is narrow:
   // these shapes are HBM-bound and the 64x64 tile wastes most of its work
@@ -730,7 +851,12 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
     return check_launch("cgemm_skinny_reduce");
   }
   if (gemv_eligible(g)) return gemm_gemv<R>(g, s);
-  if (smallkn_eligible(g)) return gemm_smallkn<R>(g, s);
+  if (smallkn_eligible(g)) {
+    // narrow outputs stream best row by row; wide outputs keep the
+    // smem-staged kernels (warp-wide conflict-free B reads)
+    const bool rowblock = g_small_engine == 0 ? g.N <= 16 : g_small_engine == 2;
+    return rowblock ? gemm_rowblock<R>(g, s) : gemm_smallkn<R>(g, s);
+  }
   int64_t tiles_n = (g.N + TBN - 1) / TBN, tiles_m = (g.M + TBM - 1) / TBM;
   int64_t tiles = tiles_n * tiles_m;
   int64_t work = tiles * g.batch;
@@ -778,6 +904,12 @@ int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K
     if (qf::tc3_gather_ok(g)) return qf::gemm_tc3(g, s);
   }
   return qf::gemm_simt<float>(g, s);
+}
+
+int qf_small_engine(int engine) {
+  int prev = qf::g_small_engine;
+  qf::g_small_engine = engine;
+  return prev;
 }
 
 int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K, const void *A, int64_t lda,

@@ -170,3 +170,17 @@ def test_gathered_a_contract_matches_permuted(mode, case):
     finally:
         tc.set_gather(True)
         tc.set_gemm_mode(prev)
+
+
+@pytest.mark.parametrize("engine", [0, 1, 2], ids=["auto", "smem", "rowblock"])
+@pytest.mark.parametrize("shape", [(3, 4096, 8, 64), (2, 4096, 64, 8), (1, 32768, 8, 8),
+                                   (4, 512, 512, 8), (2, 100, 13, 7), (1, 77, 3, 300)])
+@pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1)])
+def test_small_kxn_engines(engine, shape, ops):
+    lib = _lib.load()
+    prev = lib.qf_small_engine(engine)
+    try:
+        assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_FFMA) < 1e-5
+        assert _gemm(*shape[:3], shape[3], *ops, np.complex128) < 1e-12
+    finally:
+        lib.qf_small_engine(prev)
