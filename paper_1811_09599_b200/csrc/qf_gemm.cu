@@ -779,11 +779,14 @@ int gemm_smallkn_simple(const GemmArgs &g, cudaStream_t s) {
   using V = typename C2<R>::T;
   const int K = (int)g.K, N = (int)g.N;
   const int bpitch = N + ((N % 2 == 0) ? 1 : 0), apitch = K + ((K % 2 == 0) ? 1 : 0);
-  int rm = (int)std::min<int64_t>(g.M, std::max(1, SKN_A_MAX / apitch));
+  // A block sized to the smem left after B (complex128 entries are twice as big)
+  const int64_t a_budget = std::max<int64_t>(
+      apitch, (int64_t)(160 * 1024) / (int64_t)sizeof(V) - (int64_t)K * bpitch);
+  int rm = (int)std::min<int64_t>(g.M, std::max<int64_t>(1, std::min<int64_t>(SKN_A_MAX, a_budget) / apitch));
   int64_t blocks_m = (g.M + rm - 1) / rm;
   size_t smem = ((size_t)K * bpitch + (size_t)rm * apitch) * sizeof(V);
   auto kern = cgemm_smallkn_simple_kernel<R>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   int64_t items = g.batch * blocks_m;
   int64_t grid = std::min<int64_t>(items, (int64_t)sm_count() * 6);
   kern<<<(unsigned)grid, SKN_THREADS, smem, s>>>(g, rm, blocks_m);
@@ -797,7 +800,9 @@ int gemm_smallkn(const GemmArgs &g, cudaStream_t s) {
   if (K <= 16) return gemm_smallkn_simple<R>(g, s);
   const int bpitch = N + ((N % 2 == 0) ? 1 : 0);
   const int apitch = (K % 2 == 0) ? K + 2 : K + 1;  // even pitch keeps 16-byte pairs aligned
-  int rm = (int)std::min<int64_t>(g.M, std::max(1, SKN_A_MAX / apitch));
+  const int64_t a_budget = std::max<int64_t>(
+      apitch, ((int64_t)(160 * 1024) / (int64_t)sizeof(V) - (int64_t)K * bpitch) / 2);
+  int rm = (int)std::min<int64_t>(g.M, std::max<int64_t>(1, std::min<int64_t>(SKN_A_MAX, a_budget) / apitch));
   const int64_t blocks_m = (g.M + rm - 1) / rm;
   const size_t smem = ((((size_t)K * bpitch + 1) & ~(size_t)1) + 2 * (size_t)rm * apitch) * sizeof(V);
   // short K: one output per thread (warp spans a row: A broadcast, B
