@@ -124,6 +124,16 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -996,7 +1006,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
 
 // warp-specialised twin: 8 converter warps + 1 MMA-issue warp, per-stage
 // `full` mbarriers instead of a block barrier per k-block
-template <int STAGES, int CK, int RAW, bool SHORTK>
+template <int STAGES, int CK, int RAW, bool SHORTK, int KS>
 __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     cgemm_tc3w_kernel(const __grid_constant__ GemmArgs g, int64_t tiles_n, int64_t tiles) {
   using L = LayoutV3<STAGES, CK, RAW>;
@@ -1019,7 +1029,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
 
   if (tid == 0) {
     for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], V2_THREADS / 32);
+    for (int i = 0; i < STAGES / KS; ++i) mbar_init(&full[i], V2_THREADS / 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1129,14 +1139,19 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
   };
 
   if (warp == V2_THREADS / 32) {
-    // ===== MMA issuer: one elected thread walks the same k-block sequence
-    if (lane == 0) {
-      uint32_t qm = 0, tcount = 0;
+    // ===== MMA issuer: the whole warp walks the k-block sequence (operands stay
+    // warp-uniform, i.e. in uniform registers); one elected lane issues
+    {
+      uint32_t qm = 0, tcount = 0, gq = 0;
+      constexpr uint32_t NG = STAGES / KS;     // converted groups in flight
       for (int64_t work = blockIdx.x; work < total_work; work += gridDim.x, ++tcount) {
         for (uint32_t kb = 0; kb < nk; ++kb, ++qm) {
           const uint32_t s = qm & (STAGES - 1);
-          mbar_wait(&full[s], (qm >> L::LOG_STAGES) & 1u);
-          tc_fence_after();
+          if (kb % KS == 0) {  // one handoff per group of KS k-blocks (aligned to tiles)
+            mbar_wait(&full[gq % NG], (gq / NG) & 1u);
+            tc_fence_after();
+            ++gq;
+          }
           // SHORTK: one accumulation per tile, buffers alternate per tile;
           // otherwise chunks of CK k-blocks alternate (promotion)
           const uint32_t pos = SHORTK ? kb : (kb & (CK - 1));
@@ -1148,21 +1163,25 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
           const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
           const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
           const uint32_t acc0 = pos > 0 ? 1u : 0u;
-          mma_ts(d, a + 0, b1h, IDESC, acc0);
-          mma_ts(d, a + 0, b1l, IDESC, 1u);
-          mma_ts(d, a + 8, b1h, IDESC, 1u);
-          mma_ts(d, a + 16, b2h, IDESC, 1u);
-          mma_ts(d, a + 16, b2l, IDESC, 1u);
-          mma_ts(d, a + 24, b2h, IDESC, 1u);
-          mma_commit(&bars[s]);
-          if (SHORTK ? kb == nk - 1 : (pos == CK - 1 || kb == nk - 1))
-            mma_commit(&pbar[chunk & 1u]);
+          if (elect_one()) {
+            mma_ts(d, a + 0, b1h, IDESC, acc0);
+            mma_ts(d, a + 0, b1l, IDESC, 1u);
+            mma_ts(d, a + 8, b1h, IDESC, 1u);
+            mma_ts(d, a + 16, b2h, IDESC, 1u);
+            mma_ts(d, a + 16, b2l, IDESC, 1u);
+            mma_ts(d, a + 24, b2h, IDESC, 1u);
+            mma_commit(&bars[s]);
+            if (SHORTK ? kb == nk - 1 : (pos == CK - 1 || kb == nk - 1))
+              mma_commit(&pbar[chunk & 1u]);
+          }
+          __syncwarp();
         }
       }
     }
     __syncwarp();
   } else {
   uint32_t q = 0;            // k-blocks consumed by this CTA (drives every ring)
+  uint32_t gc = 0;           // groups handed to the MMA warp
   uint32_t pwaits[2] = {0, 0};
   fetch_setup();
   for (int i = 0; i < RAW - 1; ++i) fetch((uint32_t)i);
@@ -1290,8 +1309,13 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       fence_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+      if (kb % KS == KS - 1 || kb == nk - 1) {  // group (or tile) converted
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                           smem_u32(&full[gc % (STAGES / KS)]))
+                       : "memory");
+        ++gc;
+      }
       const uint32_t pos = kb & (CK - 1);
       const uint32_t chunk = kb >> L::LOG_CK;
       if constexpr (SHORTK) {
@@ -1354,10 +1378,10 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
                  "r"(L::TMEM_COLS));
 }
 
-template <int STAGES, int CK, int RAW, bool SHORTK>
+template <int STAGES, int CK, int RAW, bool SHORTK, int KS = 1>
 int launch_ws(const GemmArgs &g, cudaStream_t s) {
   using L = LayoutV3<STAGES, CK, RAW>;
-  auto kern = cgemm_tc3w_kernel<STAGES, CK, RAW, SHORTK>;
+  auto kern = cgemm_tc3w_kernel<STAGES, CK, RAW, SHORTK, KS>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -2152,6 +2176,10 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 3) return tc::launch_v2<6, 4>(g, s);
   if (g_tc3_variant == 4) return tc::launch_v3<4, 4, 8>(g, s);
   if (g_tc3_variant == 6) return tc::launch_pair<8, 4, 8>(g, s);
+  if (g_tc3_variant == 7)
+    return g.K <= 256 ? tc::launch_ws<8, 4, 8, true, 2>(g, s) : tc::launch_ws<8, 4, 8, false, 2>(g, s);
+  if (g_tc3_variant == 8)
+    return g.K <= 256 ? tc::launch_ws<8, 4, 8, true, 4>(g, s) : tc::launch_ws<8, 4, 8, false, 4>(g, s);
   if (g_tc3_variant == 5)
     return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level

@@ -93,7 +93,7 @@ TC_SHAPES = [(1, 128, 128, 8), (1, 128, 128, 64), (2, 256, 256, 40), (1, 300, 20
              (1, 2048, 2048, 512)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6], ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8], ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
