@@ -89,6 +89,21 @@ def _bits_str(value, n: int) -> str:
     return format(int(value), f"0{n}b")
 
 
+def _bits_matrix(values: Sequence, n: int) -> np.ndarray:
+    """(len(values), n) int32 0/1 matrix of bit-strings or integers
+    (qubit 0 = leftmost / most significant), parsed in bulk."""
+    vals = list(values)
+    if all(isinstance(v, str) for v in vals):
+        raw = "".join(vals).encode()
+        arr = np.frombuffer(raw, dtype=np.uint8).astype(np.int32) - ord("0")
+        if len(raw) != n * len(vals) or (arr.size and (arr.min() < 0 or arr.max() > 1)):
+            for v in vals:
+                _bits_str(v, n)  # raises the reference's ValueError
+        return arr.reshape(len(vals), n)
+    return np.array([[int(c) for c in _bits_str(v, n)] for v in vals], dtype=np.int32).reshape(
+        len(vals), n)
+
+
 def _completions(n_open: int, n_c: int, seed: int) -> np.ndarray:
     """The n_c completions of the open region (rq/amplitude_engine.py:159-164)."""
     if n_c == 2 ** n_open:
@@ -178,8 +193,8 @@ class AmplitudeEngine:
         this (input, chunk size, fidelity) is captured once as a CUDA graph
         and replayed for every later chunk of the same size."""
         n = self.circuit.n
-        outs = [_bits_str(o, n) for o in out_bits]
-        bits = np.array([[int(c) for c in o] for o in outs], dtype=np.int32).reshape(len(outs), n)
+        bits = _bits_matrix(out_bits, n)
+        outs = bits  # row count only below
         chunk = chunk or max(1, len(outs))
         result = np.empty(len(outs), dtype=self.dtype)
         stats = None

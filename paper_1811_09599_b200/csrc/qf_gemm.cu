@@ -539,6 +539,8 @@ __global__ void __launch_bounds__(RB_THREADS)
   const bool use_beta = (br != R(0) || bi != R(0));
   const int64_t total = g.batch * items_per_b;
   const int64_t it0 = blockIdx.x * items_per_cta, it1 = min(total, it0 + items_per_cta);
+  const bool vec_a = sizeof(V) == 8 && !g.a_roff && g.opA == QF_OP_N && g.lda % 2 == 0 &&
+                     g.sA % 2 == 0;
   int64_t cur_b = -1;
   for (int64_t item = it0; item < it1; ++item) {
     const int64_t b = item / items_per_b;
@@ -575,13 +577,22 @@ __global__ void __launch_bounds__(RB_THREADS)
                                : (g.opA == QF_OP_N ? A + row * g.lda : A + row);
       for (int k0 = 0; k0 < K; k0 += 8) {
         V a[8];
+        if (vec_a && k0 + 8 <= K) {  // row-major A: four 16-byte loads per 8 k
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k = k0 + j;
-          a[j] = V{R(0), R(0)};
-          if (k < K)
-            a[j] = g.a_roff ? __ldg(arow + g.a_coff[k])
-                            : (g.opA == QF_OP_N ? __ldg(arow + k) : __ldg(arow + (int64_t)k * g.lda));
+          for (int j = 0; j < 8; j += 2) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(arow + k0 + j));
+            a[j] = V{(R)v.x, (R)v.y};
+            a[j + 1] = V{(R)v.z, (R)v.w};
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = k0 + j;
+            a[j] = V{R(0), R(0)};
+            if (k < K)
+              a[j] = g.a_roff ? __ldg(arow + g.a_coff[k])
+                              : (g.opA == QF_OP_N ? __ldg(arow + k) : __ldg(arow + (int64_t)k * g.lda));
+          }
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
