@@ -1065,43 +1065,94 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
   const int64_t a_kstride = (g.opA == QF_OP_N) ? 1 : g.lda;   // elements between consecutive k
   const int64_t b_kstride = (g.opB == QF_OP_N) ? g.ldb : 1;
 
+  // A fetch modes.  The converter thread of TMEM lane r needs row r's k
+  // values, but one-row-per-lane global loads touch 32 sectors per warp
+  // instruction; instead each warp fetches its own 32 rows x 4 k with lanes
+  // spread along k (whole 32-byte sectors per row) and the rows land in the
+  // owning lanes' raw slots -- the hand-off stays inside the warp.
+  //   1: gathered  -- lane (r4 = lane/4, kq = lane%4): rows 8i + r4, k kq (8 B)
+  //   2: row-major -- lane (r2 = lane/2, kp = lane%2): rows 16i + r2, k 2kp..2kp+1 (16 B)
+  //   0: column-major (lane = row is already coalesced) or odd lda
+  const int a_mode = gat ? 1 : (a_vec ? 2 : 0);
+  const uint32_t rawa_m =
+      smem_u32(smem + L::RAWA_OFF) +
+      (a_mode == 1 ? (uint32_t)(((lane & 3) >> 1) * V2_THREADS * 16 + (warp * 32 + (lane >> 2)) * 16 +
+                                (lane & 1) * 8)
+                   : (uint32_t)((lane & 1) * V2_THREADS * 16 + (warp * 32 + (lane >> 1)) * 16));
+
   // ---- fetch cursor: incremental source pointers, set up once per tile
   int64_t f_work = blockIdx.x;
   uint32_t f_kb = 0;
   const float2 *fa = Ab, *fb = Bb;
   bool fa_ok = false, fb_ok = false;
+  uint32_t amask = 0, amask_next = 0;       // valid rows of this / the next tile
+  int32_t ro[4] = {0, 0, 0, 0}, ro_next[4] = {0, 0, 0, 0};
+  // gathered row offsets are loaded one tile ahead so the load latency hides
+  // behind a whole tile of k-blocks
+  auto load_ro = [&](int64_t work, int32_t (&dst)[4], uint32_t &mask) {
+    mask = 0;
+    if (work >= total_work) return;
+    const int64_t tile = work % tiles;
+    const int64_t r0 = (tile / tiles_n) * BM + lg * 32 + (lane >> 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = r0 + 8 * i < g.M;
+      dst[i] = ok ? __ldg(g.a_roff + r0 + 8 * i) : 0;
+      mask |= ok ? (1u << i) : 0u;
+    }
+  };
+  if (SHORTK && a_mode == 1) load_ro(f_work, ro_next, amask_next);
   auto fetch_setup = [&]() {
     if (f_work >= total_work) return;
     const int64_t bidx = f_work / tiles;
     const int64_t tile = f_work - bidx * tiles;
-    const int64_t am = (tile / tiles_n) * BM + row_l;
+    const int64_t mt0 = (tile / tiles_n) * BM;
+    const int64_t am = mt0 + row_l;
     const int64_t bn = (tile % tiles_n) * BN + b_n;
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
     const float2 *A = Ab + bidx * g.sA;
     const float2 *B = Bb + bidx * g.sB;
-    fa = gat ? A + g.a_roff[fa_ok ? am : 0]
-             : ((g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am);
+    if (a_mode == 1) {
+      fa = A;
+      if constexpr (SHORTK) {  // short tiles: hide the table load behind the current tile
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ro[i] = ro_next[i];
+        amask = amask_next;
+        load_ro(f_work + gridDim.x, ro_next, amask_next);
+      } else {
+        load_ro(f_work, ro, amask);
+      }
+    } else if (a_mode == 2) {
+      const int64_t r0 = mt0 + lg * 32 + (lane >> 1);
+      amask = (r0 < g.M ? 1u : 0u) | (r0 + 16 < g.M ? 2u : 0u);
+      fa = A + r0 * g.lda + 4 * half + 2 * (lane & 1);  // row r0 + 16 is fa + 16 lda
+    } else {
+      fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+      if (!fa_ok) fa = Ab;
+    }
     fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
-    if (!fa_ok) fa = Ab;
     if (!fb_ok) fb = Bb;
   };
   auto fetch = [&](uint32_t slot) {
     if (f_work < total_work) {
       const uint32_t da = rawa0 + slot * L::RAWA_SLOT, db = rawb0 + slot * L::RAWB_SLOT;
-      if (gat) {  // A row base + per-k offsets from the staged table
-        const int64_t k0 = (int64_t)f_kb * KB + 4 * half;
+      const uint32_t dm = rawa_m + slot * L::RAWA_SLOT;
+      if (a_mode == 1) {  // row offsets in registers + per-k offset from the staged table
+        const int64_t kk = (int64_t)f_kb * KB + 4 * half + (lane & 3);
+        const bool kok = kk < g.K;
+        const int32_t c = kok ? s_coff[kk] : 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool ok = fa_ok && k0 + k < g.K;
-          cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + s_coff[k0 + k] : Ab, ok);
+        for (int i = 0; i < 4; ++i) {
+          const bool ok = kok && ((amask >> i) & 1u);
+          cp_async8(dm + i * 128, ok ? fa + ro[i] + c : Ab, ok);
         }
       }
       if (!(k_tail && f_kb == nk - 1)) {
-        if (gat) {
-        } else if (a_vec) {
-          cp_async16(da, fa, fa_ok);
-          cp_async16(da + V2_THREADS * 16, fa + 2, fa_ok);
+        if (a_mode == 1) {
+        } else if (a_mode == 2) {
+          cp_async16(dm, (amask & 1u) ? fa : Ab, amask & 1u);
+          cp_async16(dm + 256, (amask & 2u) ? fa + 16 * g.lda : Ab, (amask >> 1) & 1u);
         } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
@@ -1117,9 +1168,17 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
         const int64_t k0 = (int64_t)f_kb * KB;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          if (gat) break;
+          if (a_mode != 0) break;
           const bool ok = fa_ok && k0 + 4 * half + k < g.K;
           cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
+        }
+        if (a_mode == 2) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = e >> 1, j = e & 1;
+            const bool ok = ((amask >> i) & 1u) && k0 + 4 * half + 2 * (lane & 1) + j < g.K;
+            cp_async8(dm + i * 256 + j * 8, ok ? fa + i * 16 * g.lda + j : Ab, ok);
+          }
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -1127,7 +1186,11 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
           cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
         }
       }
-      if (fa_ok && !gat) fa += KB * a_kstride;
+      if (a_mode == 2) {
+        fa += KB;
+      } else if (a_mode == 0 && fa_ok) {
+        fa += KB * a_kstride;
+      }
       if (fb_ok) fb += KB * b_kstride;
       if (++f_kb == nk) {
         f_kb = 0;
@@ -1262,6 +1325,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
       fetch((q + RAW - 1) & (RAW - 1));
       asm volatile("cp.async.wait_group %0;" ::"n"(RAW - 1) : "memory");
+      if (a_mode != 0) __syncwarp();  // raw A rows were fetched by other lanes of this warp
       const uint32_t s = q & (STAGES - 1);
       if (q >= STAGES) mbar_wait(&bars[s], ((q >> L::LOG_STAGES) + 1) & 1u);
       const uint32_t slot = q & (RAW - 1);
@@ -1396,6 +1460,370 @@ int launch_ws(const GemmArgs &g, cudaStream_t s) {
   const int64_t grid = std::min<int64_t>(tiles * g.batch, (int64_t)sm_count());
   kern<<<(unsigned)grid, V2_THREADS + 32, L::SMEM, s>>>(g, tiles_n, tiles);
   return check_launch("cgemm_tc3w");
+}
+
+// ---------------------------------------------------------------------------
+// Short-K twin of tc3w (K <= 256: one TMEM accumulation per tile, no
+// promotion).  Differences that matter for the batched small-tile GEMMs of
+// the amplitude batch (e.g. 1024 x (4096 x 64 x 64)):
+//   * each CTA walks a contiguous run of tiles, M tile fastest, so
+//     consecutive tiles share one B panel; when the k-block count divides
+//     the stage ring, stage s holds the same B k-block for every tile of the
+//     run and the B' planes are fetched and split once per run -- a tile
+//     then only streams A (fetch + split + tcgen05.st);
+//   * tile t's epilogue runs after tile t+1's LAST k-block is converted, so
+//     the converters can run a whole tile ahead of the tensor pipe;
+//   * 32-bit tile arithmetic, gathered row offsets prefetched a tile ahead.
+template <int STAGES, int RAW>
+__global__ void __launch_bounds__(V2_THREADS + 32, 1)
+    cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
+                      uint32_t total, uint32_t chunk) {
+  using L = LayoutV3<STAGES, 4, RAW>;
+  constexpr int BN = L::BN;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
+  uint64_t *pbar = bars + STAGES;                                    // [2] tile accumulated
+  uint64_t *full = pbar + 2;                                         // [STAGES] stage converted
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + STAGES);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int lg = warp & 3, half = warp >> 2;
+  const int row_l = lg * 32 + lane;
+  const int b_kp = tid & 1;
+  const int b_n = (tid >> 1) & (BN - 1);
+  const int b_chunk = tid >> 7;
+  const int b_k = b_chunk * 4 + b_kp * 2;
+
+  if (tid == 0) {
+    for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], V2_THREADS / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const bool gat = g.a_roff != nullptr;
+  int32_t *s_coff = reinterpret_cast<int32_t *>(smem + L::COFF_OFF);
+  if (gat)
+    for (int i = tid; i < (int)g.K; i += blockDim.x) s_coff[i] = g.a_coff[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
+  constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
+
+  const uint32_t w0 = blockIdx.x * chunk, w1 = min(total, w0 + chunk);
+  const uint32_t K = (uint32_t)g.K;
+  const uint32_t nk = (K + KB - 1) / KB;
+  // B of tile w sits in the stages iff the tile rd earlier in this run had
+  // the same (batch, N tile) key = w / tiles_m
+  const uint32_t rd = (STAGES % nk == 0) ? STAGES / nk : 0u;
+  auto b_reused = [&](uint32_t w) {
+    return rd != 0u && w >= w0 + rd && (w - rd) / tiles_m == w / tiles_m;
+  };
+
+  if (warp == V2_THREADS / 32) {
+    // ===== MMA issuer (whole warp walks the sequence, one elected lane issues)
+    uint32_t q = 0, t = 0;
+    for (uint32_t w = w0; w < w1; ++w, ++t) {
+      for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+        const uint32_t s = q & (STAGES - 1);
+        mbar_wait(&full[s], (q / STAGES) & 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + (t & 1u) * (uint32_t)L::P_COLS;
+        uint8_t *stage = smem + s * L::STAGE;
+        const uint32_t bhi = smem_u32(stage), blo = smem_u32(stage + L::B_PLANE);
+        const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
+        const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
+        const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
+        const uint32_t acc0 = kb > 0 ? 1u : 0u;
+        if (elect_one()) {
+          mma_ts(d, a + 0, b1h, IDESC, acc0);
+          mma_ts(d, a + 0, b1l, IDESC, 1u);
+          mma_ts(d, a + 8, b1h, IDESC, 1u);
+          mma_ts(d, a + 16, b2h, IDESC, 1u);
+          mma_ts(d, a + 16, b2l, IDESC, 1u);
+          mma_ts(d, a + 24, b2h, IDESC, 1u);
+          mma_commit(&bars[s]);
+          if (kb == nk - 1) mma_commit(&pbar[t & 1u]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 16;
+    const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * 16;
+    const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
+    const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+    const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+    float2 *Cb = reinterpret_cast<float2 *>(g.C);
+    const bool k_tail = (K % KB) != 0;
+    const bool a_vec = (g.opA == QF_OP_N) && (g.lda % 2 == 0) && (g.sA % 2 == 0);
+    const bool b_vec = (g.opB == QF_OP_T) && (g.ldb % 2 == 0) && (g.sB % 2 == 0);
+    const int64_t a_kstride = (g.opA == QF_OP_N) ? 1 : g.lda;
+    const int64_t b_kstride = (g.opB == QF_OP_N) ? g.ldb : 1;
+    // A fetch modes as in tc3w: 1 gathered (lanes along k, 8 B), 2 row-major
+    // (lanes along k, 16 B), 0 lane = row
+    const int a_mode = gat ? 1 : (a_vec ? 2 : 0);
+    const uint32_t rawa_m =
+        smem_u32(smem + L::RAWA_OFF) +
+        (a_mode == 1 ? (uint32_t)(((lane & 3) >> 1) * V2_THREADS * 16 +
+                                  (warp * 32 + (lane >> 2)) * 16 + (lane & 1) * 8)
+                     : (uint32_t)((lane & 1) * V2_THREADS * 16 + (warp * 32 + (lane >> 1)) * 16));
+
+    uint32_t f_w = w0, f_kb = 0;
+    const float2 *fa = Ab, *fb = Bb;
+    bool fa_ok = false, fb_ok = false, f_breuse = false;
+    uint32_t amask = 0, amask_next = 0;
+    int32_t ro[4] = {0, 0, 0, 0}, ro_next[4] = {0, 0, 0, 0};
+    auto load_ro = [&](uint32_t w, int32_t(&dst)[4], uint32_t &mask) {
+      mask = 0;
+      if (w >= w1) return;
+      const int64_t r0 = (int64_t)(w % tiles_m) * BM + lg * 32 + (lane >> 2);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool ok = r0 + 8 * i < g.M;
+        dst[i] = ok ? __ldg(g.a_roff + r0 + 8 * i) : 0;
+        mask |= ok ? (1u << i) : 0u;
+      }
+    };
+    auto fetch_setup = [&]() {
+      if (f_w >= w1) return;
+      const uint32_t key = f_w / tiles_m, mt = f_w - key * tiles_m;
+      const uint32_t bidx = key / tiles_n, nt = key - bidx * tiles_n;
+      const float2 *A = Ab + (int64_t)bidx * g.sA;
+      const float2 *B = Bb + (int64_t)bidx * g.sB;
+      const int64_t m0 = (int64_t)mt * BM;
+      if (a_mode == 1) {
+        fa = A;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ro[i] = ro_next[i];
+        amask = amask_next;
+        load_ro(f_w + 1, ro_next, amask_next);
+      } else if (a_mode == 2) {
+        const int64_t r0 = m0 + lg * 32 + (lane >> 1);
+        amask = (r0 < g.M ? 1u : 0u) | (r0 + 16 < g.M ? 2u : 0u);
+        fa = A + r0 * g.lda + 4 * half + 2 * (lane & 1);
+      } else {
+        const int64_t am = m0 + row_l;
+        fa_ok = am < g.M;
+        fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+        if (!fa_ok) fa = Ab;
+      }
+      f_breuse = b_reused(f_w);
+      const int64_t bn = (int64_t)nt * BN + b_n;
+      fb_ok = bn < g.N;
+      fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
+      if (!fb_ok) fb = Bb;
+    };
+    auto fetch = [&](uint32_t slot) {
+      if (f_w < w1) {
+        const bool tail = k_tail && f_kb == nk - 1;
+        const uint32_t dm = rawa_m + slot * L::RAWA_SLOT;
+        if (a_mode == 1) {
+          const uint32_t kk = f_kb * KB + 4 * half + (lane & 3);
+          const bool kok = kk < K;
+          const int32_t c = kok ? s_coff[kk] : 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const bool ok = kok && ((amask >> i) & 1u);
+            cp_async8(dm + i * 128, ok ? fa + ro[i] + c : Ab, ok);
+          }
+        } else if (a_mode == 2) {
+          if (!tail) {
+            cp_async16(dm, (amask & 1u) ? fa : Ab, amask & 1u);
+            cp_async16(dm + 256, (amask & 2u) ? fa + 16 * g.lda : Ab, (amask >> 1) & 1u);
+          } else {
+            const uint32_t k0 = f_kb * KB + 4 * half + 2 * (lane & 1);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = e >> 1, j = e & 1;
+              const bool ok = ((amask >> i) & 1u) && k0 + j < K;
+              cp_async8(dm + i * 256 + j * 8, ok ? fa + i * 16 * g.lda + j : Ab, ok);
+            }
+          }
+          fa += KB;
+        } else {
+          const uint32_t da = rawa0 + slot * L::RAWA_SLOT;
+          const uint32_t k0 = f_kb * KB + 4 * half;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool ok = fa_ok && (!tail || k0 + k < K);
+            cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
+          }
+          if (fa_ok) fa += KB * a_kstride;
+        }
+        if (!f_breuse) {
+          const uint32_t db = rawb0 + slot * L::RAWB_SLOT;
+          if (!tail) {
+            if (b_vec) {
+              cp_async16(db, fb, fb_ok);
+            } else {
+              cp_async8(db, fb, fb_ok);
+              cp_async8(db + 8, fb + b_kstride, fb_ok);
+            }
+          } else {
+            const uint32_t k0 = f_kb * KB + b_k;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = fb_ok && k0 + e < K;
+              cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
+            }
+          }
+          if (fb_ok) fb += KB * b_kstride;
+        }
+        if (++f_kb == nk) {
+          f_kb = 0;
+          ++f_w;
+          fetch_setup();
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");  // uniform group count
+    };
+
+    auto epilogue = [&](uint32_t w, uint32_t t) {
+      const uint32_t pb = t & 1u;
+      mbar_wait(&pbar[pb], (t >> 1) & 1u);
+      tc_fence_after();
+      uint32_t vr[32], vi[32];
+      const uint32_t base = tmem + lane_base + pb * (uint32_t)L::P_COLS + 32u * half;
+      tmem_ld32(base, vr);
+      tmem_ld32(base + BN, vi);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      const uint32_t key = w / tiles_m, mt = w - key * tiles_m;
+      const uint32_t bidx = key / tiles_n, nt = key - bidx * tiles_n;
+      const int64_t row = (int64_t)mt * BM + row_l;
+      if (row < g.M) {
+        const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+        const bool use_beta = (br != 0.f || bi != 0.f);
+        const int64_t c0 = (int64_t)nt * BN + 32 * half;
+        float2 *crow = Cb + (int64_t)bidx * g.sC + row * g.ldc + c0;
+        const int64_t ncols = min((int64_t)32, g.N - c0);
+        if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && (((uintptr_t)crow) & 15) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2)
+            *reinterpret_cast<float4 *>(crow + j) =
+                make_float4(__uint_as_float(vr[j]), __uint_as_float(vi[j]),
+                            __uint_as_float(vr[j + 1]), __uint_as_float(vi[j + 1]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j < ncols) {
+              const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
+              float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
+              if (use_beta) {
+                const float2 c = crow[j];
+                o.x += br * c.x - bi * c.y;
+                o.y += br * c.y + bi * c.x;
+              }
+              crow[j] = o;
+            }
+          }
+        }
+      }
+    };
+
+    if (a_mode == 1) load_ro(w0, ro_next, amask_next);
+    fetch_setup();
+    for (int i = 0; i < RAW - 1; ++i) fetch((uint32_t)i);
+    uint32_t q = 0, t = 0;
+    for (uint32_t w = w0; w < w1; ++w, ++t) {
+      const bool breuse = b_reused(w);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+        fetch((q + RAW - 1) & (RAW - 1));
+        asm volatile("cp.async.wait_group %0;" ::"n"(RAW - 1) : "memory");
+        if (a_mode != 0) __syncwarp();  // raw A rows were fetched by other lanes of this warp
+        const uint32_t s = q & (STAGES - 1);
+        if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
+        const uint32_t slot = q & (RAW - 1);
+        const float4 a01 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
+                                                              slot * L::RAWA_SLOT + tid * 16);
+        const float4 a23 = *reinterpret_cast<const float4 *>(
+            smem + L::RAWA_OFF + slot * L::RAWA_SLOT + V2_THREADS * 16 + tid * 16);
+        if (!breuse) {
+          const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
+                                                               slot * L::RAWB_SLOT + tid * 16);
+          uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
+          split_fast(bb.x, hr0, lr0);
+          split_fast(bb.y, hi0, li0);
+          split_fast(bb.z, hr1, lr1);
+          split_fast(bb.w, hi1, li1);
+          uint8_t *stage = smem + s * L::STAGE;
+          uint8_t *ph = stage, *pl = stage + L::B_PLANE;
+          *reinterpret_cast<uint2 *>(ph + 0 * L::B_BLOCK + boff) =
+              make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
+          *reinterpret_cast<uint2 *>(ph + 1 * L::B_BLOCK + boff) = make_uint2(hr0, hr1);
+          *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
+          *reinterpret_cast<uint2 *>(pl + 0 * L::B_BLOCK + boff) =
+              make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
+          *reinterpret_cast<uint2 *>(pl + 1 * L::B_BLOCK + boff) = make_uint2(lr0, lr1);
+          *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(li0, li1);
+          fence_async_smem();
+        }
+        {
+          uint32_t rh[4], rl[4], ih[4], il[4];
+          split_fast(a01.x, rh[0], rl[0]);
+          split_fast(a01.y, ih[0], il[0]);
+          split_fast(a01.z, rh[1], rl[1]);
+          split_fast(a01.w, ih[1], il[1]);
+          split_fast(a23.x, rh[2], rl[2]);
+          split_fast(a23.y, ih[2], il[2]);
+          split_fast(a23.z, rh[3], rl[3]);
+          split_fast(a23.w, ih[3], il[3]);
+          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32 + 4 * half);
+          tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+          tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+          tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+          tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        if (kb == nk - 1 && t > 0) epilogue(w - 1, t - 1);
+      }
+    }
+    if (t > 0) epilogue(w1 - 1, t - 1);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(L::TMEM_COLS));
+}
+
+template <int STAGES, int RAW>
+int launch_short(const GemmArgs &g, cudaStream_t s) {
+  using L = LayoutV3<STAGES, 4, RAW>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) {
+      set_error("tc3k: cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    attr = true;
+  }
+  const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + BM - 1) / BM;
+  const int64_t total = tiles_n * tiles_m * g.batch;
+  if (total >= (int64_t)1 << 31) {
+    set_error("tc3k: %lld tiles exceed the 32-bit tile index", (long long)total);
+    return QF_ERR_INVALID;
+  }
+  const int64_t grid0 = std::min<int64_t>(total, (int64_t)sm_count());
+  const int64_t chunk = (total + grid0 - 1) / grid0;
+  const int64_t grid = (total + chunk - 1) / chunk;
+  kern<<<(unsigned)grid, V2_THREADS + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
+                                                         (uint32_t)total, (uint32_t)chunk);
+  return check_launch("cgemm_tc3k");
 }
 
 template <int STAGES, int CK, int RAW>
@@ -2167,8 +2595,12 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   const bool small_n = g.N <= 64;
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
-    return g.K <= 256 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_ws<8, 4, 8, false>(g, s);
+    if (g.K <= 256)
+      return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_short<8, 8>(g, s);
+    return tc::launch_ws<8, 4, 8, false>(g, s);
   }
+  if (g_tc3_variant == 9)
+    return g.K <= 256 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_ws<8, 4, 8, false>(g, s);
   if (g_tc3_variant == 1)
     return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);
   if (g_tc3_variant == 2)
@@ -2184,7 +2616,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
   // double-buffered TMEM accumulators with a deferred epilogue
-  if (g.K <= 256) return tc::launch_ws<8, 4, 8, true>(g, s);
+  if (g.K <= 256) return tc::launch_short<8, 8>(g, s);
   return tc::launch_ws<8, 4, 8, false>(g, s);
 }
 

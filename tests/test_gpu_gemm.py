@@ -92,8 +92,16 @@ TC_SHAPES = [(1, 128, 128, 8), (1, 128, 128, 64), (2, 256, 256, 40), (1, 300, 20
              (3, 4096, 64, 64), (1, 1000, 130, 1000), (4, 512, 64, 8), (1, 129, 257, 3),
              (1, 2048, 2048, 512)]
 
+# short-K runs: B panels kept in the stage ring across consecutive tiles
+# (k-block counts 1/2/4/8, ragged K and M, several N tiles per batch, runs
+# that cross batch boundaries, runs of one tile)
+SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256, 512, 64, 64),
+                 (40, 640, 96, 8), (3, 2048, 128, 24), (7, 384, 64, 200)]
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8], ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4"])
+
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9],
+                ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
+                     "ws-shortk"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -111,6 +119,28 @@ def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
         pytest.skip("v1 variants are exercised at short K only")
     err = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3)
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("shape", SHORTK_SHAPES)
+@pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
+def test_tcgen05_short_k_runs(shape, ops):
+    assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3) < 1e-5
+
+
+def test_gathered_short_k_many_tiles():
+    """Gathered A through the short-K kernel with several M tiles per batch
+    (row offsets prefetched a tile ahead, B reused across the run)."""
+    rng = np.random.default_rng(7)
+    A = _rand(rng, (6, 16, 8, 32, 8), np.complex64)      # @b p s q t
+    B = _rand(rng, (6, 8, 64, 8), np.complex64)          # @b t v s
+    prev = tc.set_gemm_mode("tc3")
+    try:
+        out = tc.contract(tc.Tensor(["@b", "p", "s", "q", "t"], A), tc.Tensor(["@b", "t", "v", "s"], B))
+        got = out.transpose_to(["@b", "p", "q", "v"]).array
+    finally:
+        tc.set_gemm_mode(prev)
+    ref = np.einsum("zpsqt,ztvs->zpqv", A.astype(np.complex128), B.astype(np.complex128))
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
 
 
 @pytest.mark.parametrize("K", [1024, 4096, 32768])
