@@ -1474,11 +1474,39 @@ int launch_ws(const GemmArgs &g, cudaStream_t s) {
 //   * tile t's epilogue runs after tile t+1's LAST k-block is converted, so
 //     the converters can run a whole tile ahead of the tensor pipe;
 //   * 32-bit tile arithmetic, gathered row offsets prefetched a tile ahead.
+// shared memory of the short-K kernel: B' stages, raw A/B rings, a per-warp
+// epilogue staging tile (32 rows x 32 complex, rows padded to 272 B so both
+// the row-per-lane writes and the row-contiguous reads are conflict-free)
+template <int STAGES, int RAW>
+struct LayoutK {
+  static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
+  static constexpr int BN = V2_BN;
+  static constexpr int NP = 2 * BN;
+  static constexpr int B_BLOCK = BN * 32;
+  static constexpr int B_PLANE = 3 * B_BLOCK;
+  static constexpr int STAGE = 2 * B_PLANE;
+  static constexpr int RAWA_SLOT = V2_THREADS * 32;
+  static constexpr int RAWB_SLOT = V2_THREADS * 16;
+  static constexpr int RAWA_OFF = STAGES * STAGE;
+  static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
+  static constexpr int EPI_PITCH = 32 * 8 + 16;
+  static constexpr int EPI_OFF = RAWB_OFF + RAW * RAWB_SLOT;
+  static constexpr int BAR_OFF = EPI_OFF + (V2_THREADS / 32) * 32 * EPI_PITCH;
+  static constexpr int COFF_OFF = BAR_OFF + 1024;
+  static constexpr int COFF_MAX = 256;
+  static constexpr int SMEM = COFF_OFF + 4 * COFF_MAX;
+  static constexpr int P_COLS = NP;
+  static constexpr int A_COL0 = 2 * P_COLS;
+  static constexpr int TMEM_COLS = 512;
+  static_assert(2 * P_COLS + STAGES * 32 <= 512, "TMEM budget");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
 template <int STAGES, int RAW>
 __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk) {
-  using L = LayoutV3<STAGES, 4, RAW>;
+  using L = LayoutK<STAGES, RAW>;
   constexpr int BN = L::BN;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
@@ -1697,32 +1725,45 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       tc_fence_before();
       const uint32_t key = w / tiles_m, mt = w - key * tiles_m;
       const uint32_t bidx = key / tiles_n, nt = key - bidx * tiles_n;
-      const int64_t row = (int64_t)mt * BM + row_l;
-      if (row < g.M) {
-        const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
-        const bool use_beta = (br != 0.f || bi != 0.f);
-        const int64_t c0 = (int64_t)nt * BN + 32 * half;
-        float2 *crow = Cb + (int64_t)bidx * g.sC + row * g.ldc + c0;
-        const int64_t ncols = min((int64_t)32, g.N - c0);
-        if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && (((uintptr_t)crow) & 15) == 0) {
+      const int64_t m0 = (int64_t)mt * BM + lg * 32;  // this warp's 32 rows
+      const int64_t c0 = (int64_t)nt * BN + 32 * half;
+      const int64_t ncols = min((int64_t)32, g.N - c0);
+      const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+      const bool use_beta = (br != 0.f || bi != 0.f);
+      float2 *cw = Cb + (int64_t)bidx * g.sC + m0 * g.ldc + c0;
+      if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && g.ldc % 2 == 0 &&
+          (((uintptr_t)cw) & 15) == 0) {
+        // transpose through the warp's staging tile: each store instruction
+        // then writes two whole 256-byte row segments
+        uint8_t *stg = smem + L::EPI_OFF + warp * 32 * L::EPI_PITCH;
 #pragma unroll
-          for (int j = 0; j < 32; j += 2)
-            *reinterpret_cast<float4 *>(crow + j) =
-                make_float4(__uint_as_float(vr[j]), __uint_as_float(vi[j]),
-                            __uint_as_float(vr[j + 1]), __uint_as_float(vi[j + 1]));
-        } else {
+        for (int j = 0; j < 16; ++j)
+          *reinterpret_cast<float4 *>(stg + lane * L::EPI_PITCH + j * 16) =
+              make_float4(__uint_as_float(vr[2 * j]), __uint_as_float(vi[2 * j]),
+                          __uint_as_float(vr[2 * j + 1]), __uint_as_float(vi[2 * j + 1]));
+        __syncwarp();
+        const int rs = lane >> 4, cc = lane & 15;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (j < ncols) {
-              const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
-              float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
-              if (use_beta) {
-                const float2 c = crow[j];
-                o.x += br * c.x - bi * c.y;
-                o.y += br * c.y + bi * c.x;
-              }
-              crow[j] = o;
+        for (int i = 0; i < 16; ++i) {
+          const int r = 2 * i + rs;
+          if (m0 + r < g.M)
+            *reinterpret_cast<float4 *>(cw + r * g.ldc + 2 * cc) =
+                *reinterpret_cast<const float4 *>(stg + r * L::EPI_PITCH + cc * 16);
+        }
+        __syncwarp();
+      } else if (m0 + lane < g.M) {
+        float2 *crow = cw + (int64_t)lane * g.ldc;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j < ncols) {
+            const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
+            float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
+            if (use_beta) {
+              const float2 c = crow[j];
+              o.x += br * c.x - bi * c.y;
+              o.y += br * c.y + bi * c.x;
             }
+            crow[j] = o;
           }
         }
       }
@@ -1801,7 +1842,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
 
 template <int STAGES, int RAW>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutV3<STAGES, 4, RAW>;
+  using L = LayoutK<STAGES, RAW>;
   auto kern = cgemm_tc3k_kernel<STAGES, RAW>;
   static bool attr = false;
   if (!attr) {
@@ -1811,6 +1852,10 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
       return QF_ERR_CUDA;
     }
     attr = true;
+  }
+  if (g.K > L::COFF_MAX) {
+    set_error("tc3k: K = %lld exceeds the short-K limit %d", (long long)g.K, L::COFF_MAX);
+    return QF_ERR_INVALID;
   }
   const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + BM - 1) / BM;
   const int64_t total = tiles_n * tiles_m * g.batch;
@@ -2585,8 +2630,9 @@ static int g_tc3_variant = 0;
 bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
 
 bool tc3_eligible(const GemmArgs &g) {
-  // a 128 x 64 tile reasonably full, K long enough to amortise the pipeline
-  return g.M >= 128 && g.N >= 32 && g.K >= 32 && g.M * g.N * g.batch >= 128 * 64 * 148;
+  // a 128 x 64 tile reasonably full and enough tiles for the machine; short
+  // K is fine (the short-K kernel streams A once and keeps B resident)
+  return g.M >= 128 && g.N >= 32 && g.K >= 1 && g.M * g.N * g.batch >= 128 * 64 * 148;
 }
 
 int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
@@ -2596,7 +2642,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
     if (g.K <= 256)
-      return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_short<8, 8>(g, s);
+      return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_short<8, 4>(g, s);
     return tc::launch_ws<8, 4, 8, false>(g, s);
   }
   if (g_tc3_variant == 9)
@@ -2616,7 +2662,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
   // double-buffered TMEM accumulators with a deferred epilogue
-  if (g.K <= 256) return tc::launch_short<8, 8>(g, s);
+  if (g.K <= 256) return tc::launch_short<8, 4>(g, s);
   return tc::launch_ws<8, 4, 8, false>(g, s);
 }
 
