@@ -1472,26 +1472,58 @@ int launch_ws(const GemmArgs &g, cudaStream_t s) {
 //     run and the B' planes are fetched and split once per run -- a tile
 //     then only streams A (fetch + split + tcgen05.st);
 //   * tile t's epilogue runs after tile t+1's LAST k-block is converted, so
-//     the converters can run a whole tile ahead of the tensor pipe;
+//     the converters can run a whole tile ahead of the tensor pipe, and it
+//     goes through a per-warp staging tile so every store instruction
+//     writes whole row segments;
+//   * NW converter warps (8 or 16): NW/4 warps share each 32-lane TMEM
+//     quadrant and split the k-block's 8 k (and the epilogue's 64 columns)
+//     between them -- 16 warps hide twice the latency of 8;
 //   * 32-bit tile arithmetic, gathered row offsets prefetched a tile ahead.
+
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t a, uint32_t b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+template <int CPW>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[CPW]) {
+  if constexpr (CPW == 32) tmem_ld32(taddr, v);
+  else tmem_ld16(taddr, v);
+}
+
 // shared memory of the short-K kernel: B' stages, raw A/B rings, a per-warp
-// epilogue staging tile (32 rows x 32 complex, rows padded to 272 B so both
+// epilogue staging tile (32 rows x CPW complex, rows padded by 16 B so both
 // the row-per-lane writes and the row-contiguous reads are conflict-free)
-template <int STAGES, int RAW>
+template <int STAGES, int RAW, int NW>
 struct LayoutK {
   static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
+  static_assert(NW == 8 || NW == 16, "8 or 16 converter warps");
+  static constexpr int NT = NW * 32;                 // converter threads
+  static constexpr int NWG = NW / 4;                 // warps per TMEM lane quadrant
+  static constexpr int KPW = KB / NWG;               // k of a k-block per warp
   static constexpr int BN = V2_BN;
+  static constexpr int CPW = BN / NWG;               // epilogue columns per warp
   static constexpr int NP = 2 * BN;
   static constexpr int B_BLOCK = BN * 32;
   static constexpr int B_PLANE = 3 * B_BLOCK;
   static constexpr int STAGE = 2 * B_PLANE;
-  static constexpr int RAWA_SLOT = V2_THREADS * 32;
-  static constexpr int RAWB_SLOT = V2_THREADS * 16;
+  static constexpr int RAWA_SLOT = NT * KPW * 8;     // 8 KB: 128 rows x 8 complex
+  static constexpr int RAWB_SLOT = BN * KB * 8;      // 4 KB: 64 columns x 8 complex
   static constexpr int RAWA_OFF = STAGES * STAGE;
   static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
-  static constexpr int EPI_PITCH = 32 * 8 + 16;
+  static constexpr int EPI_PITCH = CPW * 8 + 16;
   static constexpr int EPI_OFF = RAWB_OFF + RAW * RAWB_SLOT;
-  static constexpr int BAR_OFF = EPI_OFF + (V2_THREADS / 32) * 32 * EPI_PITCH;
+  static constexpr int BAR_OFF = EPI_OFF + NW * 32 * EPI_PITCH;
   static constexpr int COFF_OFF = BAR_OFF + 1024;
   static constexpr int COFF_MAX = 256;
   static constexpr int SMEM = COFF_OFF + 4 * COFF_MAX;
@@ -1502,12 +1534,12 @@ struct LayoutK {
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-template <int STAGES, int RAW>
-__global__ void __launch_bounds__(V2_THREADS + 32, 1)
+template <int STAGES, int RAW, int NW>
+__global__ void __launch_bounds__(NW * 32 + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk) {
-  using L = LayoutK<STAGES, RAW>;
-  constexpr int BN = L::BN;
+  using L = LayoutK<STAGES, RAW, NW>;
+  constexpr int BN = L::BN, NT = L::NT, KPW = L::KPW, CPW = L::CPW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
   uint64_t *pbar = bars + STAGES;                                    // [2] tile accumulated
@@ -1515,16 +1547,12 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + STAGES);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int lg = warp & 3, half = warp >> 2;
+  const int lg = warp & 3, wg = warp >> 2;
   const int row_l = lg * 32 + lane;
-  const int b_kp = tid & 1;
-  const int b_n = (tid >> 1) & (BN - 1);
-  const int b_chunk = tid >> 7;
-  const int b_k = b_chunk * 4 + b_kp * 2;
 
   if (tid == 0) {
     for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], V2_THREADS / 32);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], NW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1547,14 +1575,11 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
   const uint32_t w0 = blockIdx.x * chunk, w1 = min(total, w0 + chunk);
   const uint32_t K = (uint32_t)g.K;
   const uint32_t nk = (K + KB - 1) / KB;
-  // B of tile w sits in the stages iff the tile rd earlier in this run had
-  // the same (batch, N tile) key = w / tiles_m
+  // B of a tile sits in the stages iff the tile rd earlier in this run had
+  // the same (batch, N tile) key, i.e. >= rd tiles of the key precede it here
   const uint32_t rd = (STAGES % nk == 0) ? STAGES / nk : 0u;
-  auto b_reused = [&](uint32_t w) {
-    return rd != 0u && w >= w0 + rd && (w - rd) / tiles_m == w / tiles_m;
-  };
 
-  if (warp == V2_THREADS / 32) {
+  if (warp == NW) {
     // ===== MMA issuer (whole warp walks the sequence, one elected lane issues)
     uint32_t q = 0, t = 0;
     for (uint32_t w = w0; w < w1; ++w, ++t) {
@@ -1583,9 +1608,6 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       }
     }
   } else {
-    const uint32_t rawa0 = smem_u32(smem + L::RAWA_OFF) + (uint32_t)tid * 16;
-    const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * 16;
-    const uint32_t boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
     const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
     const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
     float2 *Cb = reinterpret_cast<float2 *>(g.C);
@@ -1594,158 +1616,247 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     const bool b_vec = (g.opB == QF_OP_T) && (g.ldb % 2 == 0) && (g.sB % 2 == 0);
     const int64_t a_kstride = (g.opA == QF_OP_N) ? 1 : g.lda;
     const int64_t b_kstride = (g.opB == QF_OP_N) ? g.ldb : 1;
-    // A fetch modes as in tc3w: 1 gathered (lanes along k, 8 B), 2 row-major
-    // (lanes along k, 16 B), 0 lane = row
-    const int a_mode = gat ? 1 : (a_vec ? 2 : 0);
-    const uint32_t rawa_m =
-        smem_u32(smem + L::RAWA_OFF) +
-        (a_mode == 1 ? (uint32_t)(((lane & 3) >> 1) * V2_THREADS * 16 +
-                                  (warp * 32 + (lane >> 2)) * 16 + (lane & 1) * 8)
-                     : (uint32_t)((lane & 1) * V2_THREADS * 16 + (warp * 32 + (lane >> 1)) * 16));
+    const uint32_t kw0 = (uint32_t)(wg * KPW);  // this warp's first k inside a k-block
 
-    uint32_t f_w = w0, f_kb = 0;
+    // ---- A fetch.  The converter lane of TMEM row r needs row r's KPW k values.
+    //   1 gathered, k contiguous : lanes along k (kq = lane % KPW), rows
+    //                              lane/KPW + (32/KPW) i, 8 B each
+    //   3 gathered, rows contiguous (the innermost memory axis is a row
+    //                              label): lane = row, KPW 8-byte loads
+    //   2 row-major: lanes along k pairs (kp = lane % CPR), rows lane/CPR + (32/CPR) i, 16 B
+    //   0 otherwise: lane = row, KPW 8-byte loads
+    // Raw slot: thread t's k pair p at p * NT * 16 + t * 16.
+    constexpr int CPR = KPW / 2;
+    const bool rows_unit = gat && g.M > 1 && __ldg(g.a_roff + 1) - __ldg(g.a_roff) == 1;
+    const int a_mode = gat ? (rows_unit ? 3 : 1) : (a_vec ? 2 : 0);
+    const uint32_t rawa_base = smem_u32(smem + L::RAWA_OFF);
+    const uint32_t rawa_m =
+        rawa_base + (a_mode == 1 ? (uint32_t)(((lane % KPW) >> 1) * NT * 16 +
+                                              (warp * 32 + lane / KPW) * 16 + (lane & 1) * 8)
+                                 : (uint32_t)((lane % CPR) * NT * 16 + (warp * 32 + lane / CPR) * 16));
+    const uint32_t rawa0 = rawa_base + (uint32_t)tid * 16;
+    // ---- B fetch: NW = 8 -> 2 consecutive k of one column per thread (16 B);
+    // NW = 16 -> one element per thread, k fastest
+    int b_n, b_k;
+    uint32_t boff;
+    if constexpr (NW == 8) {
+      const int b_kp = tid & 1, b_chunk = tid >> 7;
+      b_n = (tid >> 1) & (BN - 1);
+      b_k = b_chunk * 4 + b_kp * 2;
+      boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
+    } else {
+      b_k = tid & 7;
+      b_n = tid >> 3;
+      boff = core_off(b_n, b_k >> 2) + (uint32_t)((b_k & 3) * 4);
+    }
+    constexpr int BE = 512 / NT;  // B elements per thread per k-block
+    const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * (8 * BE);
+
+    // tile cursors advance incrementally (M tile fastest, then N tile, batch);
+    // `run` = tiles of the current (batch, N tile) key before this one here
+    struct Cur {
+      uint32_t w, mt, nt, bidx, run;
+    };
+    auto cur_init = [&](Cur &c, uint32_t w) {
+      c.w = w;
+      const uint32_t key = w / tiles_m;
+      c.mt = w - key * tiles_m;
+      c.bidx = key / tiles_n;
+      c.nt = key - c.bidx * tiles_n;
+      c.run = 0;
+    };
+    auto cur_next = [&](Cur &c) {
+      ++c.w;
+      ++c.run;
+      if (++c.mt == tiles_m) {
+        c.mt = 0;
+        c.run = 0;
+        if (++c.nt == tiles_n) {
+          c.nt = 0;
+          ++c.bidx;
+        }
+      }
+    };
+
+    Cur fc;
+    cur_init(fc, w0);
+    uint32_t f_kb = 0;
     const float2 *fa = Ab, *fb = Bb;
     bool fa_ok = false, fb_ok = false, f_breuse = false;
     uint32_t amask = 0, amask_next = 0;
-    int32_t ro[4] = {0, 0, 0, 0}, ro_next[4] = {0, 0, 0, 0};
-    auto load_ro = [&](uint32_t w, int32_t(&dst)[4], uint32_t &mask) {
-      mask = 0;
-      if (w >= w1) return;
-      const int64_t r0 = (int64_t)(w % tiles_m) * BM + lg * 32 + (lane >> 2);
+    int32_t ro[KPW], ro_next[KPW];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const bool ok = r0 + 8 * i < g.M;
-        dst[i] = ok ? __ldg(g.a_roff + r0 + 8 * i) : 0;
-        mask |= ok ? (1u << i) : 0u;
+    for (int i = 0; i < KPW; ++i) ro[i] = ro_next[i] = 0;
+    // gathered row offsets of M tile mt (clamped loads: the value lands in its
+    // register without a predicated copy, so the prefetch really overlaps)
+    auto load_ro = [&](uint32_t mt, int32_t(&dst)[KPW], uint32_t &mask) {
+      mask = 0;
+      const int64_t mlast = g.M - 1;
+      if (a_mode == 3) {
+        const int64_t r = (int64_t)mt * BM + row_l;
+        dst[0] = __ldg(g.a_roff + min(r, mlast));
+        mask = r <= mlast ? 1u : 0u;
+        return;
+      }
+      const int64_t r0 = (int64_t)mt * BM + lg * 32 + lane / KPW;
+#pragma unroll
+      for (int i = 0; i < KPW; ++i) {
+        const int64_t r = r0 + (32 / KPW) * i;
+        dst[i] = __ldg(g.a_roff + min(r, mlast));
+        mask |= r <= mlast ? (1u << i) : 0u;
       }
     };
     auto fetch_setup = [&]() {
-      if (f_w >= w1) return;
-      const uint32_t key = f_w / tiles_m, mt = f_w - key * tiles_m;
-      const uint32_t bidx = key / tiles_n, nt = key - bidx * tiles_n;
-      const float2 *A = Ab + (int64_t)bidx * g.sA;
-      const float2 *B = Bb + (int64_t)bidx * g.sB;
-      const int64_t m0 = (int64_t)mt * BM;
-      if (a_mode == 1) {
-        fa = A;
+      if (fc.w >= w1) return;
+      const float2 *A = Ab + (int64_t)fc.bidx * g.sA;
+      const float2 *B = Bb + (int64_t)fc.bidx * g.sB;
+      const int64_t m0 = (int64_t)fc.mt * BM;
+      if (a_mode == 1 || a_mode == 3) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) ro[i] = ro_next[i];
+        for (int i = 0; i < KPW; ++i) ro[i] = ro_next[i];
         amask = amask_next;
-        load_ro(f_w + 1, ro_next, amask_next);
+        fa = a_mode == 3 ? A + ro[0] : A;
+        if (fc.w + 1 < w1) load_ro(fc.mt + 1 == tiles_m ? 0u : fc.mt + 1, ro_next, amask_next);
       } else if (a_mode == 2) {
-        const int64_t r0 = m0 + lg * 32 + (lane >> 1);
-        amask = (r0 < g.M ? 1u : 0u) | (r0 + 16 < g.M ? 2u : 0u);
-        fa = A + r0 * g.lda + 4 * half + 2 * (lane & 1);
+        const int64_t r0 = m0 + lg * 32 + lane / CPR;
+        amask = 0;
+#pragma unroll
+        for (int i = 0; i < CPR; ++i) amask |= (r0 + (32 / CPR) * i < g.M) ? (1u << i) : 0u;
+        fa = A + r0 * g.lda + kw0 + 2 * (lane % CPR);
       } else {
         const int64_t am = m0 + row_l;
         fa_ok = am < g.M;
-        fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
+        fa = (g.opA == QF_OP_N) ? A + am * g.lda + kw0 : A + (int64_t)kw0 * g.lda + am;
         if (!fa_ok) fa = Ab;
       }
-      f_breuse = b_reused(f_w);
-      const int64_t bn = (int64_t)nt * BN + b_n;
+      f_breuse = rd != 0u && fc.run >= rd;
+      const int64_t bn = (int64_t)fc.nt * BN + b_n;
       fb_ok = bn < g.N;
       fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
       if (!fb_ok) fb = Bb;
     };
     auto fetch = [&](uint32_t slot) {
-      if (f_w < w1) {
+      if (fc.w < w1) {
         const bool tail = k_tail && f_kb == nk - 1;
         const uint32_t dm = rawa_m + slot * L::RAWA_SLOT;
-        if (a_mode == 1) {
-          const uint32_t kk = f_kb * KB + 4 * half + (lane & 3);
-          const bool kok = kk < K;
-          const int32_t c = kok ? s_coff[kk] : 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const bool ok = kok && ((amask >> i) & 1u);
-            cp_async8(dm + i * 128, ok ? fa + ro[i] + c : Ab, ok);
+        const uint32_t kk0 = f_kb * KB + kw0;
+        if (a_mode == 3) {  // lane = row: KPW offsets of this warp's k from the table
+          const uint32_t da = rawa0 + slot * L::RAWA_SLOT;
+          int32_t c[KPW];
+          if constexpr (KPW == 4) {
+            const int4 v = *reinterpret_cast<const int4 *>(s_coff + kk0);
+            c[0] = v.x; c[1] = v.y; c[2] = v.z; c[3] = v.w;
+          } else {
+            const int2 v = *reinterpret_cast<const int2 *>(s_coff + kk0);
+            c[0] = v.x; c[1] = v.y;
           }
+          if (tail) {
+#pragma unroll
+            for (int k = 0; k < KPW; ++k) c[k] = kk0 + k < K ? c[k] : 0;
+          }
+#pragma unroll
+          for (int k = 0; k < KPW; ++k)
+            cp_async8(da + (k >> 1) * NT * 16 + (k & 1) * 8, fa + c[k],
+                      (amask & 1u) && (!tail || kk0 + k < K));
+        } else if (a_mode == 1) {  // lanes along k, KPW rows each
+          const uint32_t kk = kk0 + (lane % KPW);
+          const bool kok = !tail || kk < K;
+          const int32_t c = s_coff[kok ? kk : 0u];
+#pragma unroll
+          for (int i = 0; i < KPW; ++i)
+            cp_async8(dm + i * (32 / KPW) * 16, fa + (ro[i] + c), kok && ((amask >> i) & 1u));
         } else if (a_mode == 2) {
           if (!tail) {
-            cp_async16(dm, (amask & 1u) ? fa : Ab, amask & 1u);
-            cp_async16(dm + 256, (amask & 2u) ? fa + 16 * g.lda : Ab, (amask >> 1) & 1u);
-          } else {
-            const uint32_t k0 = f_kb * KB + 4 * half + 2 * (lane & 1);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
+            for (int i = 0; i < CPR; ++i) {
+              const bool ok = (amask >> i) & 1u;
+              cp_async16(dm + i * (32 / CPR) * 16, ok ? fa + i * (32 / CPR) * g.lda : Ab, ok);
+            }
+          } else {
+            const uint32_t k0 = kk0 + 2 * (lane % CPR);
+#pragma unroll
+            for (int e = 0; e < 2 * CPR; ++e) {
               const int i = e >> 1, j = e & 1;
               const bool ok = ((amask >> i) & 1u) && k0 + j < K;
-              cp_async8(dm + i * 256 + j * 8, ok ? fa + i * 16 * g.lda + j : Ab, ok);
+              cp_async8(dm + i * (32 / CPR) * 16 + j * 8, ok ? fa + i * (32 / CPR) * g.lda + j : Ab, ok);
             }
           }
           fa += KB;
         } else {
           const uint32_t da = rawa0 + slot * L::RAWA_SLOT;
-          const uint32_t k0 = f_kb * KB + 4 * half;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const bool ok = fa_ok && (!tail || k0 + k < K);
-            cp_async8(da + (k >> 1) * V2_THREADS * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
+          for (int k = 0; k < KPW; ++k) {
+            const bool ok = fa_ok && (!tail || kk0 + k < K);
+            cp_async8(da + (k >> 1) * NT * 16 + (k & 1) * 8, ok ? fa + k * a_kstride : Ab, ok);
           }
           if (fa_ok) fa += KB * a_kstride;
         }
         if (!f_breuse) {
           const uint32_t db = rawb0 + slot * L::RAWB_SLOT;
-          if (!tail) {
-            if (b_vec) {
-              cp_async16(db, fb, fb_ok);
+          const uint32_t k0 = f_kb * KB + b_k;
+          if constexpr (BE == 2) {
+            if (!tail) {
+              if (b_vec) {
+                cp_async16(db, fb, fb_ok);
+              } else {
+                cp_async8(db, fb, fb_ok);
+                cp_async8(db + 8, fb + b_kstride, fb_ok);
+              }
             } else {
-              cp_async8(db, fb, fb_ok);
-              cp_async8(db + 8, fb + b_kstride, fb_ok);
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const bool ok = fb_ok && k0 + e < K;
+                cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
+              }
             }
           } else {
-            const uint32_t k0 = f_kb * KB + b_k;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const bool ok = fb_ok && k0 + e < K;
-              cp_async8(db + 8 * e, ok ? fb + e * b_kstride : Bb, ok);
-            }
+            const bool ok = fb_ok && (!tail || k0 < K);
+            cp_async8(db, ok ? fb : Bb, ok);
           }
           if (fb_ok) fb += KB * b_kstride;
         }
         if (++f_kb == nk) {
           f_kb = 0;
-          ++f_w;
+          cur_next(fc);
           fetch_setup();
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");  // uniform group count
     };
 
-    auto epilogue = [&](uint32_t w, uint32_t t) {
+    auto epilogue = [&](uint32_t mt, uint32_t nt, uint32_t bidx, uint32_t t) {
       const uint32_t pb = t & 1u;
       mbar_wait(&pbar[pb], (t >> 1) & 1u);
       tc_fence_after();
-      uint32_t vr[32], vi[32];
-      const uint32_t base = tmem + lane_base + pb * (uint32_t)L::P_COLS + 32u * half;
-      tmem_ld32(base, vr);
-      tmem_ld32(base + BN, vi);
+      uint32_t vr[CPW], vi[CPW];
+      const uint32_t base = tmem + lane_base + pb * (uint32_t)L::P_COLS + (uint32_t)(wg * CPW);
+      tmem_ld_cols<CPW>(base, vr);
+      tmem_ld_cols<CPW>(base + BN, vi);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
-      const uint32_t key = w / tiles_m, mt = w - key * tiles_m;
-      const uint32_t bidx = key / tiles_n, nt = key - bidx * tiles_n;
       const int64_t m0 = (int64_t)mt * BM + lg * 32;  // this warp's 32 rows
-      const int64_t c0 = (int64_t)nt * BN + 32 * half;
-      const int64_t ncols = min((int64_t)32, g.N - c0);
+      const int64_t c0 = (int64_t)nt * BN + wg * CPW;
+      const int64_t ncols = min((int64_t)CPW, g.N - c0);
       const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
       const bool use_beta = (br != 0.f || bi != 0.f);
       float2 *cw = Cb + (int64_t)bidx * g.sC + m0 * g.ldc + c0;
-      if (!use_beta && ncols == 32 && ar == 1.f && ai == 0.f && g.ldc % 2 == 0 &&
+      if (!use_beta && ncols == CPW && ar == 1.f && ai == 0.f && g.ldc % 2 == 0 &&
           (((uintptr_t)cw) & 15) == 0) {
         // transpose through the warp's staging tile: each store instruction
-        // then writes two whole 256-byte row segments
+        // then writes whole CPW*8-byte row segments
         uint8_t *stg = smem + L::EPI_OFF + warp * 32 * L::EPI_PITCH;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < CPW / 2; ++j)
           *reinterpret_cast<float4 *>(stg + lane * L::EPI_PITCH + j * 16) =
               make_float4(__uint_as_float(vr[2 * j]), __uint_as_float(vi[2 * j]),
                           __uint_as_float(vr[2 * j + 1]), __uint_as_float(vi[2 * j + 1]));
         __syncwarp();
-        const int rs = lane >> 4, cc = lane & 15;
+        constexpr int LPR = CPW / 2;    // lanes per row segment
+        constexpr int RPI = 32 / LPR;   // rows per store instruction
+        const int rs = lane / LPR, cc = lane % LPR;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int r = 2 * i + rs;
+        for (int i = 0; i < 32 / RPI; ++i) {
+          const int r = RPI * i + rs;
           if (m0 + r < g.M)
             *reinterpret_cast<float4 *>(cw + r * g.ldc + 2 * cc) =
                 *reinterpret_cast<const float4 *>(stg + r * L::EPI_PITCH + cc * 16);
@@ -1754,7 +1865,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       } else if (m0 + lane < g.M) {
         float2 *crow = cw + (int64_t)lane * g.ldc;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < CPW; ++j) {
           if (j < ncols) {
             const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
             float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
@@ -1769,68 +1880,95 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
       }
     };
 
-    if (a_mode == 1) load_ro(w0, ro_next, amask_next);
+    if ((a_mode == 1 || a_mode == 3) && w0 < w1) load_ro(fc.mt, ro_next, amask_next);
     fetch_setup();
     for (int i = 0; i < RAW - 1; ++i) fetch((uint32_t)i);
+    Cur cc;
+    cur_init(cc, w0);
+    uint32_t pmt = 0, pnt = 0, pbidx = 0;  // the previous tile (its epilogue is pending)
     uint32_t q = 0, t = 0;
-    for (uint32_t w = w0; w < w1; ++w, ++t) {
-      const bool breuse = b_reused(w);
+    for (; cc.w < w1; cur_next(cc), ++t) {
+      const bool breuse = rd != 0u && cc.run >= rd;
       for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
         fetch((q + RAW - 1) & (RAW - 1));
         asm volatile("cp.async.wait_group %0;" ::"n"(RAW - 1) : "memory");
-        if (a_mode != 0) __syncwarp();  // raw A rows were fetched by other lanes of this warp
+        if (a_mode == 1 || a_mode == 2) __syncwarp();  // rows fetched by other lanes of this warp
         const uint32_t s = q & (STAGES - 1);
         if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
         const uint32_t slot = q & (RAW - 1);
-        const float4 a01 = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF +
-                                                              slot * L::RAWA_SLOT + tid * 16);
-        const float4 a23 = *reinterpret_cast<const float4 *>(
-            smem + L::RAWA_OFF + slot * L::RAWA_SLOT + V2_THREADS * 16 + tid * 16);
+        float4 av[CPR];
+#pragma unroll
+        for (int p = 0; p < CPR; ++p)
+          av[p] = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF + slot * L::RAWA_SLOT +
+                                                     p * NT * 16 + tid * 16);
         if (!breuse) {
-          const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
-                                                               slot * L::RAWB_SLOT + tid * 16);
-          uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
-          split_fast(bb.x, hr0, lr0);
-          split_fast(bb.y, hi0, li0);
-          split_fast(bb.z, hr1, lr1);
-          split_fast(bb.w, hi1, li1);
           uint8_t *stage = smem + s * L::STAGE;
           uint8_t *ph = stage, *pl = stage + L::B_PLANE;
-          *reinterpret_cast<uint2 *>(ph + 0 * L::B_BLOCK + boff) =
-              make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
-          *reinterpret_cast<uint2 *>(ph + 1 * L::B_BLOCK + boff) = make_uint2(hr0, hr1);
-          *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
-          *reinterpret_cast<uint2 *>(pl + 0 * L::B_BLOCK + boff) =
-              make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
-          *reinterpret_cast<uint2 *>(pl + 1 * L::B_BLOCK + boff) = make_uint2(lr0, lr1);
-          *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(li0, li1);
+          if constexpr (BE == 2) {
+            const float4 bb = *reinterpret_cast<const float4 *>(smem + L::RAWB_OFF +
+                                                                 slot * L::RAWB_SLOT + tid * 16);
+            uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
+            split_fast(bb.x, hr0, lr0);
+            split_fast(bb.y, hi0, li0);
+            split_fast(bb.z, hr1, lr1);
+            split_fast(bb.w, hi1, li1);
+            *reinterpret_cast<uint2 *>(ph + 0 * L::B_BLOCK + boff) =
+                make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
+            *reinterpret_cast<uint2 *>(ph + 1 * L::B_BLOCK + boff) = make_uint2(hr0, hr1);
+            *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
+            *reinterpret_cast<uint2 *>(pl + 0 * L::B_BLOCK + boff) =
+                make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
+            *reinterpret_cast<uint2 *>(pl + 1 * L::B_BLOCK + boff) = make_uint2(lr0, lr1);
+            *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(li0, li1);
+          } else {
+            const float2 bb = *reinterpret_cast<const float2 *>(smem + L::RAWB_OFF +
+                                                                 slot * L::RAWB_SLOT + tid * 8);
+            uint32_t hr, lr, hi, li;
+            split_fast(bb.x, hr, lr);
+            split_fast(bb.y, hi, li);
+            *reinterpret_cast<uint32_t *>(ph + 0 * L::B_BLOCK + boff) = hi ^ 0x80000000u;
+            *reinterpret_cast<uint32_t *>(ph + 1 * L::B_BLOCK + boff) = hr;
+            *reinterpret_cast<uint32_t *>(ph + 2 * L::B_BLOCK + boff) = hi;
+            *reinterpret_cast<uint32_t *>(pl + 0 * L::B_BLOCK + boff) = li ^ 0x80000000u;
+            *reinterpret_cast<uint32_t *>(pl + 1 * L::B_BLOCK + boff) = lr;
+            *reinterpret_cast<uint32_t *>(pl + 2 * L::B_BLOCK + boff) = li;
+          }
           fence_async_smem();
         }
         {
-          uint32_t rh[4], rl[4], ih[4], il[4];
-          split_fast(a01.x, rh[0], rl[0]);
-          split_fast(a01.y, ih[0], il[0]);
-          split_fast(a01.z, rh[1], rl[1]);
-          split_fast(a01.w, ih[1], il[1]);
-          split_fast(a23.x, rh[2], rl[2]);
-          split_fast(a23.y, ih[2], il[2]);
-          split_fast(a23.z, rh[3], rl[3]);
-          split_fast(a23.w, ih[3], il[3]);
-          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32 + 4 * half);
-          tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
-          tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
-          tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
-          tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+          uint32_t rh[KPW], rl[KPW], ih[KPW], il[KPW];
+#pragma unroll
+          for (int p = 0; p < CPR; ++p) {
+            split_fast(av[p].x, rh[2 * p], rl[2 * p]);
+            split_fast(av[p].y, ih[2 * p], il[2 * p]);
+            split_fast(av[p].z, rh[2 * p + 1], rl[2 * p + 1]);
+            split_fast(av[p].w, ih[2 * p + 1], il[2 * p + 1]);
+          }
+          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32) + kw0;
+          if constexpr (KPW == 4) {
+            tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+            tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+            tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+            tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+          } else {
+            tmem_st2(acol + 0, rh[0], rh[1]);
+            tmem_st2(acol + 8, rl[0], rl[1]);
+            tmem_st2(acol + 16, ih[0], ih[1]);
+            tmem_st2(acol + 24, il[0], il[1]);
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
-        if (kb == nk - 1 && t > 0) epilogue(w - 1, t - 1);
+        if (kb == nk - 1 && t > 0) epilogue(pmt, pnt, pbidx, t - 1);
       }
+      pmt = cc.mt;
+      pnt = cc.nt;
+      pbidx = cc.bidx;
     }
-    if (t > 0) epilogue(w1 - 1, t - 1);
+    if (t > 0) epilogue(pmt, pnt, pbidx, t - 1);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
@@ -1840,10 +1978,10 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
                  "r"(L::TMEM_COLS));
 }
 
-template <int STAGES, int RAW>
+template <int STAGES, int RAW, int NW>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutK<STAGES, RAW>;
-  auto kern = cgemm_tc3k_kernel<STAGES, RAW>;
+  using L = LayoutK<STAGES, RAW, NW>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -1866,8 +2004,8 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   const int64_t grid0 = std::min<int64_t>(total, (int64_t)sm_count());
   const int64_t chunk = (total + grid0 - 1) / grid0;
   const int64_t grid = (total + chunk - 1) / chunk;
-  kern<<<(unsigned)grid, V2_THREADS + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
-                                                         (uint32_t)total, (uint32_t)chunk);
+  kern<<<(unsigned)grid, NW * 32 + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
+                                                      (uint32_t)total, (uint32_t)chunk);
   return check_launch("cgemm_tc3k");
 }
 
@@ -2642,7 +2780,9 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
     if (g.K <= 256)
-      return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_short<8, 4>(g, s);
+      return g_tc3_variant == 9    ? tc::launch_ws<8, 4, 8, true>(g, s)
+             : g_tc3_variant == 10 ? tc::launch_short<8, 4, 8>(g, s)
+                                   : tc::launch_short<8, 4, 16>(g, s);
     return tc::launch_ws<8, 4, 8, false>(g, s);
   }
   if (g_tc3_variant == 9)
@@ -2662,7 +2802,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
   // double-buffered TMEM accumulators with a deferred epilogue
-  if (g.K <= 256) return tc::launch_short<8, 4>(g, s);
+  if (g_tc3_variant == 10 && g.K <= 256) return tc::launch_short<8, 4, 8>(g, s);
+  if (g.K <= 256) return tc::launch_short<8, 4, 16>(g, s);
   return tc::launch_ws<8, 4, 8, false>(g, s);
 }
 

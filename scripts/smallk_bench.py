@@ -22,7 +22,8 @@ for (b, M, N, K, oa, ob) in [(1024, 4096, 64, 8, 0, 0), (1024, 512, 512, 8, 1, 1
     C = torch.empty(b * M * N, dtype=torch.complex64, device="cuda")
     byts = 8 * b * (M * K + K * N + M * N)
     row = {}
-    for name, mode in (("simt", 1), ("tc3", 2)):
+    for name, mode, var in (("simt", 1, 0), ("tc3", 2, 0), ("tc3_8w", 2, 10)):
+        _lib.load().qf_tc3_set_variant(var)
         try:
             ms = timeit(lambda: tc.gemm_buffer(b, M, N, K, A, oa, B, ob, C, mode=mode), 5)
             row[name] = f"{ms:.3f} ms {byts / ms / 1e6:.0f} GB/s {8 * b * M * N * K / ms / 1e9:.1f} TF/s"

@@ -99,9 +99,9 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (40, 640, 96, 8), (3, 2048, 128, 24), (7, 384, 64, 200)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10],
                 ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
-                     "ws-shortk"])
+                     "ws-shortk", "short-8warps"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -123,23 +123,40 @@ def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
 
 @pytest.mark.parametrize("shape", SHORTK_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-def test_tcgen05_short_k_runs(shape, ops):
-    assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3) < 1e-5
-
-
-def test_gathered_short_k_many_tiles():
-    """Gathered A through the short-K kernel with several M tiles per batch
-    (row offsets prefetched a tile ahead, B reused across the run)."""
-    rng = np.random.default_rng(7)
-    A = _rand(rng, (6, 16, 8, 32, 8), np.complex64)      # @b p s q t
-    B = _rand(rng, (6, 8, 64, 8), np.complex64)          # @b t v s
-    prev = tc.set_gemm_mode("tc3")
+@pytest.mark.parametrize("variant", [0, 10], ids=["16warps", "8warps"])
+def test_tcgen05_short_k_runs(shape, ops, variant):
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(variant)
     try:
-        out = tc.contract(tc.Tensor(["@b", "p", "s", "q", "t"], A), tc.Tensor(["@b", "t", "v", "s"], B))
+        assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3) < 1e-5
+    finally:
+        lib.qf_tc3_set_variant(prev)
+
+
+@pytest.mark.parametrize("a_labels", [["@b", "p", "s", "q", "t"], ["@b", "s", "q", "t", "p"]],
+                         ids=["k-innermost", "row-innermost"])
+@pytest.mark.parametrize("variant", [0, 10], ids=["16warps", "8warps"])
+def test_gathered_short_k_many_tiles(a_labels, variant):
+    """Gathered A through the short-K kernel with several M tiles per batch
+    (row offsets prefetched a tile ahead, B reused across the run), for both
+    fetch layouts: summed label innermost (lanes along k) and free label
+    innermost (lane = row)."""
+    rng = np.random.default_rng(7)
+    dims = {"@b": 6, "p": 16, "s": 8, "q": 32, "t": 8}
+    A = _rand(rng, tuple(dims[l] for l in a_labels), np.complex64)
+    B = _rand(rng, (6, 8, 64, 8), np.complex64)          # @b t v s
+    lib = _lib.load()
+    prev = tc.set_gemm_mode("tc3")
+    prev_v = lib.qf_tc3_set_variant(variant)
+    try:
+        out = tc.contract(tc.Tensor(a_labels, A), tc.Tensor(["@b", "t", "v", "s"], B))
         got = out.transpose_to(["@b", "p", "q", "v"]).array
     finally:
         tc.set_gemm_mode(prev)
-    ref = np.einsum("zpsqt,ztvs->zpqv", A.astype(np.complex128), B.astype(np.complex128))
+        lib.qf_tc3_set_variant(prev_v)
+    sub = {"@b": "z", "p": "p", "s": "s", "q": "q", "t": "t"}
+    ref = np.einsum("".join(sub[l] for l in a_labels) + ",ztvs->zpqv", A.astype(np.complex128),
+                    B.astype(np.complex128))
     assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5
 
 
