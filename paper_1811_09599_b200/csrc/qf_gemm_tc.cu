@@ -1504,10 +1504,11 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[CPW])
 // shared memory of the short-K kernel: B' stages, raw A/B rings, a per-warp
 // epilogue staging tile (32 rows x CPW complex, rows padded by 16 B so both
 // the row-per-lane writes and the row-contiguous reads are conflict-free)
-template <int STAGES, int RAW, int NW>
+template <int STAGES, int RAW, int NW, int NE>
 struct LayoutK {
   static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
   static_assert(NW == 8 || NW == 16, "8 or 16 converter warps");
+  static_assert(NE == 0 || NE == 4, "epilogue on the converters or 4 epilogue warps");
   static constexpr int NT = NW * 32;                 // converter threads
   static constexpr int NWG = NW / 4;                 // warps per TMEM lane quadrant
   static constexpr int KPW = KB / NWG;               // k of a k-block per warp
@@ -1521,9 +1522,10 @@ struct LayoutK {
   static constexpr int RAWB_SLOT = BN * KB * 8;      // 4 KB: 64 columns x 8 complex
   static constexpr int RAWA_OFF = STAGES * STAGE;
   static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
-  static constexpr int EPI_PITCH = CPW * 8 + 16;
+  static constexpr int EPI_CH = NE ? 16 : CPW;       // columns per staging pass
+  static constexpr int EPI_PITCH = EPI_CH * 8 + 16;
   static constexpr int EPI_OFF = RAWB_OFF + RAW * RAWB_SLOT;
-  static constexpr int BAR_OFF = EPI_OFF + NW * 32 * EPI_PITCH;
+  static constexpr int BAR_OFF = EPI_OFF + (NE ? NE : NW) * 32 * EPI_PITCH;
   static constexpr int COFF_OFF = BAR_OFF + 1024;
   static constexpr int COFF_MAX = 256;
   static constexpr int SMEM = COFF_OFF + 4 * COFF_MAX;
@@ -1534,17 +1536,18 @@ struct LayoutK {
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-template <int STAGES, int RAW, int NW>
-__global__ void __launch_bounds__(NW * 32 + 32, 1)
+template <int STAGES, int RAW, int NW, int NE>
+__global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk) {
-  using L = LayoutK<STAGES, RAW, NW>;
+  using L = LayoutK<STAGES, RAW, NW, NE>;
   constexpr int BN = L::BN, NT = L::NT, KPW = L::KPW, CPW = L::CPW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
   uint64_t *pbar = bars + STAGES;                                    // [2] tile accumulated
   uint64_t *full = pbar + 2;                                         // [STAGES] stage converted
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + STAGES);
+  uint64_t *accfree = full + STAGES;                                 // [2] accumulator drained
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accfree + 2);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int lg = warp & 3, wg = warp >> 2;
@@ -1553,6 +1556,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
   if (tid == 0) {
     for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
     for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], NW);
+    for (int i = 0; i < 2; ++i) mbar_init(&accfree[i], NE ? NE : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1579,7 +1583,34 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
   // the same (batch, N tile) key, i.e. >= rd tiles of the key precede it here
   const uint32_t rd = (STAGES % nk == 0) ? STAGES / nk : 0u;
 
-  if (warp == NW) {
+  // tile cursors advance incrementally (M tile fastest, then N tile, batch);
+  // `run` = tiles of the current (batch, N tile) key before this one here
+  struct Cur {
+    uint32_t w, mt, nt, bidx, run;
+  };
+  auto cur_init = [&](Cur &c, uint32_t w) {
+    c.w = w;
+    const uint32_t key = w / tiles_m;
+    c.mt = w - key * tiles_m;
+    c.bidx = key / tiles_n;
+    c.nt = key - c.bidx * tiles_n;
+    c.run = 0;
+  };
+  auto cur_next = [&](Cur &c) {
+    ++c.w;
+    ++c.run;
+    if (++c.mt == tiles_m) {
+      c.mt = 0;
+      c.run = 0;
+      if (++c.nt == tiles_n) {
+        c.nt = 0;
+        ++c.bidx;
+      }
+    }
+  };
+
+
+  if (warp == NW + NE) {
     // ===== MMA issuer (whole warp walks the sequence, one elected lane issues)
     uint32_t q = 0, t = 0;
     for (uint32_t w = w0; w < w1; ++w, ++t) {
@@ -1594,6 +1625,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
         const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
         const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
         const uint32_t acc0 = kb > 0 ? 1u : 0u;
+        if (NE > 0 && kb == 0 && t >= 2) {  // epilogue warps drained this buffer (tile t-2)
+          mbar_wait(&accfree[t & 1u], ((t >> 1) + 1) & 1u);
+          tc_fence_after();
+        }
         if (elect_one()) {
           mma_ts(d, a + 0, b1h, IDESC, acc0);
           mma_ts(d, a + 0, b1l, IDESC, 1u);
@@ -1605,6 +1640,75 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
           if (kb == nk - 1) mma_commit(&pbar[t & 1u]);
         }
         __syncwarp();
+      }
+    }
+  } else if (NE > 0 && warp >= NW) {
+    // ===== epilogue warps: drain tile t's accumulators while the converters
+    // and the tensor pipe work on tile t+1; columns in passes of 16 through
+    // the warp's staging tile so every store writes whole 128-byte segments
+    float2 *Cb = reinterpret_cast<float2 *>(g.C);
+    const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+    const bool use_beta = (br != 0.f || bi != 0.f);
+    uint8_t *stg = smem + L::EPI_OFF + (warp - NW) * 32 * L::EPI_PITCH;
+    Cur ec;
+    cur_init(ec, w0);
+    for (uint32_t t = 0; ec.w < w1; cur_next(ec), ++t) {
+      const uint32_t pb = t & 1u;
+      mbar_wait(&pbar[pb], (t >> 1) & 1u);
+      tc_fence_after();
+      const int64_t m0 = (int64_t)ec.mt * BM + lg * 32;
+      float2 *cw = Cb + (int64_t)ec.bidx * g.sC + m0 * g.ldc + (int64_t)ec.nt * BN;
+      const int64_t ntile = min((int64_t)BN, g.N - (int64_t)ec.nt * BN);
+      const bool fast = !use_beta && ntile == BN && ar == 1.f && ai == 0.f && g.ldc % 2 == 0 &&
+                        (((uintptr_t)cw) & 15) == 0;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 16; ++ch) {
+        uint32_t vr[16], vi[16];
+        const uint32_t base = tmem + lane_base + pb * (uint32_t)L::P_COLS + (uint32_t)(ch * 16);
+        tmem_ld16(base, vr);
+        tmem_ld16(base + BN, vi);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (ch == BN / 16 - 1) {  // the whole tile is in registers/staging: free the buffer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[pb]))
+                         : "memory");
+        }
+        float2 *cc0 = cw + ch * 16;
+        if (fast) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4 *>(stg + lane * L::EPI_PITCH + j * 16) =
+                make_float4(__uint_as_float(vr[2 * j]), __uint_as_float(vi[2 * j]),
+                            __uint_as_float(vr[2 * j + 1]), __uint_as_float(vi[2 * j + 1]));
+          __syncwarp();
+          const int rs = lane >> 3, cc = lane & 7;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + rs;
+            if (m0 + r < g.M)
+              *reinterpret_cast<float4 *>(cc0 + r * g.ldc + 2 * cc) =
+                  *reinterpret_cast<const float4 *>(stg + r * L::EPI_PITCH + cc * 16);
+          }
+          __syncwarp();
+        } else if (m0 + lane < g.M) {
+          float2 *crow = cc0 + (int64_t)lane * g.ldc;
+          const int64_t ncols = min((int64_t)16, ntile - ch * 16);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < ncols) {
+              const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
+              float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
+              if (use_beta) {
+                const float2 c = crow[j];
+                o.x += br * c.x - bi * c.y;
+                o.y += br * c.y + bi * c.x;
+              }
+              crow[j] = o;
+            }
+          }
+        }
       }
     }
   } else {
@@ -1651,32 +1755,6 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
     }
     constexpr int BE = 512 / NT;  // B elements per thread per k-block
     const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * (8 * BE);
-
-    // tile cursors advance incrementally (M tile fastest, then N tile, batch);
-    // `run` = tiles of the current (batch, N tile) key before this one here
-    struct Cur {
-      uint32_t w, mt, nt, bidx, run;
-    };
-    auto cur_init = [&](Cur &c, uint32_t w) {
-      c.w = w;
-      const uint32_t key = w / tiles_m;
-      c.mt = w - key * tiles_m;
-      c.bidx = key / tiles_n;
-      c.nt = key - c.bidx * tiles_n;
-      c.run = 0;
-    };
-    auto cur_next = [&](Cur &c) {
-      ++c.w;
-      ++c.run;
-      if (++c.mt == tiles_m) {
-        c.mt = 0;
-        c.run = 0;
-        if (++c.nt == tiles_n) {
-          c.nt = 0;
-          ++c.bidx;
-        }
-      }
-    };
 
     Cur fc;
     cur_init(fc, w0);
@@ -1962,13 +2040,13 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
         __syncwarp();
         if (lane == 0)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
-        if (kb == nk - 1 && t > 0) epilogue(pmt, pnt, pbidx, t - 1);
+        if (NE == 0 && kb == nk - 1 && t > 0) epilogue(pmt, pnt, pbidx, t - 1);
       }
       pmt = cc.mt;
       pnt = cc.nt;
       pbidx = cc.bidx;
     }
-    if (t > 0) epilogue(pmt, pnt, pbidx, t - 1);
+    if (NE == 0 && t > 0) epilogue(pmt, pnt, pbidx, t - 1);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
@@ -1978,10 +2056,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1)
                  "r"(L::TMEM_COLS));
 }
 
-template <int STAGES, int RAW, int NW>
+template <int STAGES, int RAW, int NW, int NE>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutK<STAGES, RAW, NW>;
-  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW>;
+  using L = LayoutK<STAGES, RAW, NW, NE>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -2004,7 +2082,7 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   const int64_t grid0 = std::min<int64_t>(total, (int64_t)sm_count());
   const int64_t chunk = (total + grid0 - 1) / grid0;
   const int64_t grid = (total + chunk - 1) / chunk;
-  kern<<<(unsigned)grid, NW * 32 + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
+  kern<<<(unsigned)grid, (NW + NE) * 32 + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
                                                       (uint32_t)total, (uint32_t)chunk);
   return check_launch("cgemm_tc3k");
 }
@@ -2767,6 +2845,19 @@ static int g_tc3_variant = 0;
 
 bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
 
+// short-K kernel flavour: output-bound shapes (K <= 56) keep the epilogue on
+// the converter warps (more store parallelism); longer K hands it to 4
+// dedicated epilogue warps so conversion, MMA and stores overlap.
+// Variants 10/11/12 pin 8 warps / 16 warps / 16 + 4 epilogue warps.
+static int launch_short_auto(const GemmArgs &g, cudaStream_t s) {
+  if (g_tc3_variant == 10) return tc::launch_short<8, 4, 8, 0>(g, s);
+  if (g_tc3_variant == 11) return tc::launch_short<8, 4, 16, 0>(g, s);
+  if (g_tc3_variant == 12) return tc::launch_short<8, 8, 16, 4>(g, s);
+  if (g.K <= 8) return tc::launch_short<8, 4, 8, 0>(g, s);
+  if (g.K <= 56) return tc::launch_short<8, 4, 16, 0>(g, s);
+  return tc::launch_short<8, 8, 16, 4>(g, s);
+}
+
 bool tc3_eligible(const GemmArgs &g) {
   // a 128 x 64 tile reasonably full and enough tiles for the machine; short
   // K is fine (the short-K kernel streams A once and keeps B resident)
@@ -2780,9 +2871,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
     if (g.K <= 256)
-      return g_tc3_variant == 9    ? tc::launch_ws<8, 4, 8, true>(g, s)
-             : g_tc3_variant == 10 ? tc::launch_short<8, 4, 8>(g, s)
-                                   : tc::launch_short<8, 4, 16>(g, s);
+      return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : launch_short_auto(g, s);
     return tc::launch_ws<8, 4, 8, false>(g, s);
   }
   if (g_tc3_variant == 9)
@@ -2802,8 +2891,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return g.K <= 256 ? tc::launch_reg<8, 4, 4, true>(g, s) : tc::launch_reg<8, 4, 4, false>(g, s);
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
   // double-buffered TMEM accumulators with a deferred epilogue
-  if (g_tc3_variant == 10 && g.K <= 256) return tc::launch_short<8, 4, 8>(g, s);
-  if (g.K <= 256) return tc::launch_short<8, 4, 16>(g, s);
+  if (g.K <= 256) return launch_short_auto(g, s);
   return tc::launch_ws<8, 4, 8, false>(g, s);
 }
 

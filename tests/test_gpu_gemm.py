@@ -99,9 +99,9 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (40, 640, 96, 8), (3, 2048, 128, 24), (7, 384, 64, 200)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12],
                 ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
-                     "ws-shortk", "short-8warps"])
+                     "ws-shortk", "short-8warps", "short-16warps", "short-epilogue-warps"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -123,7 +123,7 @@ def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
 
 @pytest.mark.parametrize("shape", SHORTK_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-@pytest.mark.parametrize("variant", [0, 10], ids=["16warps", "8warps"])
+@pytest.mark.parametrize("variant", [10, 11, 12], ids=["8warps", "16warps", "epilogue-warps"])
 def test_tcgen05_short_k_runs(shape, ops, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
@@ -135,7 +135,7 @@ def test_tcgen05_short_k_runs(shape, ops, variant):
 
 @pytest.mark.parametrize("a_labels", [["@b", "p", "s", "q", "t"], ["@b", "s", "q", "t", "p"]],
                          ids=["k-innermost", "row-innermost"])
-@pytest.mark.parametrize("variant", [0, 10], ids=["16warps", "8warps"])
+@pytest.mark.parametrize("variant", [10, 11, 12], ids=["8warps", "16warps", "epilogue-warps"])
 def test_gathered_short_k_many_tiles(a_labels, variant):
     """Gathered A through the short-K kernel with several M tiles per batch
     (row offsets prefetched a tile ahead, B reused across the run), for both
