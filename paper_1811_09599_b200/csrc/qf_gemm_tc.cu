@@ -1495,34 +1495,46 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+
 template <int CPW>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[CPW]) {
   if constexpr (CPW == 32) tmem_ld32(taddr, v);
-  else tmem_ld16(taddr, v);
+  else if constexpr (CPW == 16) tmem_ld16(taddr, v);
+  else if constexpr (CPW == 8) tmem_ld8(taddr, v);
+  else __trap();  // narrower column groups only exist in instantiations that never run them
 }
 
 // shared memory of the short-K kernel: B' stages, raw A/B rings, a per-warp
 // epilogue staging tile (32 rows x CPW complex, rows padded by 16 B so both
 // the row-per-lane writes and the row-contiguous reads are conflict-free)
-template <int STAGES, int RAW, int NW, int NE>
+template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN>
 struct LayoutK {
   static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
   static_assert(NW == 8 || NW == 16, "8 or 16 converter warps");
   static_assert(NE == 0 || NE == 4, "epilogue on the converters or 4 epilogue warps");
+  static_assert(BN_ == 64 || (NE == 4 && (BN_ == 8 || BN_ == 16 || BN_ == 32)),
+                "narrow N tiles need the epilogue warps");
   static constexpr int NT = NW * 32;                 // converter threads
   static constexpr int NWG = NW / 4;                 // warps per TMEM lane quadrant
   static constexpr int KPW = KB / NWG;               // k of a k-block per warp
-  static constexpr int BN = V2_BN;
+  static constexpr int BN = BN_;                     // complex output columns per tile
   static constexpr int CPW = BN / NWG;               // epilogue columns per warp
   static constexpr int NP = 2 * BN;
   static constexpr int B_BLOCK = BN * 32;
   static constexpr int B_PLANE = 3 * B_BLOCK;
   static constexpr int STAGE = 2 * B_PLANE;
   static constexpr int RAWA_SLOT = NT * KPW * 8;     // 8 KB: 128 rows x 8 complex
-  static constexpr int RAWB_SLOT = BN * KB * 8;      // 4 KB: 64 columns x 8 complex
+  static constexpr int RAWB_SLOT = BN * KB * 8;      // BN columns x 8 complex
   static constexpr int RAWA_OFF = STAGES * STAGE;
   static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
-  static constexpr int EPI_CH = NE ? 16 : CPW;       // columns per staging pass
+  static constexpr int EPI_CH = NE ? (BN < 16 ? BN : 16) : CPW;  // columns per staging pass
   static constexpr int EPI_PITCH = EPI_CH * 8 + 16;
   static constexpr int EPI_OFF = RAWB_OFF + RAW * RAWB_SLOT;
   static constexpr int BAR_OFF = EPI_OFF + (NE ? NE : NW) * 32 * EPI_PITCH;
@@ -1536,11 +1548,11 @@ struct LayoutK {
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-template <int STAGES, int RAW, int NW, int NE>
+template <int STAGES, int RAW, int NW, int NE, int BN_>
 __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk) {
-  using L = LayoutK<STAGES, RAW, NW, NE>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN_>;
   constexpr int BN = L::BN, NT = L::NT, KPW = L::KPW, CPW = L::CPW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
@@ -1661,32 +1673,34 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
       const int64_t ntile = min((int64_t)BN, g.N - (int64_t)ec.nt * BN);
       const bool fast = !use_beta && ntile == BN && ar == 1.f && ai == 0.f && g.ldc % 2 == 0 &&
                         (((uintptr_t)cw) & 15) == 0;
+      constexpr int CH = L::EPI_CH;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 16; ++ch) {
-        uint32_t vr[16], vi[16];
-        const uint32_t base = tmem + lane_base + pb * (uint32_t)L::P_COLS + (uint32_t)(ch * 16);
-        tmem_ld16(base, vr);
-        tmem_ld16(base + BN, vi);
+      for (int ch = 0; ch < BN / CH; ++ch) {
+        uint32_t vr[CH], vi[CH];
+        const uint32_t base = tmem + lane_base + pb * (uint32_t)L::P_COLS + (uint32_t)(ch * CH);
+        tmem_ld_cols<CH>(base, vr);
+        tmem_ld_cols<CH>(base + BN, vi);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (ch == BN / 16 - 1) {  // the whole tile is in registers/staging: free the buffer
+        if (ch == BN / CH - 1) {  // the whole tile is in registers/staging: free the buffer
           tc_fence_before();
           __syncwarp();
           if (lane == 0)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[pb]))
                          : "memory");
         }
-        float2 *cc0 = cw + ch * 16;
+        float2 *cc0 = cw + ch * CH;
         if (fast) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < CH / 2; ++j)
             *reinterpret_cast<float4 *>(stg + lane * L::EPI_PITCH + j * 16) =
                 make_float4(__uint_as_float(vr[2 * j]), __uint_as_float(vi[2 * j]),
                             __uint_as_float(vr[2 * j + 1]), __uint_as_float(vi[2 * j + 1]));
           __syncwarp();
-          const int rs = lane >> 3, cc = lane & 7;
+          constexpr int LPR = CH / 2, RPI = 32 / LPR;  // lanes per row, rows per store
+          const int rs = lane / LPR, cc = lane % LPR;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = 4 * i + rs;
+          for (int i = 0; i < 32 / RPI; ++i) {
+            const int r = RPI * i + rs;
             if (m0 + r < g.M)
               *reinterpret_cast<float4 *>(cc0 + r * g.ldc + 2 * cc) =
                   *reinterpret_cast<const float4 *>(stg + r * L::EPI_PITCH + cc * 16);
@@ -1694,9 +1708,9 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
           __syncwarp();
         } else if (m0 + lane < g.M) {
           float2 *crow = cc0 + (int64_t)lane * g.ldc;
-          const int64_t ncols = min((int64_t)16, ntile - ch * 16);
+          const int64_t ncols = min((int64_t)CH, ntile - ch * CH);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < CH; ++j) {
             if (j < ncols) {
               const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
               float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
@@ -1741,9 +1755,12 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
     const uint32_t rawa0 = rawa_base + (uint32_t)tid * 16;
     // ---- B fetch: NW = 8 -> 2 consecutive k of one column per thread (16 B);
     // NW = 16 -> one element per thread, k fastest
+    constexpr int BEL = BN * KB;                   // B elements per k-block
+    constexpr int BE = BEL >= NT ? BEL / NT : 1;   // per participating thread
+    const bool b_thr = tid < BEL;
     int b_n, b_k;
     uint32_t boff;
-    if constexpr (NW == 8) {
+    if constexpr (BE == 2) {
       const int b_kp = tid & 1, b_chunk = tid >> 7;
       b_n = (tid >> 1) & (BN - 1);
       b_k = b_chunk * 4 + b_kp * 2;
@@ -1753,7 +1770,6 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
       b_n = tid >> 3;
       boff = core_off(b_n, b_k >> 2) + (uint32_t)((b_k & 3) * 4);
     }
-    constexpr int BE = 512 / NT;  // B elements per thread per k-block
     const uint32_t rawb0 = smem_u32(smem + L::RAWB_OFF) + (uint32_t)tid * (8 * BE);
 
     Cur fc;
@@ -1869,7 +1885,7 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
           }
           if (fa_ok) fa += KB * a_kstride;
         }
-        if (!f_breuse) {
+        if (!f_breuse && b_thr) {
           const uint32_t db = rawb0 + slot * L::RAWB_SLOT;
           const uint32_t k0 = f_kb * KB + b_k;
           if constexpr (BE == 2) {
@@ -1979,7 +1995,7 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
         for (int p = 0; p < CPR; ++p)
           av[p] = *reinterpret_cast<const float4 *>(smem + L::RAWA_OFF + slot * L::RAWA_SLOT +
                                                      p * NT * 16 + tid * 16);
-        if (!breuse) {
+        if (!breuse && b_thr) {
           uint8_t *stage = smem + s * L::STAGE;
           uint8_t *ph = stage, *pl = stage + L::B_PLANE;
           if constexpr (BE == 2) {
@@ -2056,10 +2072,10 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
                  "r"(L::TMEM_COLS));
 }
 
-template <int STAGES, int RAW, int NW, int NE>
+template <int STAGES, int RAW, int NW, int NE, int BN = V2_BN>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutK<STAGES, RAW, NW, NE>;
-  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -2853,6 +2869,9 @@ static int launch_short_auto(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 10) return tc::launch_short<8, 4, 8, 0>(g, s);
   if (g_tc3_variant == 11) return tc::launch_short<8, 4, 16, 0>(g, s);
   if (g_tc3_variant == 12) return tc::launch_short<8, 8, 16, 4>(g, s);
+  if (g.N <= 8) return tc::launch_short<8, 8, 16, 4, 8>(g, s);
+  if (g.N <= 16) return tc::launch_short<8, 8, 16, 4, 16>(g, s);
+  if (g.N <= 32) return tc::launch_short<8, 8, 16, 4, 32>(g, s);
   if (g.K <= 8) return tc::launch_short<8, 4, 8, 0>(g, s);
   if (g.K <= 56) return tc::launch_short<8, 4, 16, 0>(g, s);
   return tc::launch_short<8, 8, 16, 4>(g, s);
@@ -2861,7 +2880,10 @@ static int launch_short_auto(const GemmArgs &g, cudaStream_t s) {
 bool tc3_eligible(const GemmArgs &g) {
   // a 128 x 64 tile reasonably full and enough tiles for the machine; short
   // K is fine (the short-K kernel streams A once and keeps B resident)
-  return g.M >= 128 && g.N >= 32 && g.K >= 1 && g.M * g.N * g.batch >= 128 * 64 * 148;
+  // narrow N (12..31) only through the short-K kernel's narrow tiles; N < 12
+  // stays on the CUDA-core row-block kernel (measured faster or equal)
+  return g.M >= 128 && g.K >= 1 && (g.N >= 32 || (g.N >= 12 && g.K <= 256)) &&
+         g.M * g.batch >= 128 * 148 && g.M * g.N * g.batch >= 128 * 64 * 148 / 8;
 }
 
 int gemm_tc3(const GemmArgs &g, cudaStream_t s) {

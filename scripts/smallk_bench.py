@@ -16,7 +16,8 @@ def timeit(fn, reps=10):
 
 for (b, M, N, K, oa, ob) in [(1024, 4096, 64, 8, 0, 0), (1024, 512, 512, 8, 1, 1), (1024, 512, 512, 8, 0, 0),
                              (1024, 4096, 64, 16, 0, 0), (1024, 4096, 32, 8, 0, 0), (1024, 4096, 64, 32, 0, 0),
-                             (1024, 32768, 8, 8, 0, 0), (1024, 4096, 8, 64, 0, 0)]:
+                             (1024, 32768, 8, 8, 0, 0), (1024, 4096, 8, 64, 0, 0), (1024, 4096, 8, 64, 1, 0),
+                             (1024, 4096, 16, 64, 0, 0), (1024, 4096, 32, 64, 0, 0), (1024, 32768, 8, 8, 1, 1)]:
     A = torch.randn(b * M * K, dtype=torch.complex64, device="cuda")
     B = torch.randn(b * K * N, dtype=torch.complex64, device="cuda")
     C = torch.empty(b * M * N, dtype=torch.complex64, device="cuda")

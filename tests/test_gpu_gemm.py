@@ -96,7 +96,10 @@ TC_SHAPES = [(1, 128, 128, 8), (1, 128, 128, 64), (2, 256, 256, 40), (1, 300, 20
 # (k-block counts 1/2/4/8, ragged K and M, several N tiles per batch, runs
 # that cross batch boundaries, runs of one tile)
 SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256, 512, 64, 64),
-                 (40, 640, 96, 8), (3, 2048, 128, 24), (7, 384, 64, 200)]
+                 (40, 640, 96, 8), (3, 2048, 128, 24), (7, 384, 64, 200),
+                 # narrow N tiles (BN = 8 / 16 / 32, ragged columns)
+                 (64, 512, 8, 64), (16, 1000, 8, 8), (8, 2048, 16, 40), (5, 700, 12, 64),
+                 (9, 300, 5, 24), (4, 640, 32, 64), (3, 512, 24, 130)]
 
 
 @pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12],
@@ -123,7 +126,7 @@ def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
 
 @pytest.mark.parametrize("shape", SHORTK_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-@pytest.mark.parametrize("variant", [10, 11, 12], ids=["8warps", "16warps", "epilogue-warps"])
+@pytest.mark.parametrize("variant", [0, 10, 11, 12], ids=["auto", "8warps", "16warps", "epilogue-warps"])
 def test_tcgen05_short_k_runs(shape, ops, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
