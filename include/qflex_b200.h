@@ -140,14 +140,19 @@ int qf_fill_zero(void *y, int64_t bytes, void *stream);
 int qf_workspace_reserve(int64_t bytes, void *stream);
 int qf_workspace_release(void);
 
-/* K2 tuning/validation knob: 0 = auto, 1 = A operand staged in shared
- * memory (tcgen05 SS form), 2 = A operand in tensor memory (TS form).
+/* K2 tuning/validation knob: 0 = auto; 1/2 = unpromoted SS/TS tiles;
+ * 3 = promoted, register prefetch; 4 = promoted, cp.async stream; 5 = reg;
+ * 6 = CTA pair (cta_group::2); 7/8 = warp-specialised with grouped handoff;
+ * 9 = warp-specialised short-K; 10/11/12 = short-K run kernel with 8
+ * converter warps / 16 converter warps / 16 converter + 4 epilogue warps.
  * Returns the previous setting. */
 int qf_tc3_set_variant(int variant);
 
 /* K3 tuning/validation knob for memory-bound small K x N shapes: 0 = auto
  * (row-block streaming for N <= 16, shared-memory staged otherwise), 1 =
- * staged kernels only, 2 = row-block kernel only.  Returns the previous one. */
+ * staged kernels only, 2 = row-block kernel only, 3 = row-stream (staged,
+ * coalesced A; complex64 N <= 16, K*N <= 512) where eligible.  Returns the
+ * previous one. */
 int qf_small_engine(int engine);
 
 /* Name of the last kernel this library launched on the calling thread

@@ -642,6 +642,242 @@ int gemm_rowblock(const GemmArgs &g, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// row-stream kernel (complex64, N <= 16, K*N <= 512): the narrow-output GEMMs
+// of the amplitude batch (e.g. 1024 x (4096 x 8 x 64), 1024 x (32768 x 8 x 8)).
+// Every warp is independent and walks a contiguous run of 32-row groups:
+//   * A arrives in k-chunks (<= 16 k) through a 3-deep cp.async ring in the
+//     warp's shared memory, fetched along the layout's contiguous direction
+//     (lanes along k for row-major / k-contiguous gathers, lane = row for
+//     column-major / row-contiguous gathers) so every global request is
+//     whole sectors; the next chunk (of this or the next row group) is in
+//     flight while the current one is multiplied;
+//   * B[b] sits in the warp's shared memory (reloaded when the batch entry
+//     changes) and is read as broadcasts;
+//   * lane = row, N accumulators in registers; the 32 x N result goes
+//     through a staging tile so the stores are whole row segments.
+
+constexpr int RS_WARPS = 4;
+constexpr int RS_NBUF = 3;
+
+__device__ __forceinline__ void rs_cp8(uint32_t dst, const void *src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+
+struct RsShape {
+  int kc;        // k per chunk
+  int nchunk;    // chunks per row group
+  int apitch;    // bytes per staged A row
+  int opitch;    // bytes per staged C row
+  int bbytes;    // B[b] bytes (padded to NN columns)
+  int warp_smem; // bytes per warp
+};
+
+template <int NN>
+__global__ void __launch_bounds__(RS_WARPS * 32)
+    cgemm_rowstream_kernel(const __grid_constant__ GemmArgs g, RsShape sh, int64_t groups_per_b,
+                           int64_t items_per_warp) {
+  extern __shared__ __align__(16) unsigned char rs_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *wsm = rs_smem + (size_t)warp * sh.warp_smem;
+  float2 *Bs = reinterpret_cast<float2 *>(wsm);
+  unsigned char *Abuf = wsm + sh.bbytes;
+  unsigned char *Ost = Abuf + RS_NBUF * 32 * sh.apitch;
+  const uint32_t abuf_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(Abuf));
+  const int K = (int)g.K, N = (int)g.N, KC = sh.kc, NCH = sh.nchunk;
+  const int64_t total = g.batch * groups_per_b;
+  const int64_t gw = (int64_t)blockIdx.x * RS_WARPS + warp;
+  const int64_t it0 = gw * items_per_warp, it1 = min(total, it0 + items_per_warp);
+  if (it0 >= it1) return;
+  const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+  const bool gat = g.a_roff != nullptr;
+  // T mode: lane = row, one k per request; N mode: lanes along k (KC lanes per
+  // row).  A gathered A takes T mode when consecutive rows are adjacent.
+  const bool rows_contig = gat && g.M > 1 && __ldg(g.a_roff + 1) - __ldg(g.a_roff) == 1;
+  const bool tmode = gat ? rows_contig : g.opA == QF_OP_T;
+  const int lpr = KC, rpi = 32 / KC;  // N mode: lanes per row, rows per request
+
+  // ---- fetch cursor over (row group, chunk)
+  int64_t f_item = it0;
+  int f_ch = 0;
+  int32_t f_roff = 0;  // gathered: roff of this lane's row (T mode) / of row `lane` (N mode)
+  struct BR {
+    int64_t first, second;  // batch entry, first row
+  };
+  auto f_rows = [&](int64_t item) {
+    const int64_t b = item / groups_per_b;
+    return BR{b, (item - b * groups_per_b) * 32};
+  };
+  auto load_roff = [&](int64_t item) {
+    if (!gat) return;
+    const int64_t r = f_rows(item).second + lane;
+    f_roff = __ldg(g.a_roff + min(r, g.M - 1));
+  };
+  auto fetch = [&](int slot) {
+    if (f_item < it1) {
+      const auto br = f_rows(f_item);
+      const float2 *A = Ab + br.first * g.sA;
+      const int64_t r0 = br.second;
+      const int k0 = f_ch * KC;
+      const uint32_t dst0 = abuf_u32 + slot * 32 * sh.apitch;
+      if (tmode) {
+        const bool rok = r0 + lane < g.M;
+        for (int k = 0; k < KC; ++k) {
+          const bool ok = rok && k0 + k < K;
+          const float2 *src = gat ? A + f_roff + (ok ? g.a_coff[k0 + k] : 0)
+                                  : A + (int64_t)(ok ? k0 + k : 0) * g.lda + r0 + (rok ? lane : 0);
+          rs_cp8(dst0 + lane * sh.apitch + k * 8, ok ? src : Ab, ok);
+        }
+      } else {
+        const int kk = lane % lpr, rr = lane / lpr;
+        const bool kok = k0 + kk < K;
+        const int32_t c = (gat && kok) ? __ldg(g.a_coff + k0 + kk) : 0;
+        for (int i = 0; i < 32 / rpi; ++i) {
+          const int row = rpi * i + rr;
+          const bool ok = kok && r0 + row < g.M;
+          const float2 *src;
+          if (gat) {
+            const int32_t ro = __shfl_sync(0xffffffffu, f_roff, row);
+            src = A + ro + c;
+          } else {
+            src = A + (r0 + (ok ? row : 0)) * g.lda + (kok ? k0 + kk : 0);
+          }
+          rs_cp8(dst0 + row * sh.apitch + kk * 8, ok ? src : Ab, ok);
+        }
+      }
+      if (++f_ch == NCH) {
+        f_ch = 0;
+        ++f_item;
+        if (f_item < it1) load_roff(f_item);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  const float ar = (float)g.ar, ai = (float)g.ai, br_ = (float)g.br, bi_ = (float)g.bi;
+  const bool use_beta = (br_ != 0.f || bi_ != 0.f);
+  load_roff(it0);
+  for (int i = 0; i < RS_NBUF - 1; ++i) fetch(i);
+  int64_t cur_b = -1;
+  int q = 0;
+  for (int64_t item = it0; item < it1; ++item) {
+    const auto brow = f_rows(item);
+    const int64_t b = brow.first, r0 = brow.second;
+    if (b != cur_b) {  // B[b] -> smem, zero-padded to NN columns
+      __syncwarp();
+      const float2 *B = reinterpret_cast<const float2 *>(g.B) + b * g.sB;
+      for (int i = lane; i < K * NN; i += 32) {
+        const int k = i / NN, n = i - k * NN;
+        float2 v = make_float2(0.f, 0.f);
+        if (n < N) v = g.opB == QF_OP_N ? __ldg(B + (int64_t)k * g.ldb + n) : __ldg(B + (int64_t)n * g.ldb + k);
+        Bs[i] = v;
+      }
+      cur_b = b;
+      __syncwarp();
+    }
+    float2 acc[NN];
+#pragma unroll
+    for (int n = 0; n < NN; ++n) acc[n] = make_float2(0.f, 0.f);
+    for (int ch = 0; ch < NCH; ++ch, ++q) {
+      fetch((q + RS_NBUF - 1) % RS_NBUF);
+      asm volatile("cp.async.wait_group %0;" ::"n"(RS_NBUF - 1) : "memory");
+      __syncwarp();
+      const unsigned char *arow = Abuf + (q % RS_NBUF) * 32 * sh.apitch + lane * sh.apitch;
+      const int kbase = ch * KC;
+      const int kn = min(KC, K - kbase);
+      for (int k = 0; k < kn; k += 2) {
+        const float4 a2 = *reinterpret_cast<const float4 *>(arow + k * 8);
+        const float2 a0 = make_float2(a2.x, a2.y), a1 = make_float2(a2.z, a2.w);
+        const float4 *b0 = reinterpret_cast<const float4 *>(Bs + (kbase + k) * NN);
+#pragma unroll
+        for (int n = 0; n < NN; n += 2) {
+          const float4 bv = b0[n / 2];
+          cfma(acc[n], a0, make_float2(bv.x, bv.y));
+          cfma(acc[n + 1], a0, make_float2(bv.z, bv.w));
+        }
+        if (k + 1 < kn) {
+          const float4 *b1 = reinterpret_cast<const float4 *>(Bs + (kbase + k + 1) * NN);
+#pragma unroll
+          for (int n = 0; n < NN; n += 2) {
+            const float4 bv = b1[n / 2];
+            cfma(acc[n], a1, make_float2(bv.x, bv.y));
+            cfma(acc[n + 1], a1, make_float2(bv.z, bv.w));
+          }
+        }
+      }
+      __syncwarp();  // the ring slot is refilled by the next fetch
+    }
+    // ---- epilogue
+    float2 *C = reinterpret_cast<float2 *>(g.C) + b * g.sC;
+    const int rows = (int)min((int64_t)32, g.M - r0);
+    if (!use_beta && N == NN && g.ldc % 2 == 0 && ((reinterpret_cast<uintptr_t>(C + r0 * g.ldc)) & 15) == 0) {
+#pragma unroll
+      for (int n = 0; n < NN; n += 2) {
+        const float2 o0 = make_float2(ar * acc[n].x - ai * acc[n].y, ar * acc[n].y + ai * acc[n].x);
+        const float2 o1 = make_float2(ar * acc[n + 1].x - ai * acc[n + 1].y,
+                                      ar * acc[n + 1].y + ai * acc[n + 1].x);
+        *reinterpret_cast<float4 *>(Ost + lane * sh.opitch + n * 8) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      }
+      __syncwarp();
+      constexpr int LPR = NN / 2, RPI = 32 / LPR;
+      const int rs = lane / LPR, cc = lane % LPR;
+#pragma unroll
+      for (int i = 0; i < 32 / RPI; ++i) {
+        const int r = RPI * i + rs;
+        if (r < rows)
+          *reinterpret_cast<float4 *>(C + (r0 + r) * g.ldc + 2 * cc) =
+              *reinterpret_cast<const float4 *>(Ost + r * sh.opitch + cc * 16);
+      }
+      __syncwarp();
+    } else if (lane < rows) {
+      float2 *crow = C + (r0 + lane) * g.ldc;
+#pragma unroll
+      for (int n = 0; n < NN; ++n) {
+        if (n < N) {
+          float2 o = make_float2(ar * acc[n].x - ai * acc[n].y, ar * acc[n].y + ai * acc[n].x);
+          if (use_beta) {
+            const float2 c = crow[n];
+            o.x += br_ * c.x - bi_ * c.y;
+            o.y += br_ * c.y + bi_ * c.x;
+          }
+          crow[n] = o;
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+bool rowstream_eligible(const GemmArgs &g) {
+  return g.N <= 16 && g.N >= 1 && g.K >= 1 && g.K * ((g.N + 7) / 8 * 8) <= 512 && g.M >= 32;
+}
+
+int gemm_rowstream(const GemmArgs &g, cudaStream_t s) {
+  const int NN = g.N <= 8 ? 8 : 16;
+  RsShape sh;
+  sh.kc = g.K <= 8 ? 8 : 16;
+  sh.nchunk = (int)((g.K + sh.kc - 1) / sh.kc);
+  sh.apitch = sh.kc * 8 + 16;
+  sh.opitch = NN * 8 + 16;
+  sh.bbytes = (int)(g.K * NN * 8);
+  sh.bbytes = (sh.bbytes + 15) & ~15;
+  sh.warp_smem = sh.bbytes + RS_NBUF * 32 * sh.apitch + 32 * sh.opitch;
+  const int64_t groups_per_b = (g.M + 31) / 32;
+  const int64_t items = g.batch * groups_per_b;
+  const size_t smem = (size_t)RS_WARPS * sh.warp_smem;
+  const int per_sm = std::max(1, std::min(8, (int)((220 * 1024) / (smem + 1024))));
+  const int64_t warps = std::min<int64_t>(items, (int64_t)sm_count() * per_sm * RS_WARPS);
+  const int64_t per_warp = (items + warps - 1) / warps;
+  const int64_t nwarps = (items + per_warp - 1) / per_warp;
+  const int64_t grid = (nwarps + RS_WARPS - 1) / RS_WARPS;
+  auto kern = NN == 8 ? cgemm_rowstream_kernel<8> : cgemm_rowstream_kernel<16>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  kern<<<(unsigned)grid, RS_WARPS * 32, smem, s>>>(g, sh, groups_per_b, per_warp);
+  return check_launch("cgemm_rowstream");
+}
+
+// ---------------------------------------------------------------------------
 // batched GEMV family: N <= 4 output columns, A in N layout (rows contiguous
 // along K).  One warp per row group: lanes stride K with coalesced loads,
 // 4 rows in flight per warp, butterfly reduction.  B[b] (K x N) is read
@@ -775,8 +1011,9 @@ int validate(const GemmArgs &g) {
   return QF_OK;
 }
 
-// 0 = auto (row-block streaming for N <= 16, smem-staged otherwise),
-// 1 = smem-staged kernels only, 2 = row-block kernel only
+// 0 = auto (row-block streaming for N <= 16, smem-staged otherwise), 1 =
+// smem-staged kernels only, 2 = row-block kernel only, 3 = row-stream where
+// eligible (experimental: coalesced staged A; not yet faster than row-block)
 static int g_small_engine = 0;
 
 bool smallkn_eligible(const GemmArgs &g) {
@@ -870,6 +1107,10 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
   if (smallkn_eligible(g)) {
     // narrow outputs stream best row by row; wide outputs keep the
     // smem-staged kernels (warp-wide conflict-free B reads)
+    if constexpr (sizeof(R) == 4) {
+      if (g_small_engine == 3 && rowstream_eligible(g))
+        return gemm_rowstream(g, s);
+    }
     const bool rowblock = g_small_engine == 0 ? g.N <= 16 : g_small_engine == 2;
     return rowblock ? gemm_rowblock<R>(g, s) : gemm_smallkn<R>(g, s);
   }

@@ -222,9 +222,10 @@ def test_gathered_a_contract_matches_permuted(mode, case):
         tc.set_gemm_mode(prev)
 
 
-@pytest.mark.parametrize("engine", [0, 1, 2], ids=["auto", "smem", "rowblock"])
+@pytest.mark.parametrize("engine", [0, 1, 2, 3], ids=["auto", "smem", "rowblock", "rowstream"])
 @pytest.mark.parametrize("shape", [(3, 4096, 8, 64), (2, 4096, 64, 8), (1, 32768, 8, 8),
-                                   (4, 512, 512, 8), (2, 100, 13, 7), (1, 77, 3, 300)])
+                                   (4, 512, 512, 8), (2, 100, 13, 7), (1, 77, 3, 300),
+                                   (5, 1000, 8, 64), (7, 333, 5, 24), (3, 64, 16, 32)])
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1)])
 def test_small_kxn_engines(engine, shape, ops):
     lib = _lib.load()
