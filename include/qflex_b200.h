@@ -144,8 +144,10 @@ int qf_workspace_release(void);
  * 3 = promoted, register prefetch; 4 = promoted, cp.async stream; 5 = reg;
  * 6 = CTA pair (cta_group::2); 7/8 = warp-specialised with grouped handoff;
  * 9 = warp-specialised short-K; 10/11/12 = short-K run kernel with 8
- * converter warps / 16 converter warps / 16 converter + 4 epilogue warps.
- * Returns the previous setting. */
+ * converter warps / 16 converter warps / 16 converter + 4 epilogue warps;
+ * 13/14 = long-K kernel with a TMEM master accumulator promoted every 4 / 8
+ * k-blocks (13 is the long-K default); 15 = long-K warp-specialised kernel
+ * promoting into converter registers.  Returns the previous setting. */
 int qf_tc3_set_variant(int variant);
 
 /* K3 tuning/validation knob for memory-bound small K x N shapes: 0 = auto

@@ -1485,6 +1485,27 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t a, uint32_t b)
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
@@ -1514,12 +1535,14 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[CPW])
 // shared memory of the short-K kernel: B' stages, raw A/B rings, a per-warp
 // epilogue staging tile (32 rows x CPW complex, rows padded by 16 B so both
 // the row-per-lane writes and the row-contiguous reads are conflict-free)
-template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN>
+template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN, int CK_ = 0>
 struct LayoutK {
   static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
   static_assert(NW == 8 || NW == 16, "8 or 16 converter warps");
-  static_assert(NE == 0 || NE == 4, "epilogue on the converters or 4 epilogue warps");
-  static_assert(BN_ == 64 || (NE == 4 && (BN_ == 8 || BN_ == 16 || BN_ == 32)),
+  static_assert((CK_ == 0 && (NE == 0 || NE == 4)) || (CK_ > 0 && NE == 4 && BN_ == 64),
+                "short K: epilogue on the converters or 4 epilogue warps; long K: 4 promotion warps");
+  static_assert((CK_ & (CK_ - 1)) == 0, "promotion chunk must be a power of two");
+  static_assert(BN_ == 64 || (NE >= 4 && (BN_ == 8 || BN_ == 16 || BN_ == 32)),
                 "narrow N tiles need the epilogue warps");
   static constexpr int NT = NW * 32;                 // converter threads
   static constexpr int NWG = NW / 4;                 // warps per TMEM lane quadrant
@@ -1539,20 +1562,28 @@ struct LayoutK {
   static constexpr int EPI_OFF = RAWB_OFF + RAW * RAWB_SLOT;
   static constexpr int BAR_OFF = EPI_OFF + (NE ? NE : NW) * 32 * EPI_PITCH;
   static constexpr int COFF_OFF = BAR_OFF + 1024;
-  static constexpr int COFF_MAX = 256;
+  static constexpr int COFF_MAX = CK_ ? 4096 : 256;  // gathered-A k offsets
   static constexpr int SMEM = COFF_OFF + 4 * COFF_MAX;
   static constexpr int P_COLS = NP;
-  static constexpr int A_COL0 = 2 * P_COLS;
+  static constexpr int MASTER_COL = 2 * P_COLS;              // long K: fp32 master accumulator
+  static constexpr int A_COL0 = (CK_ ? 3 : 2) * P_COLS;
   static constexpr int TMEM_COLS = 512;
-  static_assert(2 * P_COLS + STAGES * 32 <= 512, "TMEM budget");
+  static_assert(A_COL0 + STAGES * 32 <= 512, "TMEM budget");
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-template <int STAGES, int RAW, int NW, int NE, int BN_>
+template <int STAGES, int RAW, int NW, int NE, int BN_, int CK_>
 __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk) {
-  using L = LayoutK<STAGES, RAW, NW, NE, BN_>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN_, CK_>;
+  // CK_ > 0: long-K mode.  Every CK_ k-blocks the tensor pipe's partial sum
+  // (double-buffered in TMEM) is added by 4 promotion warps into an fp32
+  // master accumulator that also lives in TMEM (CUDA-core adds: round to
+  // nearest, flat error in K), so the converter warps never stall on
+  // promotion; tiles are strided over the grid (neighbouring CTAs share A
+  // rows / B panels in L2).
+  constexpr bool PROMO = CK_ > 0;
   constexpr int BN = L::BN, NT = L::NT, KPW = L::KPW, CPW = L::CPW;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
@@ -1588,12 +1619,14 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
   const uint32_t lane_base = (uint32_t)(lg * 32) << 16;
   constexpr uint32_t IDESC = idesc_tf32(BM, L::NP);
 
-  const uint32_t w0 = blockIdx.x * chunk, w1 = min(total, w0 + chunk);
+  const uint32_t w0 = PROMO ? blockIdx.x : blockIdx.x * chunk;
+  const uint32_t w1 = PROMO ? total : min(total, w0 + chunk);
+  const uint32_t wstep = PROMO ? gridDim.x : 1u;
   const uint32_t K = (uint32_t)g.K;
   const uint32_t nk = (K + KB - 1) / KB;
   // B of a tile sits in the stages iff the tile rd earlier in this run had
   // the same (batch, N tile) key, i.e. >= rd tiles of the key precede it here
-  const uint32_t rd = (STAGES % nk == 0) ? STAGES / nk : 0u;
+  const uint32_t rd = (!PROMO && STAGES % nk == 0) ? STAGES / nk : 0u;
 
   // tile cursors advance incrementally (M tile fastest, then N tile, batch);
   // `run` = tiles of the current (batch, N tile) key before this one here
@@ -1602,6 +1635,15 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
   };
   auto cur_init = [&](Cur &c, uint32_t w) {
     c.w = w;
+    if constexpr (PROMO) {  // strided long-K tiles: N tile fastest (as tc3w)
+      const uint32_t tiles = tiles_m * tiles_n;
+      c.bidx = w / tiles;
+      const uint32_t t = w - c.bidx * tiles;
+      c.mt = t / tiles_n;
+      c.nt = t - c.mt * tiles_n;
+      c.run = 0;
+      return;
+    }
     const uint32_t key = w / tiles_m;
     c.mt = w - key * tiles_m;
     c.bidx = key / tiles_n;
@@ -1609,6 +1651,10 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
     c.run = 0;
   };
   auto cur_next = [&](Cur &c) {
+    if constexpr (PROMO) {
+      cur_init(c, c.w + wstep);
+      return;
+    }
     ++c.w;
     ++c.run;
     if (++c.mt == tiles_m) {
@@ -1624,20 +1670,31 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
 
   if (warp == NW + NE) {
     // ===== MMA issuer (whole warp walks the sequence, one elected lane issues)
-    uint32_t q = 0, t = 0;
-    for (uint32_t w = w0; w < w1; ++w, ++t) {
+    uint32_t q = 0, t = 0, chunkc = 0;
+    for (uint32_t w = w0; w < w1; w += wstep, ++t) {
       for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
         const uint32_t s = q & (STAGES - 1);
         mbar_wait(&full[s], (q / STAGES) & 1u);
         tc_fence_after();
-        const uint32_t d = tmem + (t & 1u) * (uint32_t)L::P_COLS;
+        uint32_t pbuf = t & 1u;
+        uint32_t pos = kb;
+        if constexpr (PROMO) {
+          pos = kb & (CK_ - 1);
+          pbuf = chunkc & 1u;
+          if (pos == 0 && chunkc >= 2) {  // promotion warps drained this partial
+            mbar_wait(&accfree[pbuf], ((chunkc >> 1) + 1) & 1u);
+            tc_fence_after();
+          }
+        }
+        const uint32_t d = tmem + pbuf * (uint32_t)L::P_COLS;
         uint8_t *stage = smem + s * L::STAGE;
         const uint32_t bhi = smem_u32(stage), blo = smem_u32(stage + L::B_PLANE);
         const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
         const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
         const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * 32u;
-        const uint32_t acc0 = kb > 0 ? 1u : 0u;
-        if (NE > 0 && kb == 0 && t >= 2) {  // epilogue warps drained this buffer (tile t-2)
+        const uint32_t acc0 = pos > 0 ? 1u : 0u;
+        const bool chunk_end = PROMO ? (pos == CK_ - 1 || kb == nk - 1) : (kb == nk - 1);
+        if (!PROMO && NE > 0 && kb == 0 && t >= 2) {  // epilogue warps drained this buffer (tile t-2)
           mbar_wait(&accfree[t & 1u], ((t >> 1) + 1) & 1u);
           tc_fence_after();
         }
@@ -1649,10 +1706,98 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
           mma_ts(d, a + 16, b2l, IDESC, 1u);
           mma_ts(d, a + 24, b2h, IDESC, 1u);
           mma_commit(&bars[s]);
-          if (kb == nk - 1) mma_commit(&pbar[t & 1u]);
+          if (chunk_end) mma_commit(&pbar[pbuf]);
         }
+        if (PROMO && chunk_end) ++chunkc;
         __syncwarp();
       }
+    }
+  } else if (PROMO && warp >= NW) {
+    // ===== promotion warps (one per TMEM lane quadrant, 32 rows x 64 columns):
+    // master (+)= partial in 16-column pieces, then the tile's epilogue
+    float2 *Cb = reinterpret_cast<float2 *>(g.C);
+    const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+    const bool use_beta = (br != 0.f || bi != 0.f);
+    uint8_t *stg = smem + L::EPI_OFF + (warp - NW) * 32 * L::EPI_PITCH;
+    const uint32_t nchunks = (nk + CK_ - 1) / CK_;
+    const uint32_t mbase = tmem + lane_base + (uint32_t)L::MASTER_COL;
+    uint32_t chunkc = 0;
+    Cur ec;
+    cur_init(ec, w0);
+    for (; ec.w < w1; cur_next(ec)) {
+      for (uint32_t c = 0; c < nchunks; ++c, ++chunkc) {
+        const uint32_t pbuf = chunkc & 1u;
+        mbar_wait(&pbar[pbuf], (chunkc >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t pbase = tmem + lane_base + pbuf * (uint32_t)L::P_COLS;
+#pragma unroll 1
+        for (int piece = 0; piece < 2 * BN / 32; ++piece) {  // 32 columns per round trip
+          uint32_t pv[32], mv[32];
+          tmem_ld32(pbase + piece * 32, pv);
+          if (c > 0) tmem_ld32(mbase + piece * 32, mv);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (c > 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              pv[j] = __float_as_uint(__uint_as_float(pv[j]) + __uint_as_float(mv[j]));
+          }
+          tmem_st32(mbase + piece * 32, pv);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[pbuf]))
+                       : "memory");
+      }
+      // ---- epilogue from the master accumulator, 16 columns per pass
+      const int64_t m0 = (int64_t)ec.mt * BM + lg * 32;
+      float2 *cw = Cb + (int64_t)ec.bidx * g.sC + m0 * g.ldc + (int64_t)ec.nt * BN;
+      const int64_t ntile = min((int64_t)BN, g.N - (int64_t)ec.nt * BN);
+      const bool fast = !use_beta && ntile == BN && ar == 1.f && ai == 0.f && g.ldc % 2 == 0 &&
+                        (((uintptr_t)cw) & 15) == 0;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 16; ++ch) {
+        uint32_t vr[16], vi[16];
+        tmem_ld16(mbase + ch * 16, vr);
+        tmem_ld16(mbase + BN + ch * 16, vi);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float2 *cc0 = cw + ch * 16;
+        if (fast) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4 *>(stg + lane * L::EPI_PITCH + j * 16) =
+                make_float4(__uint_as_float(vr[2 * j]), __uint_as_float(vi[2 * j]),
+                            __uint_as_float(vr[2 * j + 1]), __uint_as_float(vi[2 * j + 1]));
+          __syncwarp();
+          const int rs = lane >> 3, cc = lane & 7;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = 4 * i + rs;
+            if (m0 + r < g.M)
+              *reinterpret_cast<float4 *>(cc0 + r * g.ldc + 2 * cc) =
+                  *reinterpret_cast<const float4 *>(stg + r * L::EPI_PITCH + cc * 16);
+          }
+          __syncwarp();
+        } else if (m0 + lane < g.M) {
+          float2 *crow = cc0 + (int64_t)lane * g.ldc;
+          const int64_t ncols = min((int64_t)16, ntile - ch * 16);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < ncols) {
+              const float x = __uint_as_float(vr[j]), y = __uint_as_float(vi[j]);
+              float2 o = make_float2(ar * x - ai * y, ar * y + ai * x);
+              if (use_beta) {
+                const float2 cv = crow[j];
+                o.x += br * cv.x - bi * cv.y;
+                o.y += br * cv.y + bi * cv.x;
+              }
+              crow[j] = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();  // master reads done before the next tile's first promotion
     }
   } else if (NE > 0 && warp >= NW) {
     // ===== epilogue warps: drain tile t's accumulators while the converters
@@ -2072,10 +2217,10 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
                  "r"(L::TMEM_COLS));
 }
 
-template <int STAGES, int RAW, int NW, int NE, int BN = V2_BN>
+template <int STAGES, int RAW, int NW, int NE, int BN = V2_BN, int CK = 0>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutK<STAGES, RAW, NW, NE, BN>;
-  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN, CK>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN, CK>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -2085,8 +2230,9 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
     }
     attr = true;
   }
-  if (g.K > L::COFF_MAX) {
-    set_error("tc3k: K = %lld exceeds the short-K limit %d", (long long)g.K, L::COFF_MAX);
+  if ((CK == 0 && g.K > 256) || (g.a_roff && g.K > L::COFF_MAX)) {
+    set_error("tc3k: K = %lld exceeds the %s limit", (long long)g.K,
+              CK == 0 ? "short-K (unpromoted) 256" : "gathered-A 4096");
     return QF_ERR_INVALID;
   }
   const int64_t tiles_n = (g.N + L::BN - 1) / L::BN, tiles_m = (g.M + BM - 1) / BM;
@@ -2097,7 +2243,7 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   }
   const int64_t grid0 = std::min<int64_t>(total, (int64_t)sm_count());
   const int64_t chunk = (total + grid0 - 1) / grid0;
-  const int64_t grid = (total + chunk - 1) / chunk;
+  const int64_t grid = CK > 0 ? grid0 : (total + chunk - 1) / chunk;  // long K: strided tiles
   kern<<<(unsigned)grid, (NW + NE) * 32 + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
                                                       (uint32_t)total, (uint32_t)chunk);
   return check_launch("cgemm_tc3k");
@@ -2872,8 +3018,11 @@ static int launch_short_auto(const GemmArgs &g, cudaStream_t s) {
   if (g.N <= 8) return tc::launch_short<8, 8, 16, 4, 8>(g, s);
   if (g.N <= 16) return tc::launch_short<8, 8, 16, 4, 16>(g, s);
   if (g.N <= 32) return tc::launch_short<8, 8, 16, 4, 32>(g, s);
+  // K in (128, 256]: the promoted long-K kernel (TMEM master, 8-k-block
+  // chunks) beats one long TMEM accumulation (scripts/c5_shapes.py)
+  if (g.K > 128) return tc::launch_short<4, 8, 8, 4, 64, 8>(g, s);
   if (g.K <= 8) return tc::launch_short<8, 4, 8, 0>(g, s);
-  if (g.K <= 56) return tc::launch_short<8, 4, 16, 0>(g, s);
+  if (g.K <= 56) return g.N > 64 ? tc::launch_short<8, 4, 8, 0>(g, s) : tc::launch_short<8, 4, 16, 0>(g, s);
   return tc::launch_short<8, 8, 16, 4>(g, s);
 }
 
@@ -2882,8 +3031,9 @@ bool tc3_eligible(const GemmArgs &g) {
   // K is fine (the short-K kernel streams A once and keeps B resident)
   // narrow N (12..31) only through the short-K kernel's narrow tiles; N < 12
   // stays on the CUDA-core row-block kernel (measured faster or equal)
-  return g.M >= 128 && g.K >= 1 && (g.N >= 32 || (g.N >= 12 && g.K <= 256)) &&
-         g.M * g.batch >= 128 * 148 && g.M * g.N * g.batch >= 128 * 64 * 148 / 8;
+  if (g.M < 128 || g.K < 1) return false;
+  if (g.N >= 32) return g.M * g.N * g.batch >= 128 * 64 * 148;
+  return g.N >= 12 && g.K <= 256 && g.M * g.batch >= 128 * 148;
 }
 
 int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
@@ -2892,12 +3042,17 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   const bool small_n = g.N <= 64;
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
+    if (g_tc3_variant == 13) return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
+    if (g_tc3_variant == 14) return tc::launch_short<4, 8, 8, 4, 64, 8>(g, s);
     if (g.K <= 256)
       return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : launch_short_auto(g, s);
-    return tc::launch_ws<8, 4, 8, false>(g, s);
+    if (g_tc3_variant == 15) return tc::launch_ws<8, 4, 8, false>(g, s);
+    return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
   }
   if (g_tc3_variant == 9)
     return g.K <= 256 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_ws<8, 4, 8, false>(g, s);
+  if (g_tc3_variant == 13) return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
+  if (g_tc3_variant == 14) return tc::launch_short<4, 8, 8, 4, 64, 8>(g, s);
   if (g_tc3_variant == 1)
     return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);
   if (g_tc3_variant == 2)
@@ -2914,7 +3069,9 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
   // double-buffered TMEM accumulators with a deferred epilogue
   if (g.K <= 256) return launch_short_auto(g, s);
-  return tc::launch_ws<8, 4, 8, false>(g, s);
+  if (g_tc3_variant == 15) return tc::launch_ws<8, 4, 8, false>(g, s);
+  // long K: 8 converter warps, 4 promotion warps with a TMEM master accumulator
+  return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
 }
 
 }  // namespace qf

@@ -13,6 +13,9 @@ from paper_1811_09599_b200 import tensor_core as tc
 from paper_1811_09599_b200.amplitude_engine import _bits_str
 
 which = sys.argv[1]
+if os.environ.get("QF_TC3_VARIANT"):  # A/B the tensor-core kernel flavours
+    from paper_1811_09599_b200 import _lib
+    _lib.load().qf_tc3_set_variant(int(os.environ["QF_TC3_VARIANT"]))
 max_paths = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 ev = lambda: torch.cuda.Event(enable_timing=True)
 
@@ -58,7 +61,7 @@ for i, p in enumerate(paths[:max_paths]):
     if i == 0:
         with tc.KernelTimer() as kt:
             ex._steps.clear(); ex._sites.clear(); ex.run(p)
-        for k, d in sorted(kt.summary().items(), key=lambda x: -x[1]["ms"]):
+        for k, d in sorted(kt.summary(detail=True).items(), key=lambda x: -x[1]["ms"])[:14]:
             print(f"   {k}: {d['ms']:.1f} ms, {d['launches']} launches, "
                   f"{d['flops'] / d['ms'] / 1e9 if d['ms'] else 0:.1f} TFLOP/s, {d['bytes'] / d['ms'] / 1e6:.0f} GB/s")
 vals = acc.cpu().numpy()

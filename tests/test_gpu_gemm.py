@@ -102,9 +102,10 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (9, 300, 5, 24), (4, 640, 32, 64), (3, 512, 24, 130)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15],
                 ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
-                     "ws-shortk", "short-8warps", "short-16warps", "short-epilogue-warps"])
+                     "ws-shortk", "short-8warps", "short-16warps", "short-epilogue-warps",
+                     "long-tmem-master-ck4", "long-tmem-master-ck8", "long-ws-registers"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -164,10 +165,17 @@ def test_gathered_short_k_many_tiles(a_labels, variant):
 
 
 @pytest.mark.parametrize("K", [1024, 4096, 32768])
-def test_tcgen05_promoted_accuracy_at_long_k(K):
+@pytest.mark.parametrize("variant", [0, 13, 14, 15],
+                         ids=["default", "tmem-master-ck4", "tmem-master-ck8", "ws-registers"])
+def test_tcgen05_promoted_accuracy_at_long_k(K, variant):
     """Promotion keeps the long-K error near the FFMA kernel's (config-4
     GEMMs have K = 2^15)."""
-    err = _gemm(1, 128, 64, K, 0, 0, np.complex64, mode=_lib.GEMM_TC3)
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(variant)
+    try:
+        err = _gemm(1, 128, 64, K, 0, 0, np.complex64, mode=_lib.GEMM_TC3)
+    finally:
+        lib.qf_tc3_set_variant(prev)
     assert err < 5e-6, err
 
 
