@@ -43,6 +43,10 @@ extern "C" {
 #define QF_GEMM_FFMA 1   /* K3: plain fp32 FFMA complex GEMM (baseline)           */
 #define QF_GEMM_TC3 2    /* K2: tcgen05 kind::tf32 3xTF32 complex GEMM (sm_100a)  */
 
+/* hint or'ed into qf_cgemm_c64_gather's mode: a_roff[r] == a_roff[0] + r
+ * (consecutive rows adjacent in memory); picks the CUDA-core fetch direction */
+#define QF_GATHER_ROWS_UNIT 0x100
+
 /* operand layouts */
 #define QF_OP_N 0        /* A stored [M][K] (lda >= K); B stored [K][N] (ldb >= N) */
 #define QF_OP_T 1        /* A stored [K][M] (lda >= M); B stored [N][K] (ldb >= K) */

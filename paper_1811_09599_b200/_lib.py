@@ -24,6 +24,7 @@ QF_ERR_MEMORY = -3
 QF_ERR_UNSUPPORTED = -4
 
 GEMM_AUTO, GEMM_FFMA, GEMM_TC3 = 0, 1, 2
+GATHER_ROWS_UNIT = 0x100  # or'ed into qf_cgemm_c64_gather's mode: roff[r] = roff[0] + r
 OP_N, OP_T = 0, 1
 
 # every exported symbol declared in include/qflex_b200.h

@@ -43,6 +43,7 @@ struct GemmArgs {
   double ar, ai, br, bi;
   const int32_t *a_roff = nullptr;
   const int32_t *a_coff = nullptr;
+  bool rows_unit = false;  // gathered A hint: a_roff[r] == a_roff[0] + r
 };
 
 __device__ __forceinline__ int64_t a_offset(const GemmArgs &g, int64_t r, int64_t k) {

@@ -3053,6 +3053,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return g.K <= 256 ? tc::launch_ws<8, 4, 8, true>(g, s) : tc::launch_ws<8, 4, 8, false>(g, s);
   if (g_tc3_variant == 13) return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
   if (g_tc3_variant == 14) return tc::launch_short<4, 8, 8, 4, 64, 8>(g, s);
+  if (g_tc3_variant == 16) return tc::launch_short<4, 8, 16, 4, 64, 4>(g, s);
   if (g_tc3_variant == 1)
     return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);
   if (g_tc3_variant == 2)

@@ -251,23 +251,29 @@ def _gather_tables(dims, labels, rows, cols, device):
         off = np.zeros(1, dtype=np.int64)
         for l in group:
             off = (off[:, None] + np.arange(dim[l], dtype=np.int64)[None, :] * stride[l]).reshape(-1)
-        return torch.from_numpy(off.astype(np.int32)).to(device)
+        return off
 
-    hit = (table(rows), table(cols))
+    r, c = table(rows), table(cols)
+    # consecutive rows adjacent in memory: the K3 engines then fetch lane = row
+    rows_unit = bool(r.size > 1 and r[1] - r[0] == 1)
+    hit = (torch.from_numpy(r.astype(np.int32)).to(device),
+           torch.from_numpy(c.astype(np.int32)).to(device), rows_unit)
     if len(_GATHER_TABLES) > 512:
         _GATHER_TABLES.clear()
     _GATHER_TABLES[key] = hit
     return hit
 
 
-def gemm_gather_buffer(batch, M, N, K, A, sA, roff, coff, B, opB, C, mode=None):
+def gemm_gather_buffer(batch, M, N, K, A, sA, roff, coff, B, opB, C, mode=None, rows_unit=False):
     """C[b] = A_gathered[b] @ op(B[b]) (complex64): the big operand is read
-    through offset tables instead of being transposed first."""
+    through offset tables instead of being transposed first.  `rows_unit`
+    (roff[r] = roff[0] + r) is a fetch-direction hint for the engines."""
     ldb = N if opB == _lib.OP_N else K
     lib = _lib.load()
+    flags = _lib.GATHER_ROWS_UNIT if rows_unit else 0
     with _timed("gemm", 8 * batch * M * N * K, 8 * batch * (M * K + K * N + M * N),
                 f"b{batch} m{M} n{N} k{K} G{'NT'[opB]}" if _timer else ""):
-        st = lib.qf_cgemm_c64_gather(_gemm_mode if mode is None else mode, batch, M, N, K,
+        st = lib.qf_cgemm_c64_gather((_gemm_mode if mode is None else mode) | flags, batch, M, N, K,
                                      ctypes.c_void_p(A.data_ptr()), sA,
                                      ctypes.c_void_p(roff.data_ptr()),
                                      ctypes.c_void_p(coff.data_ptr()),
@@ -483,8 +489,10 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
             and m <= 2 ** 22 and k <= 4096 and _gather_enabled):
         # fuse the big operand's permutation into the GEMM fetch
         nb = len(batch)
-        roff, coff = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order, a.data.device)
-        gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out)
+        roff, coff, rows_unit = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order,
+                                               a.data.device)
+        gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out,
+                           rows_unit=rows_unit)
     else:
         A, opA = operand(a, a_free, True)  # N: [batch][M][K], T: [batch][K][M]
         gemm_buffer(bt, m, n, k, A.data, opA, B.data, opB, out)

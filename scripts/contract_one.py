@@ -5,6 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1811_09599_b200 import tensor_core as tc
 al, bl, dim, reps = sys.argv[1].split(), sys.argv[2].split(), int(sys.argv[3]), int(sys.argv[4])
+if len(sys.argv) > 5:  # K3 small-engine override (0 auto, 2 row-block, 3 row-stream)
+    from paper_1811_09599_b200 import _lib
+    _lib.load().qf_small_engine(int(sys.argv[5]))
 shape = lambda ls: tuple(1024 if l == "@b" else dim for l in ls)
 a = tc.Tensor(al, torch.randn(shape(al), dtype=torch.complex64, device="cuda").reshape(-1), shape(al))
 b = tc.Tensor(bl, torch.randn(shape(bl), dtype=torch.complex64, device="cuda").reshape(-1), shape(bl))
