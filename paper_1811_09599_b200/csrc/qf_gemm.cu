@@ -533,6 +533,13 @@ __global__ void __launch_bounds__(RB_THREADS)
   extern __shared__ __align__(16) unsigned char rb_smem[];
   V *Bs = reinterpret_cast<V *>(rb_smem);
   const int K = (int)g.K, N = (int)g.N;
+  int32_t *s_coff = reinterpret_cast<int32_t *>(Bs + (size_t)K * N);  // gathered-A k offsets
+  if (g.a_roff) {
+    for (int i = threadIdx.x; i < K; i += RB_THREADS) s_coff[i] = g.a_coff[i];
+    __syncthreads();
+  }
+  // full 8-column groups of an even-N B read as 16-byte pairs
+  const bool vec_b = sizeof(V) == 8 && N % 2 == 0;
   const int groups = (N + RB_NG - 1) / RB_NG;
   const int tid = threadIdx.x;
   const R ar = (R)g.ar, ai = (R)g.ai, br = (R)g.br, bi = (R)g.bi;
@@ -590,17 +597,32 @@ __global__ void __launch_bounds__(RB_THREADS)
             const int k = k0 + j;
             a[j] = V{R(0), R(0)};
             if (k < K)
-              a[j] = g.a_roff ? __ldg(arow + g.a_coff[k])
+              a[j] = g.a_roff ? __ldg(arow + s_coff[k])
                               : (g.opA == QF_OP_N ? __ldg(arow + k) : __ldg(arow + (int64_t)k * g.lda));
           }
         }
+        if (vec_b && n0 + RB_NG <= N) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (k0 + j < K) {
-            const V *bk = Bs + (k0 + j) * N + n0;
+          for (int j = 0; j < 8; ++j) {
+            if (k0 + j < K) {
+              const float4 *bk = reinterpret_cast<const float4 *>(Bs + (k0 + j) * N + n0);
 #pragma unroll
-            for (int c = 0; c < RB_NG; ++c)
-              if (n0 + c < N) cfma(acc[c], a[j], bk[c]);
+              for (int c = 0; c < RB_NG; c += 2) {
+                const float4 bv = bk[c / 2];
+                cfma(acc[c], a[j], V{(R)bv.x, (R)bv.y});
+                cfma(acc[c + 1], a[j], V{(R)bv.z, (R)bv.w});
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (k0 + j < K) {
+              const V *bk = Bs + (k0 + j) * N + n0;
+#pragma unroll
+              for (int c = 0; c < RB_NG; ++c)
+                if (n0 + c < N) cfma(acc[c], a[j], bk[c]);
+            }
           }
         }
       }
@@ -634,9 +656,9 @@ int gemm_rowblock(const GemmArgs &g, cudaStream_t s) {
   const int64_t ctas = std::min<int64_t>(items, (int64_t)sm_count() * 8);
   const int64_t per_cta = (items + ctas - 1) / ctas;
   const int64_t grid = (items + per_cta - 1) / per_cta;
-  const size_t smem = (size_t)g.K * g.N * sizeof(V);
+  const size_t smem = (size_t)g.K * g.N * sizeof(V) + (g.a_roff ? (size_t)g.K * 4 : 0);
   auto kern = cgemm_rowblock_kernel<R>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   kern<<<(unsigned)grid, RB_THREADS, smem, s>>>(g, rows_per_item, items_per_b, per_cta);
   return check_launch("cgemm_rowblock");
 }
