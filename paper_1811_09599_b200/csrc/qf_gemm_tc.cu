@@ -1535,8 +1535,12 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[CPW])
 // shared memory of the short-K kernel: B' stages, raw A/B rings, a per-warp
 // epilogue staging tile (32 rows x CPW complex, rows padded by 16 B so both
 // the row-per-lane writes and the row-contiguous reads are conflict-free)
-template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN, int CK_ = 0>
+template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN, int CK_ = 0, int NPW_ = 0>
 struct LayoutK {
+  static_assert(NPW_ == 0 || (NPW_ == 4 && NE == 4 && BN_ == 64),
+                "producer warps: 4, with epilogue/promotion warps and 64-column tiles");
+  static constexpr int NPW = NPW_;                   // producer (fetch) warps
+  static constexpr int RPITCH = 80;                  // producer mode: raw row = 8 complex + 16 B
   static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
   static_assert(NW == 8 || NW == 16, "8 or 16 converter warps");
   static_assert((CK_ == 0 && (NE == 0 || NE == 4)) || (CK_ > 0 && NE == 4 && BN_ == 64),
@@ -1553,8 +1557,8 @@ struct LayoutK {
   static constexpr int B_BLOCK = BN * 32;
   static constexpr int B_PLANE = 3 * B_BLOCK;
   static constexpr int STAGE = 2 * B_PLANE;
-  static constexpr int RAWA_SLOT = NT * KPW * 8;     // 8 KB: 128 rows x 8 complex
-  static constexpr int RAWB_SLOT = BN * KB * 8;      // BN columns x 8 complex
+  static constexpr int RAWA_SLOT = NPW_ ? BM * RPITCH : NT * KPW * 8;  // 128 rows x 8 complex
+  static constexpr int RAWB_SLOT = NPW_ ? BN * RPITCH : BN * KB * 8;   // BN columns x 8 complex
   static constexpr int RAWA_OFF = STAGES * STAGE;
   static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
   static constexpr int EPI_CH = NE ? (BN < 16 ? BN : 16) : CPW;  // columns per staging pass
@@ -1572,11 +1576,14 @@ struct LayoutK {
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-template <int STAGES, int RAW, int NW, int NE, int BN_, int CK_>
-__global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
+template <int STAGES, int RAW, int NW, int NE, int BN_, int CK_, int NPW>
+__global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk) {
-  using L = LayoutK<STAGES, RAW, NW, NE, BN_, CK_>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN_, CK_, NPW>;
+  // NPW > 0: 4 producer warps own the global fetch (cp.async into padded raw
+  // rows, completion signalled on per-slot mbarriers); the converter warps
+  // only read, split and store into TMEM / the B' planes.
   // CK_ > 0: long-K mode.  Every CK_ k-blocks the tensor pipe's partial sum
   // (double-buffered in TMEM) is added by 4 promotion warps into an fp32
   // master accumulator that also lives in TMEM (CUDA-core adds: round to
@@ -1590,7 +1597,9 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
   uint64_t *pbar = bars + STAGES;                                    // [2] tile accumulated
   uint64_t *full = pbar + 2;                                         // [STAGES] stage converted
   uint64_t *accfree = full + STAGES;                                 // [2] accumulator drained
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accfree + 2);
+  uint64_t *rawfull = accfree + 2;                                   // [RAW] producer fill landed
+  uint64_t *rawfree = rawfull + RAW;                                 // [RAW] converters read it
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rawfree + RAW);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int lg = warp & 3, wg = warp >> 2;
@@ -1600,6 +1609,10 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
     for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
     for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], NW);
     for (int i = 0; i < 2; ++i) mbar_init(&accfree[i], NE ? NE : 1);
+    for (int i = 0; i < RAW; ++i) {
+      mbar_init(&rawfull[i], NPW ? NPW * 32 : 1);
+      mbar_init(&rawfree[i], NW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1668,7 +1681,7 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
   };
 
 
-  if (warp == NW + NE) {
+  if (warp == NW + NE + NPW) {
     // ===== MMA issuer (whole warp walks the sequence, one elected lane issues)
     uint32_t q = 0, t = 0, chunkc = 0;
     for (uint32_t w = w0; w < w1; w += wstep, ++t) {
@@ -1712,6 +1725,126 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
         __syncwarp();
       }
     }
+  } else if (NPW > 0 && warp >= NW + NE) {
+    // ===== producer warps: fetch A (and B unless it is resident) for every
+    // k-block into the raw ring, rows padded to 80 B; the layout's
+    // contiguous axis is spread across lanes so requests are whole sectors
+    const int pt = tid - (NW + NE) * 32;  // 0..127
+    const float2 *Ab = reinterpret_cast<const float2 *>(g.A);
+    const float2 *Bb = reinterpret_cast<const float2 *>(g.B);
+    const bool rows_unit = gat && g.M > 1 && __ldg(g.a_roff + 1) - __ldg(g.a_roff) == 1;
+    const bool a_vec = !gat && g.opA == QF_OP_N && g.lda % 2 == 0 && g.sA % 2 == 0;
+    const bool b_vec = g.opB == QF_OP_T && g.ldb % 2 == 0 && g.sB % 2 == 0;
+    // 0 gathered, lane = row; 1 gathered, lanes along k; 2 column-major, lane = row;
+    // 3 row-major, 16-byte k pairs; 4 row-major, lanes along k
+    const int pmode = gat ? (rows_unit ? 0 : 1) : (g.opA == QF_OP_T ? 2 : (a_vec ? 3 : 4));
+    const uint32_t rawa = smem_u32(smem + L::RAWA_OFF), rawb = smem_u32(smem + L::RAWB_OFF);
+    const bool k_tail = (K % KB) != 0;
+    Cur pc;
+    cur_init(pc, w0);
+    uint32_t f = 0;
+    for (; pc.w < w1; cur_next(pc)) {
+      const bool breuse = rd != 0u && pc.run >= rd;
+      const float2 *A = Ab + (int64_t)pc.bidx * g.sA;
+      const float2 *B = Bb + (int64_t)pc.bidx * g.sB;
+      const int64_t m0 = (int64_t)pc.mt * BM, n0 = (int64_t)pc.nt * BN;
+      // per-tile row bases
+      int32_t ro[8];
+      uint32_t rmask = 0;
+      if (pmode == 0 || pmode == 2) {
+        const int64_t r = m0 + pt;
+        rmask = r < g.M ? 1u : 0u;
+        ro[0] = pmode == 0 ? __ldg(g.a_roff + min(r, g.M - 1)) : 0;
+      } else if (pmode == 1 || pmode == 4) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t r = m0 + (pt >> 3) + 16 * i;
+          rmask |= r < g.M ? (1u << i) : 0u;
+          ro[i] = pmode == 1 ? __ldg(g.a_roff + min(r, g.M - 1)) : 0;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rmask |= (m0 + (pt >> 2) + 32 * i < g.M) ? (1u << i) : 0u;
+      }
+      for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+        const uint32_t slot = f & (RAW - 1);
+        if (f >= RAW) mbar_wait(&rawfree[slot], ((f / RAW) + 1) & 1u);
+        const uint32_t dA = rawa + slot * L::RAWA_SLOT, dB = rawb + slot * L::RAWB_SLOT;
+        const uint32_t k0 = kb * KB;
+        const bool tail = k_tail && kb == nk - 1;
+        if (pmode == 0) {
+#pragma unroll
+          for (int k = 0; k < KB; ++k) {
+            const bool ok = (rmask & 1u) && (!tail || k0 + k < K);
+            cp_async8(dA + pt * L::RPITCH + k * 8, ok ? A + ro[0] + s_coff[k0 + k] : Ab, ok);
+          }
+        } else if (pmode == 2) {
+#pragma unroll
+          for (int k = 0; k < KB; ++k) {
+            const bool ok = (rmask & 1u) && (!tail || k0 + k < K);
+            cp_async8(dA + pt * L::RPITCH + k * 8, ok ? A + (int64_t)(k0 + k) * g.lda + m0 + pt : Ab, ok);
+          }
+        } else if (pmode == 1 || pmode == 4) {
+          const int k = pt & 7;
+          const bool kok = !tail || k0 + k < K;
+          const int32_t c = pmode == 1 ? s_coff[kok ? k0 + k : 0u] : 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = (pt >> 3) + 16 * i;
+            const bool ok = kok && ((rmask >> i) & 1u);
+            const float2 *src = pmode == 1 ? A + (ro[i] + c) : A + (m0 + r) * g.lda + k0 + k;
+            cp_async8(dA + r * L::RPITCH + k * 8, ok ? src : Ab, ok);
+          }
+        } else {  // pmode 3: row-major, 16-byte k pairs
+          const int kp = pt & 3;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = (pt >> 2) + 32 * i;
+            const bool rok = (rmask >> i) & 1u;
+            const float2 *src = A + (m0 + r) * g.lda + k0 + 2 * kp;
+            if (!tail) {
+              cp_async16(dA + r * L::RPITCH + kp * 16, rok ? src : Ab, rok);
+            } else {
+              const bool ok0 = rok && k0 + 2 * kp < K, ok1 = rok && k0 + 2 * kp + 1 < K;
+              cp_async8(dA + r * L::RPITCH + kp * 16, ok0 ? src : Ab, ok0);
+              cp_async8(dA + r * L::RPITCH + kp * 16 + 8, ok1 ? src + 1 : Ab, ok1);
+            }
+          }
+        }
+        if (!breuse) {
+          if (g.opB == QF_OP_N) {  // rows of B are k: lanes along n
+            const int n = pt & 63;
+            const bool nok = n0 + n < g.N;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t k = (pt >> 6) + 2 * i;
+              const bool ok = nok && (!tail || k0 + k < K);
+              cp_async8(dB + n * L::RPITCH + k * 8, ok ? B + (int64_t)(k0 + k) * g.ldb + n0 + n : Bb, ok);
+            }
+          } else if (b_vec && !tail) {  // rows of B are n, k contiguous: 16-byte k pairs
+            const int kp = pt & 3;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int n = (pt >> 2) + 32 * i;
+              const bool ok = n0 + n < g.N;
+              cp_async16(dB + n * L::RPITCH + kp * 16, ok ? B + (n0 + n) * g.ldb + k0 + 2 * kp : Bb, ok);
+            }
+          } else {
+            const int k = pt & 7;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int n = (pt >> 3) + 16 * i;
+              const bool ok = n0 + n < g.N && (!tail || k0 + k < K);
+              cp_async8(dB + n * L::RPITCH + k * 8, ok ? B + (n0 + n) * g.ldb + k0 + k : Bb, ok);
+            }
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                         smem_u32(&rawfull[slot]))
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (PROMO && warp >= NW) {
     // ===== promotion warps (one per TMEM lane quadrant, 32 rows x 64 columns):
     // master (+)= partial in 16-column pieces, then the tile's epilogue
@@ -1868,6 +2001,107 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
             }
           }
         }
+      }
+    }
+  } else if constexpr (NPW > 0) {
+    // ===== converter warps fed by the producers: raw rows -> registers
+    // (slot released at once), split, B' planes + tcgen05.st of A
+    int b_n, b_k;
+    uint32_t boff;
+    constexpr int BE = (BN * KB) / NT;  // B elements per thread per k-block (BN = 64)
+    if constexpr (BE == 2) {
+      const int b_kp = tid & 1, b_chunk = tid >> 7;
+      b_n = (tid >> 1) & (BN - 1);
+      b_k = b_chunk * 4 + b_kp * 2;
+      boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
+    } else {
+      b_k = tid & 7;
+      b_n = tid >> 3;
+      boff = core_off(b_n, b_k >> 2) + (uint32_t)((b_k & 3) * 4);
+    }
+    const uint32_t kw0 = (uint32_t)(wg * KPW);
+    constexpr int CPR = KPW / 2;
+    Cur cc;
+    cur_init(cc, w0);
+    uint32_t q = 0;
+    for (; cc.w < w1; cur_next(cc)) {
+      const bool breuse = rd != 0u && cc.run >= rd;
+      for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+        const uint32_t slot = q & (RAW - 1), s = q & (STAGES - 1);
+        mbar_wait(&rawfull[slot], (q / RAW) & 1u);
+        const uint8_t *ra = smem + L::RAWA_OFF + slot * L::RAWA_SLOT + row_l * L::RPITCH + kw0 * 8;
+        float4 av[CPR];
+#pragma unroll
+        for (int p = 0; p < CPR; ++p) av[p] = *reinterpret_cast<const float4 *>(ra + 16 * p);
+        float4 bb4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        float2 bb2 = make_float2(0.f, 0.f);
+        if (!breuse) {
+          const uint8_t *rb = smem + L::RAWB_OFF + slot * L::RAWB_SLOT + b_n * L::RPITCH + b_k * 8;
+          if constexpr (BE == 2) bb4 = *reinterpret_cast<const float4 *>(rb);
+          else bb2 = *reinterpret_cast<const float2 *>(rb);
+        }
+        __syncwarp();
+        if (lane == 0)  // release semantics order the reads above before the refill
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rawfree[slot]))
+                       : "memory");
+        if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
+        if (!breuse) {
+          uint8_t *stage = smem + s * L::STAGE;
+          uint8_t *ph = stage, *pl = stage + L::B_PLANE;
+          if constexpr (BE == 2) {
+            uint32_t hr0, lr0, hi0, li0, hr1, lr1, hi1, li1;
+            split_fast(bb4.x, hr0, lr0);
+            split_fast(bb4.y, hi0, li0);
+            split_fast(bb4.z, hr1, lr1);
+            split_fast(bb4.w, hi1, li1);
+            *reinterpret_cast<uint2 *>(ph + 0 * L::B_BLOCK + boff) =
+                make_uint2(hi0 ^ 0x80000000u, hi1 ^ 0x80000000u);
+            *reinterpret_cast<uint2 *>(ph + 1 * L::B_BLOCK + boff) = make_uint2(hr0, hr1);
+            *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
+            *reinterpret_cast<uint2 *>(pl + 0 * L::B_BLOCK + boff) =
+                make_uint2(li0 ^ 0x80000000u, li1 ^ 0x80000000u);
+            *reinterpret_cast<uint2 *>(pl + 1 * L::B_BLOCK + boff) = make_uint2(lr0, lr1);
+            *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(li0, li1);
+          } else {
+            uint32_t hr, lr, hi, li;
+            split_fast(bb2.x, hr, lr);
+            split_fast(bb2.y, hi, li);
+            *reinterpret_cast<uint32_t *>(ph + 0 * L::B_BLOCK + boff) = hi ^ 0x80000000u;
+            *reinterpret_cast<uint32_t *>(ph + 1 * L::B_BLOCK + boff) = hr;
+            *reinterpret_cast<uint32_t *>(ph + 2 * L::B_BLOCK + boff) = hi;
+            *reinterpret_cast<uint32_t *>(pl + 0 * L::B_BLOCK + boff) = li ^ 0x80000000u;
+            *reinterpret_cast<uint32_t *>(pl + 1 * L::B_BLOCK + boff) = lr;
+            *reinterpret_cast<uint32_t *>(pl + 2 * L::B_BLOCK + boff) = li;
+          }
+          fence_async_smem();
+        }
+        {
+          uint32_t rh[KPW], rl[KPW], ih[KPW], il[KPW];
+#pragma unroll
+          for (int p = 0; p < CPR; ++p) {
+            split_fast(av[p].x, rh[2 * p], rl[2 * p]);
+            split_fast(av[p].y, ih[2 * p], il[2 * p]);
+            split_fast(av[p].z, rh[2 * p + 1], rl[2 * p + 1]);
+            split_fast(av[p].w, ih[2 * p + 1], il[2 * p + 1]);
+          }
+          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * 32) + kw0;
+          if constexpr (KPW == 4) {
+            tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+            tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+            tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+            tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+          } else {
+            tmem_st2(acol + 0, rh[0], rh[1]);
+            tmem_st2(acol + 8, rl[0], rl[1]);
+            tmem_st2(acol + 16, ih[0], ih[1]);
+            tmem_st2(acol + 24, il[0], il[1]);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
       }
     }
   } else {
@@ -2217,10 +2451,10 @@ __global__ void __launch_bounds__((NW + NE) * 32 + 32, 1)
                  "r"(L::TMEM_COLS));
 }
 
-template <int STAGES, int RAW, int NW, int NE, int BN = V2_BN, int CK = 0>
+template <int STAGES, int RAW, int NW, int NE, int BN = V2_BN, int CK = 0, int NPW = 0>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutK<STAGES, RAW, NW, NE, BN, CK>;
-  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN, CK>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN, CK, NPW>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN, CK, NPW>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -2244,7 +2478,7 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   const int64_t grid0 = std::min<int64_t>(total, (int64_t)sm_count());
   const int64_t chunk = (total + grid0 - 1) / grid0;
   const int64_t grid = CK > 0 ? grid0 : (total + chunk - 1) / chunk;  // long K: strided tiles
-  kern<<<(unsigned)grid, (NW + NE) * 32 + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
+  kern<<<(unsigned)grid, (NW + NE + NPW) * 32 + 32, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
                                                       (uint32_t)total, (uint32_t)chunk);
   return check_launch("cgemm_tc3k");
 }
@@ -3047,6 +3281,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");
     if (g_tc3_variant == 13) return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
     if (g_tc3_variant == 14) return tc::launch_short<4, 8, 8, 4, 64, 8>(g, s);
+    if (g_tc3_variant == 17 && g.K <= 256) return tc::launch_short<8, 4, 8, 4, 64, 0, 4>(g, s);
+    if (g_tc3_variant == 18) return tc::launch_short<4, 8, 8, 4, 64, 4, 4>(g, s);
     if (g.K <= 256)
       return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : launch_short_auto(g, s);
     if (g_tc3_variant == 15) return tc::launch_ws<8, 4, 8, false>(g, s);
@@ -3057,6 +3293,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 13) return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
   if (g_tc3_variant == 14) return tc::launch_short<4, 8, 8, 4, 64, 8>(g, s);
   if (g_tc3_variant == 16) return tc::launch_short<4, 8, 16, 4, 64, 4>(g, s);
+  if (g_tc3_variant == 17 && g.K <= 256) return tc::launch_short<8, 4, 8, 4, 64, 0, 4>(g, s);
+  if (g_tc3_variant == 18) return tc::launch_short<4, 8, 8, 4, 64, 4, 4>(g, s);
   if (g_tc3_variant == 1)
     return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);
   if (g_tc3_variant == 2)
