@@ -1648,12 +1648,19 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
   };
   auto cur_init = [&](Cur &c, uint32_t w) {
     c.w = w;
-    if constexpr (PROMO) {  // strided long-K tiles: N tile fastest (as tc3w)
+    if constexpr (PROMO) {
+      // strided long-K tiles in groups of GM M tiles: the ~148 tiles in
+      // flight cover a GM x (148/GM) block, so A and B panels are each
+      // reused ~GM times out of L2 instead of re-streamed from HBM
+      constexpr uint32_t GM = 16;
       const uint32_t tiles = tiles_m * tiles_n;
       c.bidx = w / tiles;
       const uint32_t t = w - c.bidx * tiles;
-      c.mt = t / tiles_n;
-      c.nt = t - c.mt * tiles_n;
+      const uint32_t group = t / (GM * tiles_n), first_m = group * GM;
+      const uint32_t gsize = min(tiles_m - first_m, GM);
+      const uint32_t r = t - group * GM * tiles_n;
+      c.mt = first_m + r % gsize;
+      c.nt = r / gsize;
       c.run = 0;
       return;
     }
