@@ -27,7 +27,7 @@ for (b, M, N, K) in [(1, 4096, 4096, 4096), (1, 8192, 8192, 8192), (1, 32768, 51
     B = torch.randn(b * K * N, dtype=torch.complex64, device="cuda")
     C = torch.empty(b * M * N, dtype=torch.complex64, device="cuda")
     row = {}
-    for name, mode, var in (("ffma", 1, 0), ("tc3_default", 2, 0), ("tc3w_regs", 2, 15), ("tmem_ck8", 2, 14), ("producer", 2, 18)):
+    for name, mode, var in (("ffma", 1, 0), ("tc3_default", 2, 0), ("tc3w_regs", 2, 15), ("tmem_ck8", 2, 14), ("tma", 2, 19)):
         lib.qf_tc3_set_variant(var)
         ms = timeit(lambda: tc.gemm_buffer(b, M, N, K, A, 0, B, 0, C, mode=mode), 5)
         row[name] = round(8 * b * M * N * K / ms / 1e9, 1)

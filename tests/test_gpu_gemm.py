@@ -102,11 +102,11 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (9, 300, 5, 24), (4, 640, 32, 64), (3, 512, 24, 130)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 17, 18],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 17, 18, 19],
                 ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
                      "ws-shortk", "short-8warps", "short-16warps", "short-epilogue-warps",
                      "long-tmem-master-ck4", "long-tmem-master-ck8", "long-ws-registers",
-                     "short-producer-warps", "long-producer-warps"])
+                     "short-producer-warps", "long-producer-warps", "long-tma"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -168,9 +168,9 @@ def test_gathered_short_k_many_tiles(a_labels, variant):
 
 
 @pytest.mark.parametrize("K", [1024, 4096, 32768])
-@pytest.mark.parametrize("variant", [0, 13, 14, 15, 18],
+@pytest.mark.parametrize("variant", [0, 13, 14, 15, 18, 19],
                          ids=["default", "tmem-master-ck4", "tmem-master-ck8", "ws-registers",
-                              "producer-warps"])
+                              "producer-warps", "tma"])
 def test_tcgen05_promoted_accuracy_at_long_k(K, variant):
     """Promotion keeps the long-K error near the FFMA kernel's (config-4
     GEMMs have K = 2^15)."""
@@ -185,6 +185,15 @@ def test_tcgen05_promoted_accuracy_at_long_k(K, variant):
 
 def test_tcgen05_alpha_beta(tc_variant):
     assert _gemm(2, 256, 128, 64, 0, 0, np.complex64, _lib.GEMM_TC3, 0.5 - 1j, 1.0 + 0.5j) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(16, 1024, 128, 512), (64, 512, 64, 64), (64, 512, 16, 64),
+                                   (3, 2048, 2048, 1024)])
+@pytest.mark.parametrize("ab", [(0.5 - 1j, 0.0), (1.0, 0.5 + 0.25j), (1.0, 0.0)])
+@pytest.mark.parametrize("ops", [(0, 0), (1, 1)])
+def test_tcgen05_alpha_beta_multi_tile_runs(shape, ab, ops):
+    """alpha/beta (per-element epilogue paths) with several tiles per CTA."""
+    assert _gemm(*shape, *ops, np.complex64, _lib.GEMM_TC3, ab[0], ab[1]) < 1e-5
 
 
 def test_tcgen05_matches_ffma_bitwise_scale():
