@@ -1613,10 +1613,7 @@ template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN, int CK_ = 0, int
 struct LayoutK {
   static_assert(NPW_ == 0 || (NPW_ == (TMA_ ? 1 : 4) && NE == 4 && BN_ == 64),
                 "producer warps (4 cp.async or 1 TMA) need epilogue/promotion warps and 64-column tiles");
-  // TMA feeds only the promoted long-K flavour: the short-K run kernel with
-  // TMA returned wrong tiles on its per-element epilogue path (second tile
-  // of a CTA run), not yet understood -- so it is not built
-  static_assert(!TMA_ || CK_ > 0, "TMA is enabled for the long-K (promoted) kernel only");
+
   static constexpr int NPW = NPW_;                   // producer (fetch) warps
   static constexpr int RPITCH = 80;                  // producer mode: raw row = 8 complex + 16 B
   static_assert((STAGES & (STAGES - 1)) == 0 && (RAW & (RAW - 1)) == 0, "rings must be powers of two");
@@ -3364,6 +3361,10 @@ static int launch_short_auto(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 10) return tc::launch_short<8, 4, 8, 0>(g, s);
   if (g_tc3_variant == 11) return tc::launch_short<8, 4, 16, 0>(g, s);
   if (g_tc3_variant == 12) return tc::launch_short<8, 8, 16, 4>(g, s);
+  // TMA-fed runs (one producer warp) when the operands are plain strided
+  // views and K >= 32 (1024 x 4096 x {16,32,64} x {32,64}: 0.57-0.68 ms vs
+  // 0.74-0.96 ms for the converter-fetch kernels, scripts/smallk_bench.py)
+  if (g.K >= 32 && g.K <= 128 && tc::tma_ok(g)) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
   if (g.N <= 8) return tc::launch_short<8, 8, 16, 4, 8>(g, s);
   if (g.N <= 16) return tc::launch_short<8, 8, 16, 4, 16>(g, s);
   if (g.N <= 32) return tc::launch_short<8, 8, 16, 4, 32>(g, s);
@@ -3401,6 +3402,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     if (g_tc3_variant == 17 && g.K <= 256) return tc::launch_short<8, 4, 8, 4, 64, 0, 4>(g, s);
     if (g_tc3_variant == 18) return tc::launch_short<4, 8, 8, 4, 64, 4, 4>(g, s);
   if (g_tc3_variant == 19 && tc::tma_ok(g)) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
+  if (g_tc3_variant == 20 && tc::tma_ok(g) && g.K <= 256)
+    return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
 
     if (g.K <= 256)
       return g_tc3_variant == 9 ? tc::launch_ws<8, 4, 8, true>(g, s) : launch_short_auto(g, s);
@@ -3415,6 +3418,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 17 && g.K <= 256) return tc::launch_short<8, 4, 8, 4, 64, 0, 4>(g, s);
   if (g_tc3_variant == 18) return tc::launch_short<4, 8, 8, 4, 64, 4, 4>(g, s);
   if (g_tc3_variant == 19 && tc::tma_ok(g)) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
+  if (g_tc3_variant == 20 && tc::tma_ok(g) && g.K <= 256)
+    return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
 
   if (g_tc3_variant == 1)
     return small_n ? tc::launch<64, 6, false>(g, s) : tc::launch<128, 4, false>(g, s);

@@ -23,7 +23,7 @@ for (b, M, N, K, oa, ob) in [(1024, 4096, 64, 8, 0, 0), (1024, 512, 512, 8, 1, 1
     C = torch.empty(b * M * N, dtype=torch.complex64, device="cuda")
     byts = 8 * b * (M * K + K * N + M * N)
     row = {}
-    for name, mode, var in (("simt", 1, 0), ("tc3", 2, 0), ("tc3_8w", 2, 10), ("tc3_16w", 2, 11), ("tc3_epi", 2, 12)):
+    for name, mode, var in (("simt", 1, 0), ("tc3", 2, 0), ("tc3_8w", 2, 10), ("tc3_16w", 2, 11), ("tc3_epi", 2, 12), ("tc3_tma", 2, 20)):
         _lib.load().qf_tc3_set_variant(var)
         try:
             ms = timeit(lambda: tc.gemm_buffer(b, M, N, K, A, oa, B, ob, C, mode=mode), 5)

@@ -102,11 +102,11 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (9, 300, 5, 24), (4, 640, 32, 64), (3, 512, 24, 130)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 17, 18, 19],
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 17, 18, 19, 20],
                 ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
                      "ws-shortk", "short-8warps", "short-16warps", "short-epilogue-warps",
                      "long-tmem-master-ck4", "long-tmem-master-ck8", "long-ws-registers",
-                     "short-producer-warps", "long-producer-warps", "long-tma"])
+                     "short-producer-warps", "long-producer-warps", "long-tma", "short-tma"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -128,8 +128,8 @@ def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
 
 @pytest.mark.parametrize("shape", SHORTK_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-@pytest.mark.parametrize("variant", [0, 10, 11, 12, 17],
-                         ids=["auto", "8warps", "16warps", "epilogue-warps", "producer-warps"])
+@pytest.mark.parametrize("variant", [0, 10, 11, 12, 17, 20],
+                         ids=["auto", "8warps", "16warps", "epilogue-warps", "producer-warps", "tma"])
 def test_tcgen05_short_k_runs(shape, ops, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
