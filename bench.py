@@ -257,21 +257,28 @@ def run_gpu(args):
     base = eng.base_net(0)
     bits_dev = bits_host.t().contiguous().to(dev)       # (sites, B): row j = bits of site j
 
-    runner = eng._graph_runner(0, N_BITSTRINGS, qf.FidelitySpec()) if args.graph else None
+    runner = (eng._graph_runner(0, N_BITSTRINGS, qf.FidelitySpec(), args.late) if args.graph
+              else None)
+    from paper_1811_09599_b200.amplitude_engine import _finisher
+
+    def batched_net():
+        if args.late:
+            return base.late_outputs(bits_dev, tuple(range(circ.n)))
+        return base.fix_outputs_batch_device(bits_dev, tuple(range(circ.n)))
 
     def step_device():
         if runner is not None:           # captured plan walk, bits already resident
             acc = runner.replay_device(bits_dev)
             qf.reduce_partials(acc, group)
             return acc
-        net = base.fix_outputs_batch_device(bits_dev, tuple(range(circ.n)))
+        net = batched_net()
         ex = eng._executor(net)
         paths = qf.FidelitySpec().paths_for(ex.cut_dims)
-        acc, _ = eng._sum_paths(ex, paths, lambda t: t.data, N_BITSTRINGS)
+        acc, _ = eng._sum_paths(ex, paths, _finisher(net), N_BITSTRINGS)
         return acc
 
     def step_e2e():
-        res, _ = eng.amplitudes(0, outs, graph=args.graph)
+        res, _ = eng.amplitudes(0, outs, graph=args.graph, late=args.late)
         return res
 
     for _ in range(args.warmup):
@@ -313,12 +320,13 @@ def run_gpu(args):
 
     # ---- per-kernel profile (one extra, separately timed, eager step) ----
     with tc.KernelTimer() as kt:
-        net = base.fix_outputs_batch_device(bits_dev, tuple(range(circ.n)))
+        net = batched_net()
         ex = eng._executor(net)
-        eng._sum_paths(ex, qf.FidelitySpec().paths_for(ex.cut_dims), lambda t: t.data,
+        eng._sum_paths(ex, qf.FidelitySpec().paths_for(ex.cut_dims), _finisher(net),
                        N_BITSTRINGS)
     kinds = kt.summary()
     kerns = kt.summary(by_kernel=True)
+    exec_flops = sum(d["flops"] for d in kinds.values())   # GEMM flops actually issued
     stats_flops = qf.estimate_cost(plan, lat, DEPTH).total_flops  # per amplitude
     pk = peaks()
     result = None
@@ -372,6 +380,10 @@ def run_gpu(args):
             "cuda_graph": bool(args.graph),
             "sustained_tflops": round(amps_per_step * stats_flops / (ms / 1e3) / 1e12, 3),
             "flops_per_amplitude": stats_flops,
+            "late_output_slicing": bool(args.late),
+            "executed_flops_per_step": int(exec_flops),
+            "executed_tflops": round(exec_flops * (amps_per_step // N_BITSTRINGS) / (ms / 1e3)
+                                     / 1e12, 3),
             "gemm_mode": qf.get_gemm_mode(),
             "e2e": {"value": round(e2e, 2), "unit": "amplitudes/s",
                     "h2d_bytes_per_step": int(bits_host.numel() * 4),
@@ -604,6 +616,8 @@ def main(argv=None):
                          "config4/config5 = full-depth bounded-path runs")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the plan walk eagerly instead of replaying a captured CUDA graph")
+    ap.add_argument("--no-late", dest="late", action="store_false",
+                    help="slice every output up front (no late output slicing)")
     ap.add_argument("--paths", type=int, default=4, help="paths timed for config4/config5")
     ap.add_argument("--perm-sizes", default="24,28,30")
     ap.add_argument("--perms", type=int, default=64)

@@ -119,6 +119,36 @@ int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K
                         float alpha_re, float alpha_im, float beta_re, float beta_im,
                         void *stream);
 
+/*
+ * Late output batching (the engine's `amplitudes` path).  Early plan steps
+ * run with the circuit's `out` indices still OPEN (every combination of the
+ * few qubits they touch); once a step's open outputs would outnumber the
+ * bit-strings, the batch is sliced out of the open tensor.  This is the
+ * reference's Tensor.fix / Net2D.fix_outputs (rq/tensor_core.py:366-372,
+ * rq/network_builder.py:134-149) applied to an intermediate instead of a
+ * site tensor, and the open-qubit idea of amplitude_batch
+ * (rq/amplitude_engine.py:128-170) applied internally.
+ *
+ * qf_bit_offsets:  off[b] = sum_j bits[rows[j]*ld + b] * strides[j]
+ *   bits: DEVICE int32 matrix (row q = bit of qubit q for every entry b);
+ *   rows/strides: HOST arrays of n <= 64 entries (element strides of the
+ *   open `out` indices); off: DEVICE int64[nb].
+ * qf_gather_rows:  dst[b][o][l] = src[off[b] + ooff[o] + l]
+ *   (ooff: DEVICE int64[n_outer], or NULL for ooff[o] = o*L).
+ * qf_cgemm_c64_gather_boff: qf_cgemm_c64_gather with the entry base
+ *   b*strideA replaced by a_boff[b] (DEVICE int64[batch]), so the slice is
+ *   fused into the GEMM's operand fetch.
+ */
+int qf_bit_offsets(const int32_t *bits, int64_t ld, int n, const int32_t *rows,
+                   const int64_t *strides, int64_t nb, int64_t *off, void *stream);
+int qf_gather_rows(const void *src, void *dst, int64_t nb, const int64_t *off, int64_t n_outer,
+                   const int64_t *ooff, int64_t L, int elem_bytes, void *stream);
+int qf_cgemm_c64_gather_boff(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
+                             const void *A, const int64_t *a_boff, const int32_t *a_roff,
+                             const int32_t *a_coff, const void *B, int64_t ldb, int64_t strideB,
+                             int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re,
+                             float alpha_im, float beta_re, float beta_im, void *stream);
+
 /* complex128 twin (FFMA/DFMA only), for dtype=complex128 engines. */
 int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
                   const void *A, int64_t lda, int64_t strideA, int opA,

@@ -104,6 +104,25 @@ def _bits_matrix(values: Sequence, n: int) -> np.ndarray:
         len(vals), n)
 
 
+LATE_MIN = 4   # late output slicing pays from a handful of bit-strings up
+
+
+def _use_late(late: Optional[bool], batch: int) -> bool:
+    return batch >= LATE_MIN if late is None else bool(late)
+
+
+def base_device(net: Net2D):
+    return next(iter(net.tensors.values())).data.device
+
+
+def _finisher(net: Net2D):
+    """Path result -> flat batch buffer (slicing any outputs still open)."""
+    late = net.late
+    if late is None:
+        return lambda t: t.data
+    return lambda t: late.batch(t).data if late.outs(t) else t.data
+
+
 def _completions(n_open: int, n_c: int, seed: int) -> np.ndarray:
     """The n_c completions of the open region (rq/amplitude_engine.py:159-164)."""
     if n_c == 2 ** n_open:
@@ -185,13 +204,20 @@ class AmplitudeEngine:
 
     def amplitudes(self, in_bits: Union[str, int], out_bits: Sequence,
                    fidelity: FidelitySpec = FidelitySpec(), *,
-                   chunk: Optional[int] = None, graph: bool = False) -> tuple:
+                   chunk: Optional[int] = None, graph: bool = False,
+                   late: Optional[bool] = None) -> tuple:
         """Many amplitudes at once; returns (ndarray, PathStats per amplitude).
 
         Bit-strings ride as the '@b' GEMM batch axis through one plan walk
         per chunk (default: all of them).  With graph=True the plan walk for
         this (input, chunk size, fidelity) is captured once as a CUDA graph
-        and replayed for every later chunk of the same size."""
+        and replayed for every later chunk of the same size.
+
+        late (default: on for chunks of >= LATE_MIN bit-strings): outputs
+        are sliced late -- steps touching q qubits run once over all 2^q
+        output combinations while 2^q <= chunk/2, then the chunk's values
+        are sliced out (network_builder.Net2D.late_outputs).  PathStats keep
+        the reference's per-amplitude flop count either way."""
         n = self.circuit.n
         bits = _bits_matrix(out_bits, n)
         outs = bits  # row count only below
@@ -202,24 +228,30 @@ class AmplitudeEngine:
             base = self.base_net(in_bits)
             for lo in range(0, len(outs), chunk):
                 part = bits[lo:lo + chunk]
+                use_late = _use_late(late, len(part))
                 if graph:
-                    runner = self._graph_runner(in_bits, len(part), fidelity)
+                    runner = self._graph_runner(in_bits, len(part), fidelity, use_late)
                     result[lo:lo + len(part)] = runner(part)
                     stats = runner.stats
                     continue
-                net = base.fix_outputs_batch(part, tuple(range(n)))
+                if use_late:
+                    bits_t = torch.from_numpy(np.ascontiguousarray(part.T)).to(base_device(base))
+                    net = base.late_outputs(bits_t, tuple(range(n)))
+                else:
+                    net = base.fix_outputs_batch(part, tuple(range(n)))
                 ex = self._executor(net)
                 paths = fidelity.paths_for(ex.cut_dims)
-                acc, flops = self._sum_paths(ex, paths, lambda t: t.data, len(part))
+                acc, flops = self._sum_paths(ex, paths, _finisher(net), len(part))
                 result[lo:lo + len(part)] = acc.cpu().numpy()
                 stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
         return result, stats
 
-    def _graph_runner(self, in_bits, batch: int, fidelity: FidelitySpec) -> "_GraphRunner":
-        key = (_bits_str(in_bits, self.circuit.n), batch, fidelity.f, fidelity.seed)
+    def _graph_runner(self, in_bits, batch: int, fidelity: FidelitySpec,
+                      late: bool = False) -> "_GraphRunner":
+        key = (_bits_str(in_bits, self.circuit.n), batch, fidelity.f, fidelity.seed, late)
         cache = self.__dict__.setdefault("_graphs", {})
         if key not in cache:
-            cache[key] = _GraphRunner(self, key[0], batch, fidelity)
+            cache[key] = _GraphRunner(self, key[0], batch, fidelity, late)
         return cache[key]
 
     def amplitude_batch(self, in_bits: Union[str, int], s_ab: Union[str, int],
@@ -289,7 +321,8 @@ class _GraphRunner:
     permutations, GEMMs, path accumulation -- replays as one CUDA graph, and
     the partial amplitudes are all-reduced across ranks outside the graph."""
 
-    def __init__(self, eng: "AmplitudeEngine", in_bits: str, batch: int, fidelity: FidelitySpec):
+    def __init__(self, eng: "AmplitudeEngine", in_bits: str, batch: int, fidelity: FidelitySpec,
+                 late: bool = False):
         self.eng, self.batch = eng, batch
         n = eng.circuit.n
         dev = eng._torch_device()
@@ -298,10 +331,13 @@ class _GraphRunner:
         base = eng.base_net(in_bits)
 
         def body():
-            net = base.fix_outputs_batch_device(self.bits_t, tuple(range(n)))
+            if late:
+                net = base.late_outputs(self.bits_t, tuple(range(n)))
+            else:
+                net = base.fix_outputs_batch_device(self.bits_t, tuple(range(n)))
             ex = eng._executor(net)
             paths = fidelity.paths_for(ex.cut_dims)
-            return eng._sum_paths_local(ex, paths, lambda t: t.data, batch), ex, paths
+            return eng._sum_paths_local(ex, paths, _finisher(net), batch), ex, paths
 
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))

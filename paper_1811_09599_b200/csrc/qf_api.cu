@@ -1,6 +1,7 @@
 // Library-wide state: last-error message, launch counter, workspace,
 // device queries, and the small elementwise kernels (K4 slicing, K5
 // accumulation).
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -94,6 +95,43 @@ __global__ void gather_axis_kernel(const E *__restrict__ src, E *__restrict__ ds
   }
 }
 
+// late output batching: per-entry base offsets from the bit matrix, and
+// the materialising slice  dst[b][o][l] = src[off[b] + ooff[o] + l]
+constexpr int BITS_MAX = 64;
+struct BitRows {
+  int32_t row[BITS_MAX];
+  int64_t stride[BITS_MAX];
+};
+
+__global__ void bit_offsets_kernel(const int32_t *__restrict__ bits, int64_t ld, int n,
+                                   const __grid_constant__ BitRows r, int64_t nb,
+                                   int64_t *__restrict__ off) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = 0;
+    for (int j = 0; j < n; ++j) o += (int64_t)__ldg(bits + r.row[j] * ld + b) * r.stride[j];
+    off[b] = o;
+  }
+}
+
+// one CTA row of the grid per batch entry (blockIdx.y strides entries);
+// 32-bit index math inside an entry when it fits
+template <typename E, typename I>
+__global__ void gather_rows_kernel(const E *__restrict__ src, E *__restrict__ dst, int64_t nb,
+                                   const int64_t *__restrict__ off, I n_outer,
+                                   const int64_t *__restrict__ ooff, I L) {
+  const I per = n_outer * L;
+  for (int64_t b = blockIdx.y; b < nb; b += gridDim.y) {
+    const E *s = src + __ldg(off + b);
+    E *d = dst + b * (int64_t)per;
+    for (I r = blockIdx.x * (I)blockDim.x + threadIdx.x; r < per; r += (I)gridDim.x * blockDim.x) {
+      const I o = L == 1 ? r : r / L;
+      const I l = r - o * L;
+      d[r] = s[(ooff ? __ldg(ooff + o) : (int64_t)o * L) + l];
+    }
+  }
+}
+
 template <typename E>
 __global__ void accumulate_kernel(const E *__restrict__ x, E *__restrict__ y, int64_t n) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
@@ -162,6 +200,57 @@ int qf_gather_axis(const void *src, void *dst, int64_t outer, int64_t dim, int64
 int qf_fix_axis(const void *src, void *dst, int64_t outer, int64_t dim, int64_t inner,
                 int64_t value, int elem_bytes, void *stream) {
   return qf::gather_impl(src, dst, outer, dim, inner, nullptr, value, 1, elem_bytes, stream);
+}
+
+int qf_bit_offsets(const int32_t *bits, int64_t ld, int n, const int32_t *rows,
+                   const int64_t *strides, int64_t nb, int64_t *off, void *stream) {
+  QF_REQUIRE(n >= 0 && n <= qf::BITS_MAX, "bit_offsets: %d rows (max %d)", n, qf::BITS_MAX);
+  QF_REQUIRE(nb >= 0 && ld >= nb, "bit_offsets: bad batch %lld / ld %lld", (long long)nb,
+             (long long)ld);
+  QF_REQUIRE(nb == 0 || (off != nullptr && (n == 0 || bits != nullptr)),
+             "bit_offsets: NULL pointer");
+  if (nb == 0) return QF_OK;
+  qf::BitRows r{};
+  for (int j = 0; j < n; ++j) {
+    QF_REQUIRE(rows[j] >= 0, "bit_offsets: negative row");
+    r.row[j] = rows[j];
+    r.stride[j] = strides[j];
+  }
+  qf::bit_offsets_kernel<<<qf::grid_for(nb, 256), 256, 0, qf::as_stream(stream)>>>(bits, ld, n, r,
+                                                                                  nb, off);
+  return qf::check_launch("bit_offsets");
+}
+
+int qf_gather_rows(const void *src, void *dst, int64_t nb, const int64_t *off, int64_t n_outer,
+                   const int64_t *ooff, int64_t L, int elem_bytes, void *stream) {
+  QF_REQUIRE(nb >= 0 && n_outer >= 0 && L >= 0, "gather_rows: negative extent");
+  QF_REQUIRE(elem_bytes == 8 || elem_bytes == 16, "gather_rows: elem_bytes must be 8 or 16");
+  const int64_t total = nb * n_outer * L;
+  if (total == 0) return QF_OK;
+  QF_REQUIRE(off != nullptr, "gather_rows: off is NULL");
+  const int64_t per = n_outer * L;
+  const int64_t want = (int64_t)qf::sm_count() * 16;   // CTAs of 256 threads
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, want));
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(nb, std::min<int64_t>(65535, want / gx)));
+  dim3 grid((unsigned)gx, (unsigned)gy);
+  cudaStream_t s = qf::as_stream(stream);
+  const bool small = per < (int64_t(1) << 31);
+  if (elem_bytes == 8) {
+    if (small)
+      qf::gather_rows_kernel<float2, int32_t><<<grid, 256, 0, s>>>(
+          (const float2 *)src, (float2 *)dst, nb, off, (int32_t)n_outer, ooff, (int32_t)L);
+    else
+      qf::gather_rows_kernel<float2, int64_t><<<grid, 256, 0, s>>>(
+          (const float2 *)src, (float2 *)dst, nb, off, n_outer, ooff, L);
+  } else {
+    if (small)
+      qf::gather_rows_kernel<double2, int32_t><<<grid, 256, 0, s>>>(
+          (const double2 *)src, (double2 *)dst, nb, off, (int32_t)n_outer, ooff, (int32_t)L);
+    else
+      qf::gather_rows_kernel<double2, int64_t><<<grid, 256, 0, s>>>(
+          (const double2 *)src, (double2 *)dst, nb, off, n_outer, ooff, L);
+  }
+  return qf::check_launch("gather_rows");
 }
 
 int qf_accumulate(const void *x, void *y, int64_t n, int elem_bytes, void *stream) {

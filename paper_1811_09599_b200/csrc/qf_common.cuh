@@ -28,6 +28,7 @@ int sm_count();
 
 // Strided-batched complex GEMM arguments (all engines).  When a_roff/a_coff
 // are set, A is GATHERED: A(b, r, k) = A + b*sA + a_roff[r] + a_coff[k]
+// (b*sA -> a_boff[b] when the batch offset table is set)
 // (element offsets; opA/lda ignored) -- the operand permutation is fused
 // into the GEMM's operand fetch instead of a separate transpose pass.
 struct GemmArgs {
@@ -44,7 +45,15 @@ struct GemmArgs {
   const int32_t *a_roff = nullptr;
   const int32_t *a_coff = nullptr;
   bool rows_unit = false;  // gathered A hint: a_roff[r] == a_roff[0] + r
+  // gathered A only: per-batch entry base offsets (elements) replacing b*sA --
+  // a batch of bit-strings sliced out of a tensor whose outputs are still
+  // open (late output batching); any alignment
+  const int64_t *a_boff = nullptr;
 };
+
+__device__ __forceinline__ int64_t a_batch_off(const GemmArgs &g, int64_t b) {
+  return g.a_boff ? __ldg(g.a_boff + b) : b * g.sA;
+}
 
 __device__ __forceinline__ int64_t a_offset(const GemmArgs &g, int64_t r, int64_t k) {
   if (g.a_roff) return (int64_t)g.a_roff[r] + g.a_coff[k];

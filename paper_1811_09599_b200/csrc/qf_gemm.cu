@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     int64_t b = work / tiles;
     int64_t tile = work - b * tiles;
     int64_t m0 = (tile / tiles_n) * TBM, n0 = (tile % tiles_n) * TBN;
-    const V *A = Ab + b * g.sA;
+    const V *A = Ab + a_batch_off(g, b);
     const V *B = Bb + b * g.sB;
     V *C = Cb + b * g.sC;
 
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(STHREADS)
   const int p = tid % Ppad, kl = tid / Ppad;
   const int64_t split = blockIdx.x;
   const int64_t b = blockIdx.y;
-  const V *A = (const V *)g.A + b * g.sA;
+  const V *A = (const V *)g.A + a_batch_off(g, b);
   const V *B = (const V *)g.B + b * g.sB;
   V acc = {R(0), R(0)};
   if (p < P) {
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(SKN_THREADS)
     const int64_t b = item / blocks_m;
     const int64_t m0 = (item - b * blocks_m) * rm;
     const int rows = (int)min((int64_t)rm, g.M - m0);
-    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    const V *A = reinterpret_cast<const V *>(g.A) + a_batch_off(g, b);
     V *As = Asb[buf];
     if (g.a_roff) {
       // walk the index group that holds A's stride-1 label fastest (coalesced)
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(SKN_THREADS)
       }
       cur_b = b;
     }
-    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    const V *A = reinterpret_cast<const V *>(g.A) + a_batch_off(g, b);
     for (int i = tid; i < rows * K; i += SKN_THREADS) {
       int m, k;
       if (g.a_roff) {
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(RB_THREADS)
       cur_b = b;
       __syncthreads();
     }
-    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    const V *A = reinterpret_cast<const V *>(g.A) + a_batch_off(g, b);
     V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
     for (int task = tid; task < rows * groups; task += RB_THREADS) {
       const int r = task / groups, cg = task - r * groups;
@@ -645,12 +645,20 @@ __global__ void __launch_bounds__(RB_THREADS)
   }
 }
 
+// Rows per work item so that a small batch (the open-output steps run
+// single GEMMs) still spreads over >= 2 items per SM; never below `floor`.
+static int64_t rows_for_parallelism(const GemmArgs &g, int64_t floor) {
+  const int64_t per_b = std::max<int64_t>(1, (2 * (int64_t)sm_count() + g.batch - 1) / g.batch);
+  return std::max<int64_t>(floor, (g.M + per_b - 1) / per_b);
+}
+
 template <typename R>
 int gemm_rowblock(const GemmArgs &g, cudaStream_t s) {
   using V = typename C2<R>::T;
   const int groups = (int)((g.N + RB_NG - 1) / RB_NG);
   // ~8 row-groups of work per thread per item; items fill the machine
   int rows_per_item = (int)std::max<int64_t>(1, std::min<int64_t>(g.M, 8 * RB_THREADS / groups));
+  rows_per_item = (int)std::min<int64_t>(rows_per_item, rows_for_parallelism(g, 32));
   const int64_t items_per_b = (g.M + rows_per_item - 1) / rows_per_item;
   const int64_t items = g.batch * items_per_b;
   const int64_t ctas = std::min<int64_t>(items, (int64_t)sm_count() * 8);
@@ -743,7 +751,7 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     if (f_st < st1) {
       int64_t b, r0;
       f_base(f_st, b, r0);
-      const float2 *A = Ab + b * g.sA;
+      const float2 *A = Ab + a_batch_off(g, b);
       const int k0 = f_ch * KC;
       const uint32_t dst0 = abuf_u32 + slot * L::ABUF;
       if (mode == 0) {
@@ -946,7 +954,7 @@ __global__ void __launch_bounds__(GV_THREADS)
     const int64_t b = item / items_per_b;
     const int64_t r0 = (item - b * items_per_b) * rows_per_item;
     const int64_t r1 = min(g.M, r0 + rows_per_item);
-    const V *A = reinterpret_cast<const V *>(g.A) + b * g.sA;
+    const V *A = reinterpret_cast<const V *>(g.A) + a_batch_off(g, b);
     const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
     V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
     for (int64_t m = r0 + warp * 4; m < r1; m += (GV_THREADS / 32) * 4) {
@@ -1080,6 +1088,7 @@ int gemm_smallkn_simple(const GemmArgs &g, cudaStream_t s) {
   const int64_t a_budget = std::max<int64_t>(
       apitch, (int64_t)(160 * 1024) / (int64_t)sizeof(V) - (int64_t)K * bpitch);
   int rm = (int)std::min<int64_t>(g.M, std::max<int64_t>(1, std::min<int64_t>(SKN_A_MAX, a_budget) / apitch));
+  rm = (int)std::min<int64_t>(rm, rows_for_parallelism(g, 16));
   int64_t blocks_m = (g.M + rm - 1) / rm;
   size_t smem = ((size_t)K * bpitch + (size_t)rm * apitch) * sizeof(V);
   auto kern = cgemm_smallkn_simple_kernel<R>;
@@ -1100,6 +1109,7 @@ int gemm_smallkn(const GemmArgs &g, cudaStream_t s) {
   const int64_t a_budget = std::max<int64_t>(
       apitch, ((int64_t)(160 * 1024) / (int64_t)sizeof(V) - (int64_t)K * bpitch) / 2);
   int rm = (int)std::min<int64_t>(g.M, std::max<int64_t>(1, std::min<int64_t>(SKN_A_MAX, a_budget) / apitch));
+  rm = (int)std::min<int64_t>(rm, rows_for_parallelism(g, 16));
   const int64_t blocks_m = (g.M + rm - 1) / rm;
   const size_t smem = ((((size_t)K * bpitch + 1) & ~(size_t)1) + 2 * (size_t)rm * apitch) * sizeof(V);
   // short K: one output per thread (warp spans a row: A broadcast, B
@@ -1211,6 +1221,28 @@ int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K
   qf::GemmArgs g{batch, M, N, K, A, std::max<int64_t>(K, 1), strideA, QF_OP_N, B, ldb, strideB,
                  opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
                  rows_unit};
+  int st = qf::validate(g);
+  if (st != QF_OK) return st;
+  cudaStream_t s = qf::as_stream(stream);
+  if ((mode == QF_GEMM_AUTO && qf::tc3_eligible(g)) || mode == QF_GEMM_TC3) {
+    if (qf::tc3_gather_ok(g)) return qf::gemm_tc3(g, s);
+  }
+  return qf::gemm_simt<float>(g, s);
+}
+
+int qf_cgemm_c64_gather_boff(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
+                             const void *A, const int64_t *a_boff, const int32_t *a_roff,
+                             const int32_t *a_coff, const void *B, int64_t ldb, int64_t strideB,
+                             int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re,
+                             float alpha_im, float beta_re, float beta_im, void *stream) {
+  QF_REQUIRE(a_roff != nullptr && a_coff != nullptr && (a_boff != nullptr || batch == 0),
+             "gather gemm: offset tables are NULL");
+  const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
+  mode &= ~QF_GATHER_ROWS_UNIT;
+  // sA = 1: entry bases may be odd (the 16-byte A paths key on even sA)
+  qf::GemmArgs g{batch, M, N, K, A, std::max<int64_t>(K, 1), 1, QF_OP_N, B, ldb, strideB,
+                 opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
+                 rows_unit, a_boff};
   int st = qf::validate(g);
   if (st != QF_OK) return st;
   cudaStream_t s = qf::as_stream(stream);

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int64_t bidx = work / tiles;
     const int64_t tile = work - bidx * tiles;
     const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
-    const float2 *A = Ab + bidx * g.sA;
+    const float2 *A = Ab + a_batch_off(g, bidx);
     const float2 *B = Bb + bidx * g.sB;
     float2 *C = Cb + bidx * g.sC;
 
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
     const int64_t bidx = work / tiles;
     const int64_t tile = work - bidx * tiles;
     const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
-    const float2 *A = Ab + bidx * g.sA;
+    const float2 *A = Ab + a_batch_off(g, bidx);
     const float2 *B = Bb + bidx * g.sB;
     float2 *C = Cb + bidx * g.sC;
     const int64_t am = m0 + row_l;           // A row (this thread: k in [4*half, 4*half+4))
@@ -818,7 +818,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
     const int64_t bn = (tile % tiles_n) * BN + b_n;
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
-    const float2 *A = Ab + bidx * g.sA;
+    const float2 *A = Ab + a_batch_off(g, bidx);
     const float2 *B = Bb + bidx * g.sB;
     fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
     fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
@@ -1114,7 +1114,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     const int64_t bn = (tile % tiles_n) * BN + b_n;
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
-    const float2 *A = Ab + bidx * g.sA;
+    const float2 *A = Ab + a_batch_off(g, bidx);
     const float2 *B = Bb + bidx * g.sB;
     if (a_mode == 1) {
       fa = A;
@@ -1872,7 +1872,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     uint32_t f = 0;
     for (; pc.w < w1; cur_next(pc)) {
       const bool breuse = rd != 0u && pc.run >= rd;
-      const float2 *A = Ab + (int64_t)pc.bidx * g.sA;
+      const float2 *A = Ab + a_batch_off(g, pc.bidx);
       const float2 *B = Bb + (int64_t)pc.bidx * g.sB;
       const int64_t m0 = (int64_t)pc.mt * BM, n0 = (int64_t)pc.nt * BN;
       // per-tile row bases
@@ -2277,7 +2277,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     };
     auto fetch_setup = [&]() {
       if (fc.w >= w1) return;
-      const float2 *A = Ab + (int64_t)fc.bidx * g.sA;
+      const float2 *A = Ab + a_batch_off(g, fc.bidx);
       const float2 *B = Bb + (int64_t)fc.bidx * g.sB;
       const int64_t m0 = (int64_t)fc.mt * BM;
       if (a_mode == 1 || a_mode == 3) {
@@ -2702,7 +2702,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
     const int64_t bn = (tile % tiles_n) * BN + b_n;
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
-    const float2 *A = Ab + bidx * g.sA;
+    const float2 *A = Ab + a_batch_off(g, bidx);
     const float2 *B = Bb + bidx * g.sB;
     fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
     fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
@@ -3139,7 +3139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS + 32, 1)
       const int64_t bn = (tile % tiles_n) * BN + b_n;
       fa_ok = am < g.M;
       fb_ok = bn < g.N;
-      const float2 *A = Ab + bidx * g.sA;
+      const float2 *A = Ab + a_batch_off(g, bidx);
       const float2 *B = Bb + bidx * g.sB;
       fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
       fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;

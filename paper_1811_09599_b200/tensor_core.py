@@ -425,27 +425,40 @@ class ContractShape:
         return 8 * self.m * self.k * self.n
 
 
-def contract_shape(a: Tensor, b: Tensor) -> ContractShape:
+def contract_shape(a: Tensor, b: Tensor, skip=()) -> ContractShape:
+    """Per-entry GEMM view.  Labels in `skip` (open outputs whose slicing is
+    deferred, see LateBits) count like batch labels: not part of m or n."""
     bset, aset = set(b.labels), set(a.labels)
     bt = m = k = 1
     for l, d in zip(a.labels, a.dims):
-        if l in bset:
-            if _is_batch(l):
-                bt *= d
-            else:
-                k *= d
+        if _is_batch(l) or l in skip:   # batch axes count per entry, shared or not
+            bt *= d
+        elif l in bset:
+            k *= d
         else:
             m *= d
-    n = math.prod(d for l, d in zip(b.labels, b.dims) if l not in aset)
+    n = 1
+    for l, d in zip(b.labels, b.dims):
+        if l in aset:
+            continue
+        if _is_batch(l) or l in skip:
+            bt *= d
+        else:
+            n *= d
     return ContractShape(bt, m, k, n)
 
 
-def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int = 10) -> Tensor:
+def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int = 10,
+             front=()) -> Tensor:
     """Contract over all shared labels (batch '@' labels are kept).
 
     Output labels: batch labels (a's order), then a's free labels, then
     b's free labels -- the reference's a_free + b_free order
-    (rq/tensor_core.py:396-419) with the batch axis in front."""
+    (rq/tensor_core.py:396-419) with the batch axis in front.  Labels in
+    `front` (open outputs awaiting a late slice) are moved to the front of
+    their operand's free group when that costs no extra pass (gathered big
+    operand; memoised small-operand layout), so a later per-bit-string slice
+    reads long contiguous runs."""
     if a.data.dtype != b.data.dtype:
         raise ValueError(f"dtype mismatch: {a.dtype} vs {b.dtype}")
     if b.size > a.size:
@@ -460,6 +473,8 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
             raise ValueError(f"dimension mismatch on {l!r}: {a.dim_of(l)} vs {b.dim_of(l)}")
     a_free = [l for l in a.labels if l not in bset]
     b_free = [l for l in b.labels if l not in aset]
+    if front:
+        b_free = [l for l in b_free if l in front] + [l for l in b_free if l not in front]
     # summed-index order follows the bigger operand so it is not permuted
     if a.size >= b.size:
         k_order = shared_a
@@ -489,16 +504,210 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
             and m <= 2 ** 22 and k <= 4096 and _gather_enabled):
         # fuse the big operand's permutation into the GEMM fetch
         nb = len(batch)
+        if front:
+            a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
         roff, coff, rows_unit = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order,
                                                a.data.device)
         gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out,
                            rows_unit=rows_unit)
     else:
+        if front and list(a.labels) not in (a_n, a_t):   # permuted anyway
+            a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
         A, opA = operand(a, a_free, True)  # N: [batch][M][K], T: [batch][K][M]
         gemm_buffer(bt, m, n, k, A.data, opA, B.data, opB, out)
     labels = tuple(batch + a_free + b_free)
     dims = tuple(a.dim_of(l) for l in batch + a_free) + tuple(b.dim_of(l) for l in b_free)
     return Tensor(labels, out, dims)
+
+
+# ---------------------------------------------------------------------------
+# late output batching
+
+
+def _strides(t: Tensor) -> dict:
+    out, acc = {}, 1
+    for l, d in zip(reversed(t.labels), reversed(t.dims)):
+        out[l] = acc
+        acc *= d
+    return out
+
+
+_ROW_TABLES: dict = {}
+
+
+def _outer_table(dims, labels, outer, device):
+    """int64 offsets of the `outer` label group (row-major over `outer`)."""
+    key = (tuple(dims), tuple(labels), tuple(outer), str(device))
+    hit = _ROW_TABLES.get(key)
+    if hit is None:
+        stride = {}
+        acc = 1
+        for l, d in zip(reversed(labels), reversed(dims)):
+            stride[l] = acc
+            acc *= d
+        dim = dict(zip(labels, dims))
+        off = np.zeros(1, dtype=np.int64)
+        for l in outer:
+            off = (off[:, None] + np.arange(dim[l], dtype=np.int64)[None, :] * stride[l]).reshape(-1)
+        hit = torch.from_numpy(off).to(device)
+        if len(_ROW_TABLES) > 256:
+            _ROW_TABLES.clear()
+        _ROW_TABLES[key] = hit
+    return hit
+
+
+class LateBits:
+    """Bit-strings whose output slicing is deferred ("late output batching").
+
+    The reference fixes every output index before contracting
+    (Net2D.fix_outputs, rq/network_builder.py:134-149).  For a batch of B
+    bit-strings the early plan steps touch only a few qubits, so this keeps
+    those `out` indices OPEN -- computing all 2^q combinations once instead
+    of B copies -- and slices the batch out (Tensor.fix per bit-string,
+    rq/tensor_core.py:366-372) only when 2^q would exceed `limit` (default
+    B/2).  Same products and sums per amplitude, in a different grouping.
+
+    bits_t: DEVICE int32 (rows, B) matrix; `rows` maps an out label to its
+    row.  The slice is either fused into the next GEMM's operand fetch
+    (qf_cgemm_c64_gather_boff) or materialised (qf_gather_rows)."""
+
+    def __init__(self, bits_t, rows: dict, limit: Optional[int] = None, label: str = "@b"):
+        if bits_t.dtype != torch.int32 or bits_t.dim() != 2 or not bits_t.is_contiguous():
+            raise ValueError("bits must be a contiguous 2-D int32 device tensor")
+        self.bits_t = bits_t
+        self.rows = dict(rows)
+        self.nb = int(bits_t.shape[1])
+        self.limit = max(1, self.nb // 2) if limit is None else int(limit)
+        self.label = label
+
+    def outs(self, t: Tensor) -> list:
+        return [l for l in t.labels if l in self.rows]
+
+    def offsets(self, t: Tensor, outs) -> "torch.Tensor":
+        """Per-entry element offsets of the bit-strings' slice of `t`."""
+        st = _strides(t)
+        off = torch.empty(max(self.nb, 1), dtype=torch.int64, device=t.data.device)
+        rows = (_i32 * max(1, len(outs)))(*[self.rows[l] for l in outs])
+        strides = (ctypes.c_int64 * max(1, len(outs)))(*[st[l] for l in outs])
+        with _timed("gather", 0, 4 * self.nb * (len(outs) + 2), "bit_offsets" if _timer else ""):
+            rc = _lib.load().qf_bit_offsets(ctypes.c_void_p(self.bits_t.data_ptr()), self.nb,
+                                            len(outs), rows, strides, self.nb,
+                                            ctypes.c_void_p(off.data_ptr()), stream_handle())
+        _lib.check(rc, "bit_offsets")
+        return off
+
+    def batch(self, t: Tensor) -> Tensor:
+        """Slice the batch out of `t`'s open outputs: new leading batch axis."""
+        outs = self.outs(t)
+        if not outs:
+            return t
+        if self.label in t.labels:
+            raise ValueError(f"tensor already has batch label {self.label!r}")
+        oset = set(outs)
+        rest = [(l, d) for l, d in zip(t.labels, t.dims) if l not in oset]
+        inner = 0
+        while inner < len(t.labels) and t.labels[len(t.labels) - 1 - inner] not in oset:
+            inner += 1
+        L = math.prod(t.dims[len(t.dims) - inner:]) if inner else 1
+        outer = [l for l in t.labels[:len(t.labels) - inner] if l not in oset]
+        per = math.prod(d for _, d in rest)
+        off = self.offsets(t, outs)
+        n_outer = per // L
+        ooff = (_outer_table(t.dims, t.labels, outer, t.data.device) if outer else None)
+        out = device_buffer(self.nb * per, t.data.dtype, t.data.device)
+        eb = _elem_bytes(t.data)
+        with _timed("gather", 0, 2 * eb * self.nb * per,
+                    f"late rows b{self.nb} x{n_outer} L{L}" if _timer else ""):
+            rc = _lib.load().qf_gather_rows(ctypes.c_void_p(t.data.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), self.nb,
+                                            ctypes.c_void_p(off.data_ptr()), n_outer,
+                                            ctypes.c_void_p(ooff.data_ptr() if ooff is not None
+                                                            else 0), L, eb, stream_handle())
+        _lib.check(rc, "gather_rows")
+        return Tensor((self.label,) + tuple(l for l, _ in rest), out,
+                      (self.nb,) + tuple(d for _, d in rest))
+
+    def _batched_size(self, t: Tensor) -> int:
+        outs = self.outs(t)
+        return t.size // (1 << len(outs)) * self.nb if outs else t.size
+
+
+_i32 = ctypes.c_int32
+
+
+def contract_late(a: Tensor, b: Tensor, late: LateBits) -> Tensor:
+    """`contract` for networks whose outputs are sliced late (LateBits).
+
+    Both operands without a batch axis and few open outputs between them:
+    an ordinary contraction (the outputs are free indices).  Otherwise the
+    open outputs are sliced to the batch first -- for the bigger operand
+    fused into the GEMM's gathered operand fetch when it can be."""
+    oa, ob = late.outs(a), late.outs(b)
+    if not oa and not ob:
+        return contract(a, b)
+    lb = late.label
+    if lb not in a.labels and lb not in b.labels and 2 ** (len(oa) + len(ob)) <= late.limit:
+        return contract(a, b, front=late.rows)
+    big, small = (a, b) if late._batched_size(a) >= late._batched_size(b) else (b, a)
+    if late.outs(small):
+        small = late.batch(small)
+    if late.outs(big):
+        fused = _contract_sliced(big, small, late)
+        if fused is not None:
+            return fused
+        big = late.batch(big)
+    return contract(big, small)
+
+
+def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
+    """a (open outputs, no batch axis) x b (batched): slice a's outputs per
+    entry inside the GEMM's operand fetch.  None if not eligible."""
+    lb = late.label
+    if (lb not in b.labels or a.data.dtype != torch.complex64 or not _gather_enabled
+            or a.size >= 2 ** 31):
+        return None
+    outs = set(late.outs(a))
+    labels = [l for l in a.labels if l not in outs]
+    bset = set(b.labels)
+    k_order = [l for l in labels if l in bset]
+    a_free = [l for l in labels if l not in bset]
+    for l in k_order:
+        if a.dim_of(l) != b.dim_of(l):
+            raise ValueError(f"dimension mismatch on {l!r}: {a.dim_of(l)} vs {b.dim_of(l)}")
+    aset = set(labels)
+    b_free = [l for l in b.labels if l not in aset and l != lb]
+    m = math.prod(a.dim_of(l) for l in a_free)
+    k = math.prod(a.dim_of(l) for l in k_order)
+    n = math.prod(b.dim_of(l) for l in b_free)
+    if m > 2 ** 22 or k > 4096 or k == 0:
+        return None
+    nb = late.nb
+    # small operand: [batch][K][N] (N) or [batch][N][K] (T)
+    n_layout = [lb] + k_order + b_free
+    t_layout = [lb] + b_free + k_order
+    if list(b.labels) == n_layout:
+        B, opB = b, _lib.OP_N
+    elif list(b.labels) == t_layout:
+        B, opB = b, _lib.OP_T
+    else:
+        B, opB = b.transpose_to(n_layout), _lib.OP_N
+    roff, coff, rows_unit = _gather_tables(a.dims, a.labels, a_free, k_order, a.data.device)
+    boff = late.offsets(a, late.outs(a))
+    out = device_buffer(nb * m * n, a.data.dtype, a.data.device)
+    ldb = n if opB == _lib.OP_N else k
+    flags = _lib.GATHER_ROWS_UNIT if rows_unit else 0
+    with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
+                f"b{nb} m{m} n{n} k{k} S{'NT'[opB]}" if _timer else ""):
+        st = _lib.load().qf_cgemm_c64_gather_boff(
+            _gemm_mode | flags, nb, m, n, k, ctypes.c_void_p(a.data.data_ptr()),
+            ctypes.c_void_p(boff.data_ptr()), ctypes.c_void_p(roff.data_ptr()),
+            ctypes.c_void_p(coff.data_ptr()), ctypes.c_void_p(B.data.data_ptr()), max(ldb, 1),
+            k * n, opB, ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
+            stream_handle())
+    _lib.check(st, "gemm_gather_boff")
+    labels_out = (lb,) + tuple(a_free) + tuple(b_free)
+    dims = (nb,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
+    return Tensor(labels_out, out, dims)
 
 
 # ---------------------------------------------------------------------------

@@ -14,9 +14,10 @@ lat = qf.Lattice.named("grid:5x5"); circ = qf.generate_rqc(lat, "1+24+1", 0)
 eng = qf.AmplitudeEngine(circ, qf.grid_plan(lat, n_cuts=1))
 rng = np.random.Generator(np.random.PCG64(0))
 outs = [format(int(v), "025b") for v in rng.integers(0, 2 ** 25, size=nb)]
-for _ in range(2): eng.amplitudes(0, outs)
+late = os.environ.get("QF_LATE", "1") != "0"
+for _ in range(2): eng.amplitudes(0, outs, late=late)
 with tc.KernelTimer() as kt:
-    eng.amplitudes(0, outs)
+    eng.amplitudes(0, outs, late=late)
 s = kt.summary(detail=True)
 tot = sum(d["ms"] for d in s.values())
 print(f"mode={mode} batch={nb} total kernel ms {tot:.2f}")

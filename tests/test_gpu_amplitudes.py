@@ -39,14 +39,15 @@ def gemm_mode(request):
     qf.set_gemm_mode(prev)
 
 
+@pytest.mark.parametrize("late", [False, True])
 @pytest.mark.parametrize("idx", range(19))
-def test_amplitude_cases_batched(golden, idx, gemm_mode):
+def test_amplitude_cases_batched(golden, idx, gemm_mode, late):
     if idx >= len(golden["amplitudes"]):
         pytest.skip("no such case")
     case = golden["amplitudes"][idx]
     eng = _engine(golden, case)
     fid = qf.FidelitySpec(case["f"], case["fseed"])
-    got, stats = eng.amplitudes(case["in_bits"], case["out_bits"], fid)
+    got, stats = eng.amplitudes(case["in_bits"], case["out_bits"], fid, late=late)
     assert rel_l2(got, golden_amps(case)) < _tol(case["dtype"]), case["name"]
     assert (stats.paths_total, stats.paths_used, stats.flops) == \
         (case["paths_total"], case["paths_used"], case["flops"])
@@ -198,18 +199,58 @@ def test_slice_late_is_transparent(golden):
     assert rel_l2(res[True][0], golden_amps(case)[:16]) < 1e-4
 
 
+@pytest.mark.parametrize("late", [False, True])
 @pytest.mark.parametrize("name", ["config1_c64", "config2_c64", "g4x4s3_cuts2_f025_c64"])
-def test_cuda_graph_replay_matches_eager(golden, name):
+def test_cuda_graph_replay_matches_eager(golden, name, late):
     case = next(c for c in golden["amplitudes"] if c["name"] == name)
     eng = _engine(golden, case)
     fid = qf.FidelitySpec(case["f"], case["fseed"])
     outs = case["out_bits"]
-    eager, st_e = eng.amplitudes(case["in_bits"], outs, fid)
+    eager, st_e = eng.amplitudes(case["in_bits"], outs, fid, late=not late)
     for _ in range(2):  # capture once, then replay with new bits each call
-        g1, st_g = eng.amplitudes(case["in_bits"], outs, fid, graph=True)
+        g1, st_g = eng.amplitudes(case["in_bits"], outs, fid, graph=True, late=late)
         assert rel_l2(g1, eager) < 1e-6
         assert (st_g.flops, st_g.paths_used) == (st_e.flops, st_e.paths_used)
     rev = list(reversed(outs))
-    g2, _ = eng.amplitudes(case["in_bits"], rev, fid, graph=True)
+    g2, _ = eng.amplitudes(case["in_bits"], rev, fid, graph=True, late=late)
     assert rel_l2(g2, eager[::-1]) < 1e-6
     assert rel_l2(g1, golden_amps(case)) < 1e-4
+
+
+@pytest.mark.parametrize("limit", [1, 2, 16, 2 ** 16])
+@pytest.mark.parametrize("name", ["config1_c64", "g4x4s3_cuts2_f025_c64", "config1_c128"])
+def test_late_output_slicing_limits(golden, name, limit):
+    """Late output slicing at every threshold: limit 1 slices at the first
+    contraction, 2^16 keeps a 4x4 network fully open (the whole output state
+    is contracted, then the bit-strings are sliced from it)."""
+    case = next((c for c in golden["amplitudes"] if c["name"] == name), None)
+    if case is None:
+        pytest.skip("no such case")
+    eng = _engine(golden, case)
+    fid = qf.FidelitySpec(case["f"], case["fseed"])
+    n = eng.circuit.n
+    bits = np.array([[int(ch) for ch in o] for o in case["out_bits"]], dtype=np.int32)
+    base = eng.base_net(case["in_bits"])
+    bits_t = torch.from_numpy(np.ascontiguousarray(bits.T)).cuda()
+    net = base.late_outputs(bits_t, tuple(range(n)), limit=limit)
+    ex = eng._executor(net)
+    from paper_1811_09599_b200.amplitude_engine import _finisher
+    fin = _finisher(net)
+    tot = None
+    for p in fid.paths_for(ex.cut_dims):
+        r = fin(ex.run(p))
+        tot = r.clone() if tot is None else tot + r
+    assert rel_l2(tot.cpu().numpy()[: len(bits)], golden_amps(case)) < _tol(case["dtype"])
+    assert ex.flops == case["flops"]
+
+
+def test_late_config2_1024_matches_early(golden):
+    case = next(c for c in golden["amplitudes"] if c["name"] == "config2_c64")
+    eng = _engine(golden, case)
+    rng = np.random.Generator(np.random.PCG64(0))
+    outs = [format(int(v), "025b") for v in rng.integers(0, 2 ** 25, size=1024)]
+    early, st0 = eng.amplitudes(0, outs, late=False)
+    late, st1 = eng.amplitudes(0, outs, late=True)
+    assert rel_l2(late, early) < 1e-5
+    assert (st0.flops, st0.paths_used) == (st1.flops, st1.paths_used)
+    assert rel_l2(late[:48], golden_amps(case)) < 1e-4

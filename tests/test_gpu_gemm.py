@@ -256,3 +256,51 @@ def test_small_kxn_engines(engine, shape, ops):
         assert _gemm(*shape[:3], shape[3], *ops, np.complex128) < 1e-12
     finally:
         lib.qf_small_engine(prev)
+
+
+@pytest.mark.parametrize("mode", ["auto", "ffma", "tc3"])
+@pytest.mark.parametrize("case", range(6))
+def test_late_sliced_contract_matches_numpy(mode, case):
+    """Late output slicing: a tensor with open `out` indices (anywhere in its
+    layout, innermost included) contracted with a batched tensor -- the
+    per-bit-string slice fused into the gathered GEMM fetch
+    (qf_cgemm_c64_gather_boff) or materialised (qf_gather_rows) -- equals
+    slicing first and contracting per bit-string."""
+    rng = np.random.default_rng(300 + case)
+    nb = [16, 64, 5, 33, 128, 8][case]
+    dims = {"p": 8, "q": 8, "r": 4, "s": 8, "t": 8, "v": 16, "out0": 2, "out1": 2, "out2": 2}
+    a_labels = [["p", "out0", "s", "q", "t", "out1"], ["out1", "s", "p", "t", "q", "r"],
+                ["p", "s", "out0", "out2", "q", "t"], ["s", "p", "out0", "t", "out1", "q"],
+                ["p", "q", "s", "t", "out2"], ["out0", "out1", "out2", "s", "t", "p"]][case]
+    b_labels = ["@b", "t", "v", "s"]
+    outs = [l for l in a_labels if l.startswith("out")]
+    A = _rand(rng, [dims[l] for l in a_labels], np.complex64)
+    B = _rand(rng, [nb] + [dims[l] for l in b_labels[1:]], np.complex64)
+    bits = rng.integers(0, 2, size=(3, nb)).astype(np.int32)
+    rows = {"out0": 0, "out1": 1, "out2": 2}
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {l: rows[l] for l in outs})
+    prev = tc.set_gemm_mode(mode)
+    try:
+        ta, tb = tc.Tensor(a_labels, A), tc.Tensor(b_labels, B)
+        got = tc.contract_late(ta, tb, late)
+        sliced = late.batch(ta)
+        assert sliced.labels[0] == "@b" and not late.outs(sliced)
+    finally:
+        tc.set_gemm_mode(prev)
+    rest = [l for l in a_labels if l not in outs]
+    idx = tuple(bits[rows[l]] if l in outs else slice(None) for l in a_labels)
+    # numpy advanced indexing: the batch axis lands first when the indexed
+    # axes are not adjacent, else in place of the first one -- move it first
+    As = A[idx]
+    first = min(a_labels.index(l) for l in outs)
+    adjacent = all(a_labels.index(o) - first == i for i, o in enumerate(outs))
+    if adjacent and first > 0:
+        As = np.moveaxis(As, first, 0)
+    np.testing.assert_array_equal(sliced.array, As)
+    keep = ["@b"] + [l for l in rest if l not in b_labels] + [l for l in b_labels[1:] if l not in rest]
+    sub = {l: chr(ord("a") + i) for i, l in enumerate(["@b"] + list(dims))}
+    spec = "".join(sub[l] for l in ["@b"] + rest) + "," + "".join(sub[l] for l in b_labels) + \
+        "->" + "".join(sub[l] for l in keep)
+    ref = np.einsum(spec, As.astype(np.complex128), B.astype(np.complex128))
+    out = got.transpose_to(keep).array
+    assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-5
