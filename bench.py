@@ -255,7 +255,10 @@ def run_gpu(args):
     bits_host = torch.tensor([[int(c) for c in o] for o in outs], dtype=torch.int32).pin_memory()
     # ---- device-resident step (value) ----
     base = eng.base_net(0)
-    bits_dev = bits_host.t().contiguous().to(dev)       # (sites, B): row j = bits of site j
+    dev_bits = bits_host
+    if args.late:   # the order amplitudes() walks a late-sliced batch in (host sort)
+        dev_bits = bits_host[torch.from_numpy(eng.batch_order(bits_host.numpy()))]
+    bits_dev = dev_bits.t().contiguous().to(dev)        # (sites, B): row j = bits of site j
 
     runner = (eng._graph_runner(0, N_BITSTRINGS, qf.FidelitySpec(), args.late) if args.graph
               else None)

@@ -47,6 +47,10 @@ extern "C" {
  * (consecutive rows adjacent in memory); picks the CUDA-core fetch direction */
 #define QF_GATHER_ROWS_UNIT 0x100
 
+/* hint or'ed into qf_cgemm_c64_gather_boff's mode: every a_boff[b] is even
+ * (entry bases 16-byte aligned; enables the paired A loads) */
+#define QF_BOFF_EVEN 0x200
+
 /* operand layouts */
 #define QF_OP_N 0        /* A stored [M][K] (lda >= K); B stored [K][N] (ldb >= N) */
 #define QF_OP_T 1        /* A stored [K][M] (lda >= M); B stored [N][K] (ldb >= K) */
@@ -137,7 +141,8 @@ int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K
  *   (ooff: DEVICE int64[n_outer], or NULL for ooff[o] = o*L).
  * qf_cgemm_c64_gather_boff: qf_cgemm_c64_gather with the entry base
  *   b*strideA replaced by a_boff[b] (DEVICE int64[batch]), so the slice is
- *   fused into the GEMM's operand fetch.
+ *   fused into the GEMM's operand fetch.  a_roff = a_coff = NULL: each slice
+ *   is a plain row-major [M][K] block (lda = K) at its entry base.
  */
 int qf_bit_offsets(const int32_t *bits, int64_t ld, int n, const int32_t *rows,
                    const int64_t *strides, int64_t nb, int64_t *off, void *stream);

@@ -229,9 +229,17 @@ class AmplitudeEngine:
             for lo in range(0, len(outs), chunk):
                 part = bits[lo:lo + chunk]
                 use_late = _use_late(late, len(part))
+                order = None
+                if use_late:   # walk the batch in plan order: shared prefixes adjacent
+                    order = self.batch_order(part)
+                    part = part[order]
                 if graph:
                     runner = self._graph_runner(in_bits, len(part), fidelity, use_late)
-                    result[lo:lo + len(part)] = runner(part)
+                    vals = runner(part)
+                    if order is not None:
+                        result[lo + order] = vals
+                    else:
+                        result[lo:lo + len(part)] = vals
                     stats = runner.stats
                     continue
                 if use_late:
@@ -242,9 +250,25 @@ class AmplitudeEngine:
                 ex = self._executor(net)
                 paths = fidelity.paths_for(ex.cut_dims)
                 acc, flops = self._sum_paths(ex, paths, _finisher(net), len(part))
-                result[lo:lo + len(part)] = acc.cpu().numpy()
+                if order is not None:
+                    result[lo + order] = acc.cpu().numpy()
+                else:
+                    result[lo:lo + len(part)] = acc.cpu().numpy()
                 stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
         return result, stats
+
+    def batch_order(self, bits: np.ndarray) -> np.ndarray:
+        """Order in which a late-sliced batch is walked: bit-strings sorted by
+        their qubits in the order the plan first consumes them, so entries
+        that share an open prefix are adjacent and re-read it from L2."""
+        seq = []
+        for step in self.plan.steps():
+            for x in step.inputs:
+                if x[:1] == "t" and x[1:].isdigit() and int(x[1:]) not in seq:
+                    seq.append(int(x[1:]))
+        seq += [q for q in range(self.circuit.n) if q not in seq]
+        bits = np.asarray(bits)
+        return np.lexsort([bits[:, q] for q in reversed(seq)])
 
     def _graph_runner(self, in_bits, batch: int, fidelity: FidelitySpec,
                       late: bool = False) -> "_GraphRunner":

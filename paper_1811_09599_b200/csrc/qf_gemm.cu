@@ -1235,14 +1235,22 @@ int qf_cgemm_c64_gather_boff(int mode, int64_t batch, int64_t M, int64_t N, int6
                              const int32_t *a_coff, const void *B, int64_t ldb, int64_t strideB,
                              int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re,
                              float alpha_im, float beta_re, float beta_im, void *stream) {
-  QF_REQUIRE(a_roff != nullptr && a_coff != nullptr && (a_boff != nullptr || batch == 0),
+  QF_REQUIRE((a_roff != nullptr) == (a_coff != nullptr) && (a_boff != nullptr || batch == 0),
              "gather gemm: offset tables are NULL");
   const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
-  mode &= ~QF_GATHER_ROWS_UNIT;
-  // sA = 1: entry bases may be odd (the 16-byte A paths key on even sA)
-  qf::GemmArgs g{batch, M, N, K, A, std::max<int64_t>(K, 1), 1, QF_OP_N, B, ldb, strideB,
-                 opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
-                 rows_unit, a_boff};
+  const bool even = (mode & QF_BOFF_EVEN) != 0;
+  mode &= ~(QF_GATHER_ROWS_UNIT | QF_BOFF_EVEN);
+  // sA only keys the 16-byte A paths here: 2 = every entry base is even
+  qf::GemmArgs g{batch, M, N, K, A, std::max<int64_t>(K, 1), even ? 2 : 1, QF_OP_N, B, ldb,
+                 strideB, opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im, a_roff,
+                 a_coff, rows_unit && a_roff != nullptr, a_boff};
+  if (!a_roff) {  // plain row-major [M][K] slices at the entry bases
+    int st = qf::validate(g);
+    if (st != QF_OK) return st;
+    cudaStream_t s = qf::as_stream(stream);
+    if (mode == QF_GEMM_TC3 || (mode == QF_GEMM_AUTO && qf::tc3_eligible(g))) return qf::gemm_tc3(g, s);
+    return qf::gemm_simt<float>(g, s);
+  }
   int st = qf::validate(g);
   if (st != QF_OK) return st;
   cudaStream_t s = qf::as_stream(stream);

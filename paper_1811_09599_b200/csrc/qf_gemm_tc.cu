@@ -2543,7 +2543,8 @@ static bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1,
 
 // TMA needs 16-byte global strides and a non-gathered A
 bool tma_ok(const GemmArgs &g) {
-  return !g.a_roff && g.lda % 2 == 0 && g.sA % 2 == 0 && g.ldb % 2 == 0 && g.sB % 2 == 0 &&
+  return !g.a_roff && !g.a_boff && g.lda % 2 == 0 && g.sA % 2 == 0 && g.ldb % 2 == 0 &&
+         g.sB % 2 == 0 &&
          (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 &&
          g.batch < ((int64_t)1 << 31);
 }

@@ -647,7 +647,8 @@ def contract_late(a: Tensor, b: Tensor, late: LateBits) -> Tensor:
         return contract(a, b)
     lb = late.label
     if lb not in a.labels and lb not in b.labels and 2 ** (len(oa) + len(ob)) <= late.limit:
-        return contract(a, b, front=late.rows)
+        r = _contract_open(a, b, late)
+        return r if r is not None else contract(a, b, front=late.rows)
     big, small = (a, b) if late._batched_size(a) >= late._batched_size(b) else (b, a)
     if late.outs(small):
         small = late.batch(small)
@@ -657,6 +658,78 @@ def contract_late(a: Tensor, b: Tensor, late: LateBits) -> Tensor:
             return fused
         big = late.batch(big)
     return contract(big, small)
+
+
+_ZEROS: dict = {}
+
+
+def _zero_offsets(n: int, device):
+    key = (n, str(device))
+    z = _ZEROS.get(key)
+    if z is None:
+        z = _ZEROS[key] = torch.zeros(n, dtype=torch.int64, device=device)
+    return z
+
+
+def _contract_open(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
+    """Both operands with open outputs, no batch axis yet: the smaller
+    operand's open outputs become the GEMM batch (its slices side by side,
+    the big operand broadcast through all-zero entry offsets and read
+    through gathered tables), so the result keeps EVERY open output in
+    front: [small's outs, big's outs, rows, cols].  A later per-bit-string
+    slice is then one contiguous block per entry.  None if not eligible."""
+    big, small = (a, b) if a.size >= b.size else (b, a)
+    so = late.outs(small)
+    if (not so or big.data.dtype != torch.complex64 or not _gather_enabled
+            or big.size >= 2 ** 31):
+        return None
+    sset, bset = set(small.labels), set(big.labels)
+    if any(_is_batch(l) for l in sset | bset):
+        return None
+    k_order = [l for l in big.labels if l in sset]
+    front = set(late.rows)
+    a_free = [l for l in big.labels if l not in sset]
+    a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
+    s_free = [l for l in small.labels if l not in bset and l not in so]
+    for l in k_order:
+        if big.dim_of(l) != small.dim_of(l):
+            raise ValueError(f"dimension mismatch on {l!r}: {big.dim_of(l)} vs {small.dim_of(l)}")
+    m = math.prod(big.dim_of(l) for l in a_free)
+    k = math.prod(big.dim_of(l) for l in k_order)
+    n = math.prod(small.dim_of(l) for l in s_free)
+    if k > 4096 or k == 0:
+        return None
+    nbat = 1 << len(so)
+    B = small.transpose_to(tuple(so + k_order + s_free))    # [outs][K][N]
+    out = device_buffer(nbat * m * n, big.data.dtype, big.data.device)
+    lib = _lib.load()
+    detail = f"b{nbat} m{m} n{n} k{k} O" if _timer else ""
+    if m <= 2 ** 22 and list(big.labels) != a_free + k_order:
+        # big operand read in place through offset tables, broadcast over the batch
+        roff, coff, rows_unit = _gather_tables(big.dims, big.labels, a_free, k_order,
+                                               big.data.device)
+        zeros = _zero_offsets(nbat, big.data.device)
+        flags = _lib.GATHER_ROWS_UNIT if rows_unit else 0
+        with _timed("gemm", 8 * nbat * m * n * k, 8 * (m * k + nbat * (k * n + m * n)), detail):
+            st = lib.qf_cgemm_c64_gather_boff(
+                _gemm_mode | flags, nbat, m, n, k, ctypes.c_void_p(big.data.data_ptr()),
+                ctypes.c_void_p(zeros.data_ptr()), ctypes.c_void_p(roff.data_ptr()),
+                ctypes.c_void_p(coff.data_ptr()), ctypes.c_void_p(B.data.data_ptr()), max(n, 1),
+                k * n, _lib.OP_N, ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n,
+                1.0, 0.0, 0.0, 0.0, stream_handle())
+    else:
+        # (too many rows for offset tables) one permute, then batch stride 0
+        A = big.transpose_to(tuple(a_free + k_order))
+        with _timed("gemm", 8 * nbat * m * n * k, 8 * (m * k + nbat * (k * n + m * n)), detail):
+            st = lib.qf_cgemm_c64(_gemm_mode, nbat, m, n, k, ctypes.c_void_p(A.data.data_ptr()),
+                                  max(k, 1), 0, _lib.OP_N, ctypes.c_void_p(B.data.data_ptr()),
+                                  max(n, 1), k * n, _lib.OP_N, ctypes.c_void_p(out.data_ptr()),
+                                  max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+    _lib.check(st, "gemm_open")
+    labels = tuple(so + a_free + s_free)
+    dims = tuple(small.dim_of(l) for l in so) + tuple(big.dim_of(l) for l in a_free) + \
+        tuple(small.dim_of(l) for l in s_free)
+    return Tensor(labels, out, dims)
 
 
 def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
@@ -691,18 +764,25 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
         B, opB = b, _lib.OP_T
     else:
         B, opB = b.transpose_to(n_layout), _lib.OP_N
-    roff, coff, rows_unit = _gather_tables(a.dims, a.labels, a_free, k_order, a.data.device)
-    boff = late.offsets(a, late.outs(a))
+    a_outs = late.outs(a)
+    st_a = _strides(a)
+    flags = _lib.BOFF_EVEN if all(st_a[l] % 2 == 0 for l in a_outs) else 0
+    if list(a.labels) == a_outs + a_free + k_order:
+        roff = coff = None        # every slice is a plain row-major [M][K] block
+    else:
+        roff, coff, rows_unit = _gather_tables(a.dims, a.labels, a_free, k_order, a.data.device)
+        flags |= _lib.GATHER_ROWS_UNIT if rows_unit else 0
+    boff = late.offsets(a, a_outs)
     out = device_buffer(nb * m * n, a.data.dtype, a.data.device)
     ldb = n if opB == _lib.OP_N else k
-    flags = _lib.GATHER_ROWS_UNIT if rows_unit else 0
     with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
-                f"b{nb} m{m} n{n} k{k} S{'NT'[opB]}" if _timer else ""):
+                f"b{nb} m{m} n{n} k{k} {'P' if roff is None else 'S'}{'NT'[opB]}" if _timer else ""):
         st = _lib.load().qf_cgemm_c64_gather_boff(
             _gemm_mode | flags, nb, m, n, k, ctypes.c_void_p(a.data.data_ptr()),
-            ctypes.c_void_p(boff.data_ptr()), ctypes.c_void_p(roff.data_ptr()),
-            ctypes.c_void_p(coff.data_ptr()), ctypes.c_void_p(B.data.data_ptr()), max(ldb, 1),
-            k * n, opB, ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
+            ctypes.c_void_p(boff.data_ptr()),
+            ctypes.c_void_p(roff.data_ptr() if roff is not None else 0),
+            ctypes.c_void_p(coff.data_ptr() if coff is not None else 0),
+            ctypes.c_void_p(B.data.data_ptr()), max(ldb, 1), k * n, opB, ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
             stream_handle())
     _lib.check(st, "gemm_gather_boff")
     labels_out = (lb,) + tuple(a_free) + tuple(b_free)

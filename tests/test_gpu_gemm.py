@@ -304,3 +304,32 @@ def test_late_sliced_contract_matches_numpy(mode, case):
     ref = np.einsum(spec, As.astype(np.complex128), B.astype(np.complex128))
     out = got.transpose_to(keep).array
     assert np.linalg.norm(out - ref) / np.linalg.norm(ref) < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["auto", "ffma", "tc3"])
+@pytest.mark.parametrize("case", range(4))
+def test_late_open_contract_equals_plain(mode, case):
+    """Two operands with open outputs and no batch axis: the smaller one's
+    outputs become the GEMM batch (big operand broadcast) -- same tensor as
+    the plain contraction, outputs moved to the front."""
+    rng = np.random.default_rng(400 + case)
+    dims = {"p": 8, "q": 8, "s": 8, "t": 8, "v": 8, "out0": 2, "out1": 2, "out2": 2}
+    a_labels = [["p", "out0", "s", "q", "t"], ["out1", "s", "p", "t", "q", "out0"],
+                ["s", "p", "t", "q"], ["p", "q", "out0", "s", "t"]][case]
+    b_labels = [["t", "v", "s", "out2"], ["out2", "t", "v", "s"], ["t", "s", "out2", "v"],
+                ["s", "out1", "out2", "t"]][case]
+    A = _rand(rng, [dims[l] for l in a_labels], np.complex64)
+    B = _rand(rng, [dims[l] for l in b_labels], np.complex64)
+    late = tc.LateBits(torch.zeros((3, 64), dtype=torch.int32, device="cuda"),
+                       {"out0": 0, "out1": 1, "out2": 2})
+    prev = tc.set_gemm_mode(mode)
+    try:
+        got = tc.contract_late(tc.Tensor(a_labels, A), tc.Tensor(b_labels, B), late)
+        want = tc.contract(tc.Tensor(a_labels, A), tc.Tensor(b_labels, B))
+    finally:
+        tc.set_gemm_mode(prev)
+    assert sorted(got.labels) == sorted(want.labels)
+    w = want.transpose_to(got.labels).array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+    outs = [l for l in got.labels if l.startswith("out")]
+    assert list(got.labels[:len(outs)]) == outs   # open outputs lead
