@@ -50,6 +50,8 @@ extern "C" {
 /* hint or'ed into qf_cgemm_c64_gather_boff's mode: every a_boff[b] is even
  * (entry bases 16-byte aligned; enables the paired A loads) */
 #define QF_BOFF_EVEN 0x200
+/* same for b_boff in qf_cgemm_c64_ex */
+#define QF_BBOFF_EVEN 0x400
 
 /* operand layouts */
 #define QF_OP_N 0        /* A stored [M][K] (lda >= K); B stored [K][N] (ldb >= N) */
@@ -153,6 +155,23 @@ int qf_cgemm_c64_gather_boff(int mode, int64_t batch, int64_t M, int64_t N, int6
                              const int32_t *a_coff, const void *B, int64_t ldb, int64_t strideB,
                              int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re,
                              float alpha_im, float beta_re, float beta_im, void *stream);
+
+/*
+ * General form of the complex64 GEMM: every operand option at once.
+ *   A(b, r, k) = A + baseA(b) + (a_roff ? a_roff[r] + a_coff[k] : opA/lda offset)
+ *   B(b)       = B + baseB(b) (opB/ldb layout)
+ *   baseA(b) = a_boff ? a_boff[b] : b*strideA;  baseB(b) = b_boff ? b_boff[b] : b*strideB
+ * Used by the late output slicing path to contract a batched intermediate
+ * with a site tensor whose output is still open: B(b) is the site's slice
+ * for bit-string b, read in place (no batched copy of the site tensor).
+ * mode may carry QF_GATHER_ROWS_UNIT, QF_BOFF_EVEN, QF_BBOFF_EVEN.
+ */
+int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                    int64_t lda, int64_t strideA, int opA, const int64_t *a_boff,
+                    const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
+                    int64_t strideB, int opB, const int64_t *b_boff, void *C, int64_t ldc,
+                    int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                    float beta_im, void *stream);
 
 /* complex128 twin (FFMA/DFMA only), for dtype=complex128 engines. */
 int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,

@@ -26,13 +26,14 @@ QF_ERR_UNSUPPORTED = -4
 GEMM_AUTO, GEMM_FFMA, GEMM_TC3 = 0, 1, 2
 GATHER_ROWS_UNIT = 0x100  # or'ed into qf_cgemm_c64_gather's mode: roff[r] = roff[0] + r
 BOFF_EVEN = 0x200         # or'ed into qf_cgemm_c64_gather_boff's mode: entry bases even
+BBOFF_EVEN = 0x400        # or'ed into qf_cgemm_c64_ex's mode: B entry bases even
 OP_N, OP_T = 0, 1
 
 # every exported symbol declared in include/qflex_b200.h
 EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_info", "qf_permute", "qf_permute_c64",
     "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_cgemm_c64_gather", "qf_zgemm_c128",
-    "qf_bit_offsets", "qf_gather_rows", "qf_cgemm_c64_gather_boff",
+    "qf_bit_offsets", "qf_gather_rows", "qf_cgemm_c64_gather_boff", "qf_cgemm_c64_ex",
     "qf_accumulate",
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
     "qf_small_engine",
@@ -89,6 +90,12 @@ def _declare(lib):
                                              _c_void_p, _i64, _i64,
                                              ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                              ctypes.c_float, _c_void_p]
+    lib.qf_cgemm_c64_ex.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64,
+                                    _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p, _c_void_p,
+                                    _c_void_p, _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p,
+                                    _c_void_p, _i64, _i64,
+                                    ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                    ctypes.c_float, _c_void_p]
     lib.qf_bit_offsets.argtypes = [_c_void_p, _i64, ctypes.c_int, ctypes.POINTER(_i32),
                                    ctypes.POINTER(_i64), _i64, _c_void_p, _c_void_p]
     lib.qf_gather_rows.argtypes = [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64,

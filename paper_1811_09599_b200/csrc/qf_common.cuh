@@ -49,7 +49,14 @@ struct GemmArgs {
   // a batch of bit-strings sliced out of a tensor whose outputs are still
   // open (late output batching); any alignment
   const int64_t *a_boff = nullptr;
+  // per-batch entry base offsets of B replacing b*sB (a site tensor whose
+  // output is sliced per bit-string: B(b) = B + b_boff[b]); any alignment
+  const int64_t *b_boff = nullptr;
 };
+
+__device__ __forceinline__ int64_t b_batch_off(const GemmArgs &g, int64_t b) {
+  return g.b_boff ? __ldg(g.b_boff + b) : b * g.sB;
+}
 
 __device__ __forceinline__ int64_t a_batch_off(const GemmArgs &g, int64_t b) {
   return g.a_boff ? __ldg(g.a_boff + b) : b * g.sA;

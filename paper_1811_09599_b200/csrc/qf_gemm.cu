@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(TTHREADS, 2)
     int64_t tile = work - b * tiles;
     int64_t m0 = (tile / tiles_n) * TBM, n0 = (tile % tiles_n) * TBN;
     const V *A = Ab + a_batch_off(g, b);
-    const V *B = Bb + b * g.sB;
+    const V *B = Bb + b_batch_off(g, b);
     V *C = Cb + b * g.sC;
 
     V acc[4][4];
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(STHREADS)
   const int64_t split = blockIdx.x;
   const int64_t b = blockIdx.y;
   const V *A = (const V *)g.A + a_batch_off(g, b);
-  const V *B = (const V *)g.B + b * g.sB;
+  const V *B = (const V *)g.B + b_batch_off(g, b);
   V acc = {R(0), R(0)};
   if (p < P) {
     int64_t m = p / g.N, n = p % g.N;
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(SKN_THREADS)
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   auto stage_b = [&](int64_t b) {
-    const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+    const V *B = reinterpret_cast<const V *>(g.B) + b_batch_off(g, b);
     for (int i = tid; i < K * N; i += SKN_THREADS) {
       int k, n;
       if (g.opB == QF_OP_N) {
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(SKN_THREADS)
     const int rows = (int)min((int64_t)rm, g.M - m0);
     __syncthreads();  // previous item done with smem
     if (b != cur_b) {
-      const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+      const V *B = reinterpret_cast<const V *>(g.B) + b_batch_off(g, b);
       for (int i = tid; i < K * N; i += SKN_THREADS) {
         int k, n;
         if (g.opB == QF_OP_N) {
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(RB_THREADS)
     const int rows = (int)min((int64_t)rows_per_item, g.M - r0);
     if (b != cur_b) {
       __syncthreads();
-      const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+      const V *B = reinterpret_cast<const V *>(g.B) + b_batch_off(g, b);
       for (int i = tid; i < K * N; i += RB_THREADS) {
         int k, n;
         if (g.opB == QF_OP_N) {
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     f_base(st, b, r0);
     if (b != cur_b) {  // CTA-uniform: every warp walks the same steps
       __syncthreads();
-      const float2 *B = reinterpret_cast<const float2 *>(g.B) + b * g.sB;
+      const float2 *B = reinterpret_cast<const float2 *>(g.B) + b_batch_off(g, b);
       for (int i = threadIdx.x; i < K * NN; i += RS_WARPS * 32) {
         const int k = i / NN, n = i - k * NN;
         float2 v = make_float2(0.f, 0.f);
@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(GV_THREADS)
     const int64_t r0 = (item - b * items_per_b) * rows_per_item;
     const int64_t r1 = min(g.M, r0 + rows_per_item);
     const V *A = reinterpret_cast<const V *>(g.A) + a_batch_off(g, b);
-    const V *B = reinterpret_cast<const V *>(g.B) + b * g.sB;
+    const V *B = reinterpret_cast<const V *>(g.B) + b_batch_off(g, b);
     V *C = reinterpret_cast<V *>(g.C) + b * g.sC;
     for (int64_t m = r0 + warp * 4; m < r1; m += (GV_THREADS / 32) * 4) {
       V acc[4][NC];
@@ -1257,6 +1257,37 @@ int qf_cgemm_c64_gather_boff(int mode, int64_t batch, int64_t M, int64_t N, int6
   if ((mode == QF_GEMM_AUTO && qf::tc3_eligible(g)) || mode == QF_GEMM_TC3) {
     if (qf::tc3_gather_ok(g)) return qf::gemm_tc3(g, s);
   }
+  return qf::gemm_simt<float>(g, s);
+}
+
+int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                    int64_t lda, int64_t strideA, int opA, const int64_t *a_boff,
+                    const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
+                    int64_t strideB, int opB, const int64_t *b_boff, void *C, int64_t ldc,
+                    int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                    float beta_im, void *stream) {
+  QF_REQUIRE((a_roff != nullptr) == (a_coff != nullptr), "gemm_ex: a_roff/a_coff must pair");
+  const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
+  const bool a_even = (mode & QF_BOFF_EVEN) != 0, b_even = (mode & QF_BBOFF_EVEN) != 0;
+  mode &= ~(QF_GATHER_ROWS_UNIT | QF_BOFF_EVEN | QF_BBOFF_EVEN);
+  // with entry-offset tables the batch strides only key the 16-byte paths
+  if (a_boff) strideA = a_even ? 2 : 1;
+  if (b_boff) strideB = b_even ? 2 : 1;
+  if (a_roff) {
+    lda = std::max<int64_t>(K, 1);
+    opA = QF_OP_N;
+  }
+  qf::GemmArgs g{batch, M, N, K, A, lda, strideA, opA, B, ldb, strideB, opB, C, ldc, strideC,
+                 alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
+                 rows_unit && a_roff != nullptr, a_boff, b_boff};
+  int st = qf::validate(g);
+  if (st != QF_OK) return st;
+  cudaStream_t s = qf::as_stream(stream);
+  if (mode == QF_GEMM_TC3 || (mode == QF_GEMM_AUTO && qf::tc3_eligible(g))) {
+    if (!a_roff || qf::tc3_gather_ok(g)) return qf::gemm_tc3(g, s);
+  }
+  QF_REQUIRE(mode == QF_GEMM_AUTO || mode == QF_GEMM_FFMA || mode == QF_GEMM_TC3,
+             "gemm_ex: unknown mode %d", mode);
   return qf::gemm_simt<float>(g, s);
 }
 

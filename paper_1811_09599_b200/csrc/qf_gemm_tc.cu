@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int64_t tile = work - bidx * tiles;
     const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
     const float2 *A = Ab + a_batch_off(g, bidx);
-    const float2 *B = Bb + bidx * g.sB;
+    const float2 *B = Bb + b_batch_off(g, bidx);
     float2 *C = Cb + bidx * g.sC;
 
     // thread -> operand element mapping
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
     const int64_t tile = work - bidx * tiles;
     const int64_t m0 = (tile / tiles_n) * BM, n0 = (tile % tiles_n) * BN;
     const float2 *A = Ab + a_batch_off(g, bidx);
-    const float2 *B = Bb + bidx * g.sB;
+    const float2 *B = Bb + b_batch_off(g, bidx);
     float2 *C = Cb + bidx * g.sC;
     const int64_t am = m0 + row_l;           // A row (this thread: k in [4*half, 4*half+4))
     const int bn_local = tid % BN;
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
     const float2 *A = Ab + a_batch_off(g, bidx);
-    const float2 *B = Bb + bidx * g.sB;
+    const float2 *B = Bb + b_batch_off(g, bidx);
     fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
     fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
     if (!fa_ok) fa = Ab;
@@ -1115,7 +1115,7 @@ __global__ void __launch_bounds__(V2_THREADS + 32, 1)
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
     const float2 *A = Ab + a_batch_off(g, bidx);
-    const float2 *B = Bb + bidx * g.sB;
+    const float2 *B = Bb + b_batch_off(g, bidx);
     if (a_mode == 1) {
       fa = A;
       if constexpr (SHORTK) {  // short tiles: hide the table load behind the current tile
@@ -1873,7 +1873,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     for (; pc.w < w1; cur_next(pc)) {
       const bool breuse = rd != 0u && pc.run >= rd;
       const float2 *A = Ab + a_batch_off(g, pc.bidx);
-      const float2 *B = Bb + (int64_t)pc.bidx * g.sB;
+      const float2 *B = Bb + b_batch_off(g, pc.bidx);
       const int64_t m0 = (int64_t)pc.mt * BM, n0 = (int64_t)pc.nt * BN;
       // per-tile row bases
       int32_t ro[8];
@@ -2278,7 +2278,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     auto fetch_setup = [&]() {
       if (fc.w >= w1) return;
       const float2 *A = Ab + a_batch_off(g, fc.bidx);
-      const float2 *B = Bb + (int64_t)fc.bidx * g.sB;
+      const float2 *B = Bb + b_batch_off(g, fc.bidx);
       const int64_t m0 = (int64_t)fc.mt * BM;
       if (a_mode == 1 || a_mode == 3) {
 #pragma unroll
@@ -2543,7 +2543,7 @@ static bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1,
 
 // TMA needs 16-byte global strides and a non-gathered A
 bool tma_ok(const GemmArgs &g) {
-  return !g.a_roff && !g.a_boff && g.lda % 2 == 0 && g.sA % 2 == 0 && g.ldb % 2 == 0 &&
+  return !g.a_roff && !g.a_boff && !g.b_boff && g.sA > 0 && g.sB > 0 && g.lda % 2 == 0 && g.sA % 2 == 0 && g.ldb % 2 == 0 &&
          g.sB % 2 == 0 &&
          (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 &&
          g.batch < ((int64_t)1 << 31);
@@ -2704,7 +2704,7 @@ __global__ void __launch_bounds__(V2_THREADS, 1)
     fa_ok = am < g.M;
     fb_ok = bn < g.N;
     const float2 *A = Ab + a_batch_off(g, bidx);
-    const float2 *B = Bb + bidx * g.sB;
+    const float2 *B = Bb + b_batch_off(g, bidx);
     fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
     fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
     if (!fa_ok) fa = Ab;
@@ -3141,7 +3141,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(V2_THREADS + 32, 1)
       fa_ok = am < g.M;
       fb_ok = bn < g.N;
       const float2 *A = Ab + a_batch_off(g, bidx);
-      const float2 *B = Bb + bidx * g.sB;
+      const float2 *B = Bb + b_batch_off(g, bidx);
       fa = (g.opA == QF_OP_N) ? A + am * g.lda + 4 * half : A + (int64_t)(4 * half) * g.lda + am;
       fb = (g.opB == QF_OP_N) ? B + (int64_t)b_k * g.ldb + bn : B + bn * g.ldb + b_k;
       if (!fa_ok) fa = Ab;

@@ -650,13 +650,10 @@ def contract_late(a: Tensor, b: Tensor, late: LateBits) -> Tensor:
         r = _contract_open(a, b, late)
         return r if r is not None else contract(a, b, front=late.rows)
     big, small = (a, b) if late._batched_size(a) >= late._batched_size(b) else (b, a)
-    if late.outs(small):
-        small = late.batch(small)
-    if late.outs(big):
-        fused = _contract_sliced(big, small, late)
-        if fused is not None:
-            return fused
-        big = late.batch(big)
+    fused = _contract_sliced(big, small, late)
+    if fused is not None:
+        return fused
+    big, small = late.batch(big), late.batch(small)
     return contract(big, small)
 
 
@@ -733,62 +730,98 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
 
 
 def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
-    """a (open outputs, no batch axis) x b (batched): slice a's outputs per
-    entry inside the GEMM's operand fetch.  None if not eligible."""
+    """One batched GEMM for a late-sliced network: `a` (the bigger operand)
+    and `b` each either carry the batch axis or still have open outputs
+    (b may also have neither -- broadcast).  An open operand's per-bit-string
+    slice is an entry base offset (qf_cgemm_c64_ex a_boff / b_boff), so
+    nothing is materialised: the big one is read in place (plain or through
+    gathered tables), the small one is a site tensor with its outputs moved
+    in front (memoised layout).  None if not eligible."""
     lb = late.label
-    if (lb not in b.labels or a.data.dtype != torch.complex64 or not _gather_enabled
-            or a.size >= 2 ** 31):
+    if a.data.dtype != torch.complex64 or not _gather_enabled or a.size >= 2 ** 31:
         return None
-    outs = set(late.outs(a))
-    labels = [l for l in a.labels if l not in outs]
-    bset = set(b.labels)
-    k_order = [l for l in labels if l in bset]
-    a_free = [l for l in labels if l not in bset]
+    nb = late.nb
+    ao, bo = late.outs(a), late.outs(b)
+    a_bat, b_bat = lb in a.labels, lb in b.labels
+    if (a_bat and (ao or a.labels[0] != lb)) or (b_bat and bo) or (not a_bat and not ao):
+        return None
+    a_core = [l for l in a.labels if l != lb and l not in ao]
+    b_core = [l for l in b.labels if l != lb and l not in bo]
+    bset, aset = set(b_core), set(a_core)
+    k_order = [l for l in a_core if l in bset]
+    a_free = [l for l in a_core if l not in bset]
+    b_free = [l for l in b_core if l not in aset]
+    if any(_is_batch(l) for l in a_free + b_free):
+        return None
     for l in k_order:
         if a.dim_of(l) != b.dim_of(l):
             raise ValueError(f"dimension mismatch on {l!r}: {a.dim_of(l)} vs {b.dim_of(l)}")
-    aset = set(labels)
-    b_free = [l for l in b.labels if l not in aset and l != lb]
     m = math.prod(a.dim_of(l) for l in a_free)
     k = math.prod(a.dim_of(l) for l in k_order)
     n = math.prod(b.dim_of(l) for l in b_free)
-    if m > 2 ** 22 or k > 4096 or k == 0:
+    if k == 0 or k > 4096:
         return None
-    nb = late.nb
-    # small operand: [batch][K][N] (N) or [batch][N][K] (T)
-    n_layout = [lb] + k_order + b_free
-    t_layout = [lb] + b_free + k_order
-    if list(b.labels) == n_layout:
-        B, opB = b, _lib.OP_N
-    elif list(b.labels) == t_layout:
-        B, opB = b, _lib.OP_T
+    lib = _lib.load()
+    flags = 0
+    # ---- A: batched entries or per-bit-string slices of the open tensor
+    a_boff = roff = coff = None
+    entry_a = a.size // nb if a_bat else 0
+    if ao:
+        st_a = _strides(a)
+        if all(st_a[l] % 2 == 0 for l in ao):
+            flags |= _lib.BOFF_EVEN
+    core_labels = a.labels[1:] if a_bat else tuple(l for l in a.labels if l not in ao)
+    if list(core_labels) == a_free + k_order and (a_bat or list(a.labels) == ao + a_core):
+        opA, lda = _lib.OP_N, max(k, 1)
+    elif list(core_labels) == k_order + a_free and (a_bat or list(a.labels) == ao + a_core):
+        opA, lda = _lib.OP_T, max(m, 1)
     else:
-        B, opB = b.transpose_to(n_layout), _lib.OP_N
-    a_outs = late.outs(a)
-    st_a = _strides(a)
-    flags = _lib.BOFF_EVEN if all(st_a[l] % 2 == 0 for l in a_outs) else 0
-    if list(a.labels) == a_outs + a_free + k_order:
-        roff = coff = None        # every slice is a plain row-major [M][K] block
+        if m > 2 ** 22:
+            return None
+        if a_bat:
+            roff, coff, ru = _gather_tables(a.dims[1:], a.labels[1:], a_free, k_order,
+                                            a.data.device)
+        else:
+            roff, coff, ru = _gather_tables(a.dims, a.labels, a_free, k_order, a.data.device)
+        flags |= _lib.GATHER_ROWS_UNIT if ru else 0
+        opA, lda = _lib.OP_N, max(k, 1)
+    if ao:
+        a_boff = late.offsets(a, ao)
+    # ---- B: batched entries, per-bit-string slices, or broadcast
+    b_boff = None
+    if bo:
+        B = b.transpose_to(tuple(bo + k_order + b_free))
+        opB, sB = _lib.OP_N, 0
+        b_boff = late.offsets(B, bo)
+        if all(_strides(B)[l] % 2 == 0 for l in bo):
+            flags |= _lib.BBOFF_EVEN
+    elif b_bat:
+        n_lay, t_lay = [lb] + k_order + b_free, [lb] + b_free + k_order
+        if list(b.labels) == t_lay:
+            B, opB = b, _lib.OP_T
+        else:
+            B, opB = b.transpose_to(tuple(n_lay)), _lib.OP_N
+        sB = k * n
     else:
-        roff, coff, rows_unit = _gather_tables(a.dims, a.labels, a_free, k_order, a.data.device)
-        flags |= _lib.GATHER_ROWS_UNIT if rows_unit else 0
-    boff = late.offsets(a, a_outs)
+        B, opB, sB = b.transpose_to(tuple(k_order + b_free)), _lib.OP_N, 0
+    ldb = max(n, 1) if opB == _lib.OP_N else max(k, 1)
     out = device_buffer(nb * m * n, a.data.dtype, a.data.device)
-    ldb = n if opB == _lib.OP_N else k
+    tag = ("G" if roff is not None else "NT"[opA]) + ("S" if ao else "") + "," + \
+        ("S" if bo else "B" if b_bat else "0")
+    vp = ctypes.c_void_p
     with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
-                f"b{nb} m{m} n{n} k{k} {'P' if roff is None else 'S'}{'NT'[opB]}" if _timer else ""):
-        st = _lib.load().qf_cgemm_c64_gather_boff(
-            _gemm_mode | flags, nb, m, n, k, ctypes.c_void_p(a.data.data_ptr()),
-            ctypes.c_void_p(boff.data_ptr()),
-            ctypes.c_void_p(roff.data_ptr() if roff is not None else 0),
-            ctypes.c_void_p(coff.data_ptr() if coff is not None else 0),
-            ctypes.c_void_p(B.data.data_ptr()), max(ldb, 1), k * n, opB, ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
-            stream_handle())
-    _lib.check(st, "gemm_gather_boff")
+                f"b{nb} m{m} n{n} k{k} {tag}" if _timer else ""):
+        st = lib.qf_cgemm_c64_ex(
+            _gemm_mode | flags, nb, m, n, k, vp(a.data.data_ptr()), lda, entry_a, opA,
+            vp(a_boff.data_ptr() if a_boff is not None else 0),
+            vp(roff.data_ptr() if roff is not None else 0),
+            vp(coff.data_ptr() if coff is not None else 0),
+            vp(B.data.data_ptr()), ldb, sB, opB, vp(b_boff.data_ptr() if b_boff is not None else 0),
+            vp(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+    _lib.check(st, "gemm_ex")
     labels_out = (lb,) + tuple(a_free) + tuple(b_free)
     dims = (nb,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
     return Tensor(labels_out, out, dims)
-
 
 # ---------------------------------------------------------------------------
 # permutation API shims (reference signatures; one device pass whatever the plan)

@@ -333,3 +333,33 @@ def test_late_open_contract_equals_plain(mode, case):
     assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
     outs = [l for l in got.labels if l.startswith("out")]
     assert list(got.labels[:len(outs)]) == outs   # open outputs lead
+
+
+@pytest.mark.parametrize("mode", ["auto", "ffma", "tc3"])
+@pytest.mark.parametrize("case", range(4))
+def test_late_batched_times_open_site(mode, case):
+    """A batched intermediate times a tensor whose outputs are still open:
+    the small operand's slice per bit-string is read in place through B
+    entry offsets (qf_cgemm_c64_ex b_boff) -- equals slicing it first."""
+    rng = np.random.default_rng(500 + case)
+    nb = [64, 17, 128, 1024][case]
+    dims = {"p": 8, "q": 8, "s": 8, "t": 8, "v": 8, "out0": 2, "out1": 2}
+    a_labels = [["@b", "p", "q", "s", "t"], ["@b", "s", "p", "t", "q"], ["@b", "t", "s", "p", "q"],
+                ["@b", "p", "s", "q", "t"]][case]
+    b_labels = [["t", "s", "v", "out0"], ["out1", "t", "v", "s", "out0"], ["s", "out0", "t"],
+                ["t", "v", "s", "out1"]][case]
+    outs = [l for l in b_labels if l.startswith("out")]
+    A = _rand(rng, [nb] + [dims[l] for l in a_labels[1:]], np.complex64)
+    Bm = _rand(rng, [dims[l] for l in b_labels], np.complex64)
+    bits = rng.integers(0, 2, size=(2, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"out0": 0, "out1": 1})
+    prev = tc.set_gemm_mode(mode)
+    try:
+        ta, tb = tc.Tensor(a_labels, A), tc.Tensor(b_labels, Bm)
+        got = tc.contract_late(ta, tb, late)
+        want = tc.contract(ta, late.batch(tb))
+    finally:
+        tc.set_gemm_mode(prev)
+    assert sorted(got.labels) == sorted(want.labels)
+    w = want.transpose_to(got.labels).array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
