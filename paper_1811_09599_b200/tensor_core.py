@@ -448,6 +448,24 @@ def contract_shape(a: Tensor, b: Tensor, skip=()) -> ContractShape:
     return ContractShape(bt, m, k, n)
 
 
+# measured B200 rates (scripts/gemm_bench.py, bench.py --workload permute):
+# gathered-A tensor-core GEMMs ~140 TFLOP/s at long K, plain strided ones fed
+# by TMA ~205 TFLOP/s, the permutation ~5.5 TB/s, GEMM operand streams ~5 TB/s
+_RATE_GATHER, _RATE_TMA, _RATE_PERMUTE, _RATE_HBM = 140e12, 205e12, 5.5e12, 5.0e12
+
+
+def _permute_pays(bt: int, m: int, k: int, n: int) -> bool:
+    """For compute-bound shapes a separate permute of the big operand plus
+    the TMA-fed GEMM beats fetching it through offset tables."""
+    if k < 128 or n < 128:
+        return False
+    flops = 8.0 * bt * m * k * n
+    nbytes = 8.0 * bt * (m * k + k * n + m * n)
+    t_gather = max(flops / _RATE_GATHER, nbytes / _RATE_HBM)
+    t_perm = 16.0 * bt * m * k / _RATE_PERMUTE + max(flops / _RATE_TMA, nbytes / _RATE_HBM)
+    return t_perm < t_gather
+
+
 def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int = 10,
              front=()) -> Tensor:
     """Contract over all shared labels (batch '@' labels are kept).
@@ -501,7 +519,8 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     entry = a.size // max(bt, 1)
     if (list(a.labels) not in (a_n, a_t) and a.data.dtype == torch.complex64
             and list(a.labels[:len(batch)]) == batch and entry >= 4096 and entry < 2 ** 31
-            and m <= 2 ** 22 and k <= 4096 and _gather_enabled):
+            and m <= 2 ** 22 and k <= 4096 and _gather_enabled
+            and not _permute_pays(bt, m, k, n)):
         # fuse the big operand's permutation into the GEMM fetch
         nb = len(batch)
         if front:
