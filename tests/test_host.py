@@ -216,3 +216,53 @@ def test_completions_match_reference_rule():
     rng = np.random.Generator(np.random.PCG64(5))
     want = np.sort(rng.choice(256, size=32, replace=False))
     assert list(ae._completions(8, 32, 5)) == list(want)
+
+
+def test_late_bits_validation_and_outs():
+    """LateBits host logic (no GPU): the bit matrix contract, the default
+    limit (half the batch) and which labels count as open outputs."""
+    import torch
+    from paper_1811_09599_b200 import tensor_core as tc
+    bits = torch.zeros((3, 64), dtype=torch.int32)
+    late = tc.LateBits(bits, {"out0": 0, "out2": 2})
+    assert (late.nb, late.limit, late.label) == (64, 32, "@b")
+    assert tc.LateBits(bits, {}, limit=5).limit == 5
+    t = tc.Tensor(("e0_1", "out0", "e0_5", "out2"), torch.zeros(8 * 2 * 8 * 2), (8, 2, 8, 2))
+    assert late.outs(t) == ["out0", "out2"]
+    assert late._batched_size(t) == 8 * 8 * 64
+    with pytest.raises(ValueError):
+        tc.LateBits(bits.to(torch.int64), {})
+    with pytest.raises(ValueError):
+        tc.LateBits(torch.zeros(64, dtype=torch.int32), {})
+    with pytest.raises(ValueError):
+        tc.LateBits(bits.t(), {})          # not contiguous
+
+
+def test_contract_shape_counts_open_outputs_like_batch():
+    """Per-amplitude flop accounting: batch axes (shared or not) and open
+    outputs awaiting a late slice are not part of m or n."""
+    import torch
+    from paper_1811_09599_b200 import tensor_core as tc
+    a = tc.Tensor(("@b", "p", "k"), torch.zeros(4 * 8 * 16), (4, 8, 16))
+    b = tc.Tensor(("k", "q", "out3"), torch.zeros(16 * 5 * 2), (16, 5, 2))
+    shp = tc.contract_shape(a, b, skip={"out3"})
+    assert (shp.batch, shp.m, shp.k, shp.n) == (8, 8, 16, 5)
+    assert shp.flops == 8 * 8 * 16 * 5
+    assert tc.contract_shape(a, b).n == 10
+
+
+def test_batch_order_follows_plan_site_order():
+    lat = qf.Lattice.rectangle(5, 5)
+    circ = qf.generate_rqc(lat, "1+8+1", seed=0)
+    eng = qf.AmplitudeEngine(circ, qf.grid_plan(lat, n_cuts=1))
+    rng = np.random.default_rng(0)
+    bits = rng.integers(0, 2, size=(200, 25))
+    order = eng.batch_order(bits)
+    assert sorted(order.tolist()) == list(range(200))
+    seq = []
+    for step in eng.plan.steps():
+        for x in step.inputs:
+            if x.startswith("t") and x[1:].isdigit() and int(x[1:]) not in seq:
+                seq.append(int(x[1:]))
+    keys = [tuple(row[q] for q in seq) for row in bits[order]]
+    assert keys == sorted(keys)
