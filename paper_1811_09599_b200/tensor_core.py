@@ -312,7 +312,7 @@ class Tensor:
     uploaded once.  `.array` downloads a numpy copy (API compatibility with
     the reference's numpy-backed Tensor)."""
 
-    __slots__ = ("labels", "data", "dims", "_layouts")
+    __slots__ = ("labels", "_data", "dims", "_layouts", "_view")
 
     def __init__(self, labels: Sequence[str], array, dims: Optional[Sequence[int]] = None):
         labels = tuple(labels)
@@ -335,9 +335,59 @@ class Tensor:
         if len(dims) != len(labels):
             raise ValueError(f"{len(dims)}-d array with {len(labels)} labels")
         self.labels = labels
-        self.data = data
+        self._data = data
         self.dims = dims
         self._layouts = None  # memoised transposes (labels -> Tensor)
+        self._view = None     # (base, label, value) of a lazy fix (see fix_view)
+
+    @property
+    def data(self):
+        """Flat device buffer (a lazy fix view is materialised on first use)."""
+        d = self._data
+        if d is None:
+            base, label, value = self._view
+            d = fix_buffer(base.data, base.dims, base.labels.index(label), value)
+            self._data = d
+        return d
+
+    @data.setter
+    def data(self, value):
+        self._data = value
+
+    @property
+    def buf(self):
+        """The storage (for dtype/device queries); never materialises a view."""
+        return self._data if self._data is not None else self._view[0].buf
+
+    def raw(self):
+        """(buffer, element offset, stride of the leading index) -- a view's
+        entries along its leading (batch) index are contiguous blocks of the
+        base buffer; a plain tensor is (data, 0, entry size)."""
+        if self._data is not None or self._view is None:
+            lead = self.dims[0] if self.dims else 1
+            return self.data, 0, self.size // max(lead, 1)
+        base, label, value = self._view
+        ax = base.labels.index(label)
+        block = math.prod(base.dims[ax + 1:])
+        return base.data, value * block, base.dims[ax] * block if ax == 1 else 0
+
+    def fix_view(self, label: str, value: int) -> "Tensor":
+        """`fix` without a copy when the fixed index is the outermost one or
+        directly follows a leading batch axis: the result is a strided view
+        (each batch entry a contiguous block) that the late-slicing GEMMs read
+        in place; any other use materialises it.  Otherwise a plain fix."""
+        ax = self.labels.index(label)
+        if self._view is not None or not (ax == 0 or (ax == 1 and _is_batch(self.labels[0]))):
+            return self.fix(label, value)
+        if not 0 <= value < self.dims[ax]:
+            raise ValueError(f"value {value} out of range for {label!r} (dim {self.dims[ax]})")
+        t = Tensor.__new__(Tensor)
+        t.labels = self.labels[:ax] + self.labels[ax + 1:]
+        t.dims = self.dims[:ax] + self.dims[ax + 1:]
+        t._data = None
+        t._layouts = None
+        t._view = (self, label, int(value))
+        return t
 
     @property
     def size(self) -> int:
@@ -345,11 +395,11 @@ class Tensor:
 
     @property
     def nbytes(self) -> int:
-        return self.size * _elem_bytes(self.data)
+        return self.size * _elem_bytes(self.buf)
 
     @property
     def dtype(self):
-        return _NP_OF[self.data.dtype]
+        return _NP_OF[self.buf.dtype]
 
     @property
     def array(self) -> np.ndarray:
@@ -477,7 +527,7 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     their operand's free group when that costs no extra pass (gathered big
     operand; memoised small-operand layout), so a later per-bit-string slice
     reads long contiguous runs."""
-    if a.data.dtype != b.data.dtype:
+    if a.buf.dtype != b.buf.dtype:
         raise ValueError(f"dtype mismatch: {a.dtype} vs {b.dtype}")
     if b.size > a.size:
         # the big operand goes first (its layout decides the GEMM); the output
@@ -605,7 +655,7 @@ class LateBits:
     def offsets(self, t: Tensor, outs) -> "torch.Tensor":
         """Per-entry element offsets of the bit-strings' slice of `t`."""
         st = _strides(t)
-        off = torch.empty(max(self.nb, 1), dtype=torch.int64, device=t.data.device)
+        off = torch.empty(max(self.nb, 1), dtype=torch.int64, device=t.buf.device)
         rows = (_i32 * max(1, len(outs)))(*[self.rows[l] for l in outs])
         strides = (ctypes.c_int64 * max(1, len(outs)))(*[st[l] for l in outs])
         with _timed("gather", 0, 4 * self.nb * (len(outs) + 2), "bit_offsets" if _timer else ""):
@@ -696,7 +746,7 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     slice is then one contiguous block per entry.  None if not eligible."""
     big, small = (a, b) if a.size >= b.size else (b, a)
     so = late.outs(small)
-    if (not so or big.data.dtype != torch.complex64 or not _gather_enabled
+    if (not so or big.buf.dtype != torch.complex64 or not _gather_enabled
             or big.size >= 2 ** 31):
         return None
     sset, bset = set(small.labels), set(big.labels)
@@ -753,11 +803,11 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     and `b` each either carry the batch axis or still have open outputs
     (b may also have neither -- broadcast).  An open operand's per-bit-string
     slice is an entry base offset (qf_cgemm_c64_ex a_boff / b_boff), so
-    nothing is materialised: the big one is read in place (plain or through
-    gathered tables), the small one is a site tensor with its outputs moved
-    in front (memoised layout).  None if not eligible."""
+    nothing is materialised: the big one is read in place (plain, through
+    gathered tables, or as a cut-slice view), the small one is a site tensor
+    with its outputs moved in front (memoised layout).  None if not eligible."""
     lb = late.label
-    if a.data.dtype != torch.complex64 or not _gather_enabled or a.size >= 2 ** 31:
+    if a.buf.dtype != torch.complex64 or not _gather_enabled or a.size >= 2 ** 31:
         return None
     nb = late.nb
     ao, bo = late.outs(a), late.outs(b)
@@ -782,9 +832,13 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
         return None
     lib = _lib.load()
     flags = 0
-    # ---- A: batched entries or per-bit-string slices of the open tensor
+    # ---- A: batched entries (or a cut-slice view of them), or per-bit-string
+    # slices of the open tensor
     a_boff = roff = coff = None
-    entry_a = a.size // nb if a_bat else 0
+    if a_bat:
+        a_buf, a_off, entry_a = a.raw()
+    else:
+        a_buf, a_off, entry_a = a.data, 0, 0
     if ao:
         st_a = _strides(a)
         if all(st_a[l] % 2 == 0 for l in ao):
@@ -799,9 +853,9 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
             return None
         if a_bat:
             roff, coff, ru = _gather_tables(a.dims[1:], a.labels[1:], a_free, k_order,
-                                            a.data.device)
+                                            a.buf.device)
         else:
-            roff, coff, ru = _gather_tables(a.dims, a.labels, a_free, k_order, a.data.device)
+            roff, coff, ru = _gather_tables(a.dims, a.labels, a_free, k_order, a.buf.device)
         flags |= _lib.GATHER_ROWS_UNIT if ru else 0
         opA, lda = _lib.OP_N, max(k, 1)
     if ao:
@@ -824,14 +878,14 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     else:
         B, opB, sB = b.transpose_to(tuple(k_order + b_free)), _lib.OP_N, 0
     ldb = max(n, 1) if opB == _lib.OP_N else max(k, 1)
-    out = device_buffer(nb * m * n, a.data.dtype, a.data.device)
-    tag = ("G" if roff is not None else "NT"[opA]) + ("S" if ao else "") + "," + \
-        ("S" if bo else "B" if b_bat else "0")
+    out = device_buffer(nb * m * n, a.buf.dtype, a.buf.device)
+    tag = ("G" if roff is not None else "NT"[opA]) + ("S" if ao else "") + \
+        ("V" if a._data is None else "") + "," + ("S" if bo else "B" if b_bat else "0")
     vp = ctypes.c_void_p
     with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
                 f"b{nb} m{m} n{n} k{k} {tag}" if _timer else ""):
         st = lib.qf_cgemm_c64_ex(
-            _gemm_mode | flags, nb, m, n, k, vp(a.data.data_ptr()), lda, entry_a, opA,
+            _gemm_mode | flags, nb, m, n, k, vp(a_buf.data_ptr() + 8 * a_off), lda, entry_a, opA,
             vp(a_boff.data_ptr() if a_boff is not None else 0),
             vp(roff.data_ptr() if roff is not None else 0),
             vp(coff.data_ptr() if coff is not None else 0),

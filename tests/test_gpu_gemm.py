@@ -363,3 +363,33 @@ def test_late_batched_times_open_site(mode, case):
     assert sorted(got.labels) == sorted(want.labels)
     w = want.transpose_to(got.labels).array
     assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+
+
+@pytest.mark.parametrize("mode", ["auto", "ffma", "tc3"])
+@pytest.mark.parametrize("nb", [8, 256])
+def test_cut_slice_view_read_in_place(mode, nb):
+    """Slice-late cuts: with the kept-open cut index right after the batch
+    axis, a per-path fix is a strided view that the next late-sliced GEMM
+    reads in place -- equal to fixing (copying) first."""
+    rng = np.random.default_rng(600 + nb)
+    A = _rand(rng, (nb, 4, 8, 8, 8), np.complex64)                 # @b c p q s
+    W = _rand(rng, (8, 8, 2), np.complex64)                        # p q out1
+    bits = rng.integers(0, 2, size=(2, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"out0": 0, "out1": 1})
+    prev = tc.set_gemm_mode(mode)
+    try:
+        lead = tc.Tensor(["@b", "c", "p", "q", "s"], A)
+        tw = tc.Tensor(["p", "q", "out1"], W)
+        for v in (0, 3):
+            view = lead.fix_view("c", v)
+            assert view._data is None
+            got = tc.contract_late(view, tw, late)
+            assert view._data is None                               # read in place
+            want = tc.contract(lead.fix("c", v), late.batch(tw))
+            w = want.transpose_to(got.labels).array
+            assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+            np.testing.assert_array_equal(view.array, lead.fix("c", v).array)
+        mid = lead.fix_view("q", 1)                                 # not leading: plain fix
+        assert mid._data is not None
+    finally:
+        tc.set_gemm_mode(prev)
