@@ -173,6 +173,26 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
                     int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                     float beta_im, void *stream);
 
+/*
+ * Strided-view A for the TMA-fed tensor-core kernel (no offset tables): the
+ * big operand of a contraction whose shared labels are its innermost index
+ * (kin, contiguous, kin % 8 == 0) and at most one more index (kout), with its
+ * free labels in at most two runs (rows_a fast, rows_b slow):
+ *   A(b, r, k) = A + b*strideA + ra*s_rows_a + rb*s_rows_b + ko*s_kout + ki
+ *   r = rb*rows_a + ra,  k = ko*kin + ki        (element strides, all even)
+ * b_boff/b_nslice: B entries as whole [K][N] slices of a buffer of b_nslice
+ * (late output slicing; NULL/0 = strided B).  Returns QF_ERR_UNSUPPORTED when
+ * the view or shape does not fit the TMA kernel (the caller falls back to
+ * qf_cgemm_c64_ex with offset tables).
+ */
+int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                      int64_t strideA, int64_t kin, int64_t rows_a, int64_t s_rows_a,
+                      int64_t kout, int64_t s_kout, int64_t rows_b, int64_t s_rows_b,
+                      const void *B, int64_t ldb, int64_t strideB, int opB,
+                      const int64_t *b_boff, int64_t b_nslice, void *C, int64_t ldc,
+                      int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                      float beta_im, void *stream);
+
 /* complex128 twin (FFMA/DFMA only), for dtype=complex128 engines. */
 int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
                   const void *A, int64_t lda, int64_t strideA, int opA,

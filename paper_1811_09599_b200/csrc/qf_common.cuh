@@ -52,6 +52,13 @@ struct GemmArgs {
   // per-batch entry base offsets of B replacing b*sB (a site tensor whose
   // output is sliced per bit-string: B(b) = B + b_boff[b]); any alignment
   const int64_t *b_boff = nullptr;
+  // b_boff values are whole [K][N] blocks of a B buffer holding b_nslice of
+  // them (the TMA kernel then addresses B slice b_boff[b] / (K*N)); 0 = unknown
+  int64_t b_nslice = 0;
+  // A as a strided view read by a 5-D TMA map (TMA kernel only; v_kin = 0:
+  // unused): k = ko*v_kin + ki with ki innermost and contiguous, row
+  // r = rb*v_ra + ra; v_s* are element strides of ra, ko and rb
+  int64_t v_kin = 0, v_ra = 0, v_sra = 0, v_kout = 0, v_skout = 0, v_rb = 0, v_srb = 0;
 };
 
 __device__ __forceinline__ int64_t b_batch_off(const GemmArgs &g, int64_t b) {

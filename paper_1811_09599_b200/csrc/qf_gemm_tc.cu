@@ -1824,6 +1824,8 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
       for (; pc.w < w1; cur_next(pc)) {
         const bool breuse = rd != 0u && pc.run >= rd;
         const int32_t m0 = (int32_t)(pc.mt * BM), n0 = (int32_t)(pc.nt * BN), b = (int32_t)pc.bidx;
+        const int32_t bslice =
+            g.b_boff ? (int32_t)(__ldg(g.b_boff + pc.bidx) / (g.K * g.N)) : b;
         for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
           const uint32_t slot = f & (RAW - 1);
           if (f >= RAW) mbar_wait(&rawfree[slot], ((f / RAW) + 1) & 1u);
@@ -1832,20 +1834,33 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                        : "memory");
           const int32_t k0 = (int32_t)(kb * KB);
-          // A: opA N -> coords {2k, m, b}; opA T -> {2m, k, b}
-          const int32_t a0 = g.opA == QF_OP_N ? 2 * k0 : 2 * m0, a1 = g.opA == QF_OP_N ? m0 : k0;
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-              "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(rawa + slot * L::RAWA_SLOT),
-              "l"(&tmA), "r"(a0), "r"(a1), "r"(b), "r"(bar)
-              : "memory");
+          if (g.v_kin) {
+            // A view: {2 ki, ra, ko, rb, b}; the box spans 128 rows of (ra, rb)
+            const uint32_t kbi = (uint32_t)(g.v_kin / KB);
+            const int32_t ki = (int32_t)(kb % kbi) * (2 * KB), ko = (int32_t)(kb / kbi);
+            const int32_t ra = g.v_ra >= BM ? (int32_t)(m0 % g.v_ra) : 0;
+            const int32_t rb = (int32_t)(m0 / g.v_ra);
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(rawa + slot * L::RAWA_SLOT),
+                "l"(&tmA), "r"(ki), "r"(ra), "r"(ko), "r"(rb), "r"(b), "r"(bar)
+                : "memory");
+          } else {
+            // A: opA N -> coords {2k, m, b}; opA T -> {2m, k, b}
+            const int32_t a0 = g.opA == QF_OP_N ? 2 * k0 : 2 * m0, a1 = g.opA == QF_OP_N ? m0 : k0;
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(rawa + slot * L::RAWA_SLOT),
+                "l"(&tmA), "r"(a0), "r"(a1), "r"(b), "r"(bar)
+                : "memory");
+          }
           if (!breuse) {
-            // B: opB N -> {2n, k, b}; opB T -> {2k, n, b}
+            // B: opB N -> {2n, k, slice}; opB T -> {2k, n, slice}
             const int32_t c0 = g.opB == QF_OP_N ? 2 * n0 : 2 * k0, c1 = g.opB == QF_OP_N ? k0 : n0;
             asm volatile(
                 "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
                 "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(rawb + slot * L::RAWB_SLOT),
-                "l"(&tmB), "r"(c0), "r"(c1), "r"(b), "r"(bar)
+                "l"(&tmB), "r"(c0), "r"(c1), "r"(bslice), "r"(bar)
                 : "memory");
           }
         }
@@ -2541,10 +2556,40 @@ static bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// TMA needs 16-byte global strides and a non-gathered A
+// 5-D float tensor map of an A view (dims innermost first, byte strides)
+static bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5],
+                       const uint64_t (&strides)[4], const uint32_t (&box)[5]) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  cuuint64_t d[5];
+  cuuint64_t st[4];
+  cuuint32_t bx[5];
+  for (int i = 0; i < 5; ++i) d[i] = dims[i], bx[i] = box[i];
+  for (int i = 0; i < 4; ++i) st[i] = strides[i];
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(ptr), d, st, bx, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA needs 16-byte global strides and A/B entries addressable by coordinates
+// (no offset tables; B entry offsets only as whole [K][N] slices)
 bool tma_ok(const GemmArgs &g) {
-  return !g.a_roff && !g.a_boff && !g.b_boff && g.sA > 0 && g.sB > 0 && g.lda % 2 == 0 && g.sA % 2 == 0 && g.ldb % 2 == 0 &&
-         g.sB % 2 == 0 &&
+  const bool a_ok = !g.a_roff && !g.a_boff && g.sA > 0 && g.sA % 2 == 0 && g.lda % 2 == 0;
+  const bool b_ok = g.b_boff ? (g.b_nslice > 0 && (g.K * g.N) % 2 == 0)
+                             : (g.sB > 0 && g.sB % 2 == 0);
+  const bool v_ok = !g.v_kin || (g.v_kin % KB == 0 && g.v_sra % 2 == 0 && g.v_skout % 2 == 0 &&
+                                 g.v_srb % 2 == 0 &&
+                                 (g.v_ra >= BM ? g.v_ra % BM == 0 : BM % g.v_ra == 0) &&
+                                 g.opA == QF_OP_N);
+  return a_ok && b_ok && v_ok && g.ldb % 2 == 0 &&
          (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 &&
          g.batch < ((int64_t)1 << 31);
 }
@@ -2556,12 +2601,26 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   CUtensorMap tmA{}, tmB{};
   if constexpr (TMA) {
     const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
-    const bool okA = g.opA == QF_OP_N
-                         ? make_tmap(&tmA, g.A, 2 * g.K, g.M, nb, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 16, 128, true)
-                         : make_tmap(&tmA, g.A, 2 * g.M, g.K, nb, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 256, 8, false);
+    bool okA;
+    if (g.v_kin) {
+      const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
+      const uint64_t dims[5] = {(uint64_t)(2 * g.v_kin), (uint64_t)g.v_ra, (uint64_t)g.v_kout,
+                                (uint64_t)g.v_rb, nb};
+      const uint64_t strides[4] = {(uint64_t)g.v_sra * 8, (uint64_t)g.v_skout * 8,
+                                   (uint64_t)g.v_srb * 8, (uint64_t)std::max<int64_t>(g.sA, 1) * 8};
+      const uint32_t box[5] = {16, bra, 1, (uint32_t)(BM / bra), 1};
+      okA = make_tmap5(&tmA, g.A, dims, strides, box);
+    } else {
+      okA = g.opA == QF_OP_N
+                ? make_tmap(&tmA, g.A, 2 * g.K, g.M, nb, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 16, 128, true)
+                : make_tmap(&tmA, g.A, 2 * g.M, g.K, nb, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 256, 8, false);
+    }
+    // B entries: strided batch, or b_nslice whole [K][N] slices picked per entry
+    const uint64_t nbs = g.b_boff ? (uint64_t)g.b_nslice : nb;
+    const int64_t sbs = g.b_boff ? g.K * g.N : std::max<int64_t>(g.sB, 1);
     const bool okB = g.opB == QF_OP_N
-                         ? make_tmap(&tmB, g.B, 2 * g.N, g.K, nb, g.ldb * 8, std::max<int64_t>(g.sB, 1) * 8, 128, 8, false)
-                         : make_tmap(&tmB, g.B, 2 * g.K, g.N, nb, g.ldb * 8, std::max<int64_t>(g.sB, 1) * 8, 16, 64, true);
+                         ? make_tmap(&tmB, g.B, 2 * g.N, g.K, nbs, g.ldb * 8, sbs * 8, 128, 8, false)
+                         : make_tmap(&tmB, g.B, 2 * g.K, g.N, nbs, g.ldb * 8, sbs * 8, 16, 64, true);
     if (!okA || !okB) {
       set_error("tc3k: cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld)", (long long)g.M,
                 (long long)g.N, (long long)g.K);
@@ -3395,6 +3454,15 @@ bool tc3_eligible(const GemmArgs &g) {
 int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
   QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
+  if (g.v_kin) {  // A views are read by the TMA-fed short-K kernel only
+    if (!(g.K >= 32 && g.K <= 128 && g.N > 32 && tc::tma_ok(g))) {
+      set_error("tc3: A view (kin %lld, rows %lld x %lld) not TMA-describable for K=%lld N=%lld",
+                (long long)g.v_kin, (long long)g.v_ra, (long long)g.v_rb, (long long)g.K,
+                (long long)g.N);
+      return QF_ERR_UNSUPPORTED;
+    }
+    return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
+  }
   const bool small_n = g.N <= 64;
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables
     QF_REQUIRE(tc3_gather_ok(g), "tc3: gathered A needs K <= 4096");

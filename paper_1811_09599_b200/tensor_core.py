@@ -516,8 +516,78 @@ def _permute_pays(bt: int, m: int, k: int, n: int) -> bool:
     return t_perm < t_gather
 
 
+def _a_view(labels, dims, a_free, k_order):
+    """The big operand's per-entry layout as a TMA-describable view, or None:
+    its innermost label summed (kin, contiguous, dim % 8 == 0), at most one
+    more summed label (kout), and its free labels (in memory order) in at
+    most two runs around kout.  -> (kin, rows_a, s_rows_a, kout, s_kout,
+    rows_b, s_rows_b) in elements (see qf_cgemm_c64_view)."""
+    if not k_order or not labels or labels[-1] != k_order[-1] or len(k_order) > 2:
+        return None
+    if [l for l in labels if l not in k_order] != list(a_free):
+        return None
+    dim = dict(zip(labels, dims))
+    stride, acc = {}, 1
+    for l, d in zip(reversed(labels), reversed(dims)):
+        stride[l] = acc
+        acc *= d
+    kin = dim[k_order[-1]]
+    if kin % 8:
+        return None
+    if len(k_order) == 2:
+        ko = k_order[0]
+        pos = labels.index(ko)
+        run_b, run_a = labels[:pos], labels[pos + 1:-1]
+        kout, s_kout = dim[ko], stride[ko]
+    else:
+        run_b, run_a = (), labels[:-1]
+        kout, s_kout = 1, kin
+    if not run_a:
+        return None            # summed labels contiguous: a plain layout
+    rows_a = math.prod(dim[l] for l in run_a)
+    s_rows_a = stride[run_a[-1]]
+    rows_b = math.prod(dim[l] for l in run_b) if run_b else 1
+    s_rows_b = stride[run_b[-1]] if run_b else acc
+    if not (rows_a % 128 == 0 if rows_a >= 128 else 128 % rows_a == 0):
+        return None
+    if any(x % 2 for x in (s_rows_a, s_kout, s_rows_b)):
+        return None
+    return kin, rows_a, s_rows_a, kout, s_kout, rows_b, s_rows_b
+
+
+def _gemm_view(nb, m, n, k, a_ptr, strideA, view, B, ldb, sB, opB, out, b_boff=None,
+               b_nslice=0) -> bool:
+    """Run the TMA-fed kernel on a view of the big operand; False if the
+    library reports the shape/view unsupported (caller falls back)."""
+    if _gemm_mode == _lib.GEMM_FFMA or strideA % 2 or not _view_enabled:
+        return False
+    kin, ra, sra, ko, sko, rb, srb = view
+    lib = _lib.load()
+    with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
+                f"b{nb} m{m} n{n} k{k} V{'NT'[opB]}" if _timer else ""):
+        st = lib.qf_cgemm_c64_view(
+            _gemm_mode, nb, m, n, k, ctypes.c_void_p(a_ptr), strideA, kin, ra, sra, ko, sko, rb,
+            srb, ctypes.c_void_p(B.data.data_ptr()), ldb, sB, opB,
+            ctypes.c_void_p(b_boff.data_ptr() if b_boff is not None else 0), int(b_nslice),
+            ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+    if st == _lib.QF_ERR_UNSUPPORTED:
+        return False
+    _lib.check(st, "gemm_view")
+    return True
+
+
+_view_enabled = True
+
+
+def set_view(enabled: bool) -> bool:
+    """Enable/disable TMA-fed strided views of the big operand; returns the previous value."""
+    global _view_enabled
+    prev, _view_enabled = _view_enabled, bool(enabled)
+    return prev
+
+
 def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int = 10,
-             front=()) -> Tensor:
+             front=(), tail=()) -> Tensor:
     """Contract over all shared labels (batch '@' labels are kept).
 
     Output labels: batch labels (a's order), then a's free labels, then
@@ -526,7 +596,9 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     `front` (open outputs awaiting a late slice) are moved to the front of
     their operand's free group when that costs no extra pass (gathered big
     operand; memoised small-operand layout), so a later per-bit-string slice
-    reads long contiguous runs."""
+    reads long contiguous runs.  Labels in `tail` (those of the operand this
+    result meets next) go last among the small operand's free labels, so the
+    next contraction finds a summed label innermost (TMA-fed view)."""
     if a.buf.dtype != b.buf.dtype:
         raise ValueError(f"dtype mismatch: {a.dtype} vs {b.dtype}")
     if b.size > a.size:
@@ -543,6 +615,8 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     b_free = [l for l in b.labels if l not in aset]
     if front:
         b_free = [l for l in b_free if l in front] + [l for l in b_free if l not in front]
+    if tail:
+        b_free = [l for l in b_free if l not in tail] + [l for l in b_free if l in tail]
     # summed-index order follows the bigger operand so it is not permuted
     if a.size >= b.size:
         k_order = shared_a
@@ -571,14 +645,19 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
             and list(a.labels[:len(batch)]) == batch and entry >= 4096 and entry < 2 ** 31
             and m <= 2 ** 22 and k <= 4096 and _gather_enabled
             and not _permute_pays(bt, m, k, n)):
-        # fuse the big operand's permutation into the GEMM fetch
+        # fuse the big operand's permutation into the GEMM fetch: a strided
+        # view read by TMA when it has one, else offset tables
         nb = len(batch)
-        if front:
-            a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
-        roff, coff, rows_unit = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order,
-                                               a.data.device)
-        gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out,
-                           rows_unit=rows_unit)
+        view = _a_view(a.labels[nb:], a.dims[nb:], a_free, k_order)
+        ldb = n if opB == _lib.OP_N else k
+        if view is None or not _gemm_view(bt, m, n, k, a.data.data_ptr(), entry, view, B,
+                                          max(ldb, 1), k * n, opB, out):
+            if front:
+                a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
+            roff, coff, rows_unit = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order,
+                                                   a.data.device)
+            gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out,
+                               rows_unit=rows_unit)
     else:
         if front and list(a.labels) not in (a_n, a_t):   # permuted anyway
             a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
@@ -704,7 +783,7 @@ class LateBits:
 _i32 = ctypes.c_int32
 
 
-def contract_late(a: Tensor, b: Tensor, late: LateBits) -> Tensor:
+def contract_late(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Tensor:
     """`contract` for networks whose outputs are sliced late (LateBits).
 
     Both operands without a batch axis and few open outputs between them:
@@ -713,17 +792,17 @@ def contract_late(a: Tensor, b: Tensor, late: LateBits) -> Tensor:
     fused into the GEMM's gathered operand fetch when it can be."""
     oa, ob = late.outs(a), late.outs(b)
     if not oa and not ob:
-        return contract(a, b)
+        return contract(a, b, tail=tail)
     lb = late.label
     if lb not in a.labels and lb not in b.labels and 2 ** (len(oa) + len(ob)) <= late.limit:
-        r = _contract_open(a, b, late)
-        return r if r is not None else contract(a, b, front=late.rows)
+        r = _contract_open(a, b, late, tail)
+        return r if r is not None else contract(a, b, front=late.rows, tail=tail)
     big, small = (a, b) if late._batched_size(a) >= late._batched_size(b) else (b, a)
-    fused = _contract_sliced(big, small, late)
+    fused = _contract_sliced(big, small, late, tail)
     if fused is not None:
         return fused
     big, small = late.batch(big), late.batch(small)
-    return contract(big, small)
+    return contract(big, small, tail=tail)
 
 
 _ZEROS: dict = {}
@@ -737,7 +816,7 @@ def _zero_offsets(n: int, device):
     return z
 
 
-def _contract_open(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
+def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Tensor]:
     """Both operands with open outputs, no batch axis yet: the smaller
     operand's open outputs become the GEMM batch (its slices side by side,
     the big operand broadcast through all-zero entry offsets and read
@@ -757,6 +836,7 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     a_free = [l for l in big.labels if l not in sset]
     a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
     s_free = [l for l in small.labels if l not in bset and l not in so]
+    s_free = [l for l in s_free if l not in tail] + [l for l in s_free if l in tail]
     for l in k_order:
         if big.dim_of(l) != small.dim_of(l):
             raise ValueError(f"dimension mismatch on {l!r}: {big.dim_of(l)} vs {small.dim_of(l)}")
@@ -798,7 +878,7 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     return Tensor(labels, out, dims)
 
 
-def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
+def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Tensor]:
     """One batched GEMM for a late-sliced network: `a` (the bigger operand)
     and `b` each either carry the batch axis or still have open outputs
     (b may also have neither -- broadcast).  An open operand's per-bit-string
@@ -820,6 +900,7 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     k_order = [l for l in a_core if l in bset]
     a_free = [l for l in a_core if l not in bset]
     b_free = [l for l in b_core if l not in aset]
+    b_free = [l for l in b_free if l not in tail] + [l for l in b_free if l in tail]
     if any(_is_batch(l) for l in a_free + b_free):
         return None
     for l in k_order:
@@ -851,13 +932,7 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
     else:
         if m > 2 ** 22:
             return None
-        if a_bat:
-            roff, coff, ru = _gather_tables(a.dims[1:], a.labels[1:], a_free, k_order,
-                                            a.buf.device)
-        else:
-            roff, coff, ru = _gather_tables(a.dims, a.labels, a_free, k_order, a.buf.device)
-        flags |= _lib.GATHER_ROWS_UNIT if ru else 0
-        opA, lda = _lib.OP_N, max(k, 1)
+        opA, lda, roff = _lib.OP_N, max(k, 1), "tables"
     if ao:
         a_boff = late.offsets(a, ao)
     # ---- B: batched entries, per-bit-string slices, or broadcast
@@ -879,6 +954,22 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
         B, opB, sB = b.transpose_to(tuple(k_order + b_free)), _lib.OP_N, 0
     ldb = max(n, 1) if opB == _lib.OP_N else max(k, 1)
     out = device_buffer(nb * m * n, a.buf.dtype, a.buf.device)
+    labels_out = (lb,) + tuple(a_free) + tuple(b_free)
+    dims = (nb,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
+    if roff == "tables":
+        # batched big operand with scattered summed labels: a TMA-fed strided
+        # view when it has one, else offset tables
+        view = _a_view(a.labels[1:], a.dims[1:], a_free, k_order) if a_bat else None
+        if view is not None and _gemm_view(
+                nb, m, n, k, a_buf.data_ptr() + 8 * a_off, entry_a, view, B, ldb, sB, opB, out,
+                b_boff, B.size // max(k * n, 1) if bo else 0):
+            return Tensor(labels_out, out, dims)
+        if a_bat:
+            roff, coff, ru = _gather_tables(a.dims[1:], a.labels[1:], a_free, k_order,
+                                            a.buf.device)
+        else:
+            roff, coff, ru = _gather_tables(a.dims, a.labels, a_free, k_order, a.buf.device)
+        flags |= _lib.GATHER_ROWS_UNIT if ru else 0
     tag = ("G" if roff is not None else "NT"[opA]) + ("S" if ao else "") + \
         ("V" if a._data is None else "") + "," + ("S" if bo else "B" if b_bat else "0")
     vp = ctypes.c_void_p
@@ -892,8 +983,6 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits) -> Optional[Tensor]:
             vp(B.data.data_ptr()), ldb, sB, opB, vp(b_boff.data_ptr() if b_boff is not None else 0),
             vp(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
     _lib.check(st, "gemm_ex")
-    labels_out = (lb,) + tuple(a_free) + tuple(b_free)
-    dims = (nb,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
     return Tensor(labels_out, out, dims)
 
 # ---------------------------------------------------------------------------
