@@ -193,6 +193,24 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
                       int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                       float beta_im, void *stream);
 
+/*
+ * GPU state-vector simulator (complex128), the verification twin of the
+ * reference's dense simulator (rq/oracle.py:51-74, kernels
+ * rq/_kernels.py:162-271).  Bit p of a state index is qubit n-1-p (qubit 0 =
+ * most significant, rq/oracle.py:8-10).
+ * qf_sv_basis:  state = |index>  (2^n complex128 entries)
+ * qf_sv_apply:  one pass over the state: tiles of the k <= 10 ascending bit
+ *   positions `bits` (HOST), applying nops <= 24 gates in order; gate o is
+ *   kind[o] (0 = one-qubit, 1 = CZ, 2 = iSWAP) on tile-local bit positions
+ *   op_bits[2o], op_bits[2o+1]; one-qubit matrices in mats[8o..8o+7] as
+ *   (re, im) of m00, m01, m10, m11 (all HOST arrays).
+ * qf_sv_gather: out[i] = state[idx[i]]  (idx: DEVICE int64)
+ */
+int qf_sv_basis(void *state, int n, int64_t index, void *stream);
+int qf_sv_apply(void *state, int n, int k, const int32_t *bits, int nops, const int32_t *kind,
+                const int32_t *op_bits, const double *mats, void *stream);
+int qf_sv_gather(const void *state, const int64_t *idx, int64_t count, void *out, void *stream);
+
 /* complex128 twin (FFMA/DFMA only), for dtype=complex128 engines. */
 int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
                   const void *A, int64_t lda, int64_t strideA, int opA,

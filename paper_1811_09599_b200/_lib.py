@@ -34,7 +34,7 @@ EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_info", "qf_permute", "qf_permute_c64",
     "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_cgemm_c64_gather", "qf_zgemm_c128",
     "qf_bit_offsets", "qf_gather_rows", "qf_cgemm_c64_gather_boff", "qf_cgemm_c64_ex",
-    "qf_cgemm_c64_view",
+    "qf_cgemm_c64_view", "qf_sv_basis", "qf_sv_apply", "qf_sv_gather",
     "qf_accumulate",
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
     "qf_small_engine",
@@ -103,6 +103,11 @@ def _declare(lib):
                                       _c_void_p, _i64, _i64,
                                       ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                       ctypes.c_float, _c_void_p]
+    lib.qf_sv_basis.argtypes = [_c_void_p, ctypes.c_int, _i64, _c_void_p]
+    lib.qf_sv_apply.argtypes = [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32),
+                                ctypes.c_int, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                ctypes.POINTER(ctypes.c_double), _c_void_p]
+    lib.qf_sv_gather.argtypes = [_c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]
     lib.qf_bit_offsets.argtypes = [_c_void_p, _i64, ctypes.c_int, ctypes.POINTER(_i32),
                                    ctypes.POINTER(_i64), _i64, _c_void_p, _c_void_p]
     lib.qf_gather_rows.argtypes = [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64,

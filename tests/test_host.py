@@ -266,3 +266,20 @@ def test_batch_order_follows_plan_site_order():
                 seq.append(int(x[1:]))
     keys = [tuple(row[q] for q in seq) for row in bits[order]]
     assert keys == sorted(keys)
+
+
+def test_statevector_pass_plan_covers_each_gate_once():
+    from paper_1811_09599_b200 import statevector as sv
+    lat = qf.Lattice.rectangle(5, 5)
+    circ = qf.generate_rqc(lat, "1+8+1", seed=1)
+    n = circ.n
+    for gates in circ.by_cycle():
+        passes = sv.plan_passes(gates, n)
+        seen = [g for _, gs in passes for g in gs]
+        assert sorted(map(id, seen)) == sorted(map(id, gates))
+        for bits, gs in passes:
+            assert len(bits) == min(sv.TILE_BITS, n) and bits == sorted(set(bits))
+            assert set(range(sv.LOW_BITS)) <= set(bits)
+            assert len(gs) <= sv.MAX_OPS
+            for g in gs:
+                assert {n - 1 - q for q in g.qubits} <= set(bits)
