@@ -21,7 +21,11 @@ from .contraction_plan import (ContractionPlan, CostEstimate, CutSpec, ContractS
                                execute_plan, format_plan, grid_plan, load_plan, parse_plan,
                                two_region_plan)
 from .network_builder import Net2D, Net3D, build_3d, contract_grid, contract_time, gate_tensor
+from .sampler import (SampleRun, SamplerConfig, SamplingErrorReport, accept_probability,
+                      circuit_batches, estimate_sampling_error, frugal_sample, required_batches,
+                      sample_circuit, write_samples)
 from .slices import SliceShard, current_shard, reduce_partials, shard_range
+from .statevector import evolve, exact_amplitude, exact_amplitudes, exact_distribution
 from .tensor_core import (PermutePlan, Tensor, benchmark_csv, benchmark_permute, contract,
                           get_gemm_mode, permute_fast, permute_naive, plan_permutation,
                           set_gemm_mode)
@@ -41,5 +45,9 @@ __all__ = [
     "AmplitudeEngine", "AmplitudeBatch", "FidelitySpec", "PathStats", "mixed_state_samples",
     "amplitude_record", "batch_records", "read_amplitudes", "write_amplitudes",
     "SliceShard", "current_shard", "reduce_partials", "shard_range",
+    "SamplerConfig", "SamplingErrorReport", "SampleRun", "accept_probability",
+    "required_batches", "frugal_sample", "estimate_sampling_error", "circuit_batches",
+    "sample_circuit", "write_samples",
+    "evolve", "exact_amplitude", "exact_amplitudes", "exact_distribution",
     "LibraryMissingError", "__version__",
 ]

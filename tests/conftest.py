@@ -43,3 +43,9 @@ def rel_l2(got, want) -> float:
 def golden_amps(case):
     import numpy as np
     return np.array([complex(re, im) for re, im in case["amps"]])
+
+
+@pytest.fixture(scope="session")
+def golden_sampler():
+    with open(os.path.join(GOLDEN, "golden_sampler.json")) as fh:
+        return json.load(fh)
