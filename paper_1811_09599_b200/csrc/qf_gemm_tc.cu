@@ -1826,6 +1826,13 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         const int32_t m0 = (int32_t)(pc.mt * BM), n0 = (int32_t)(pc.nt * BN), b = (int32_t)pc.bidx;
         const int32_t bslice =
             g.b_boff ? (int32_t)(__ldg(g.b_boff + pc.bidx) / (g.K * g.N)) : b;
+        // A view: row coordinates of this tile, k-block -> (ki, ko) counters
+        int32_t v_ra = 0, v_rb = 0, v_ki = 0, v_ko = 0;
+        const int32_t v_kbi = g.v_kin ? (int32_t)(g.v_kin / KB) : 1;
+        if (g.v_kin) {
+          v_rb = (int32_t)(m0 / (int32_t)g.v_ra);
+          v_ra = g.v_ra >= BM ? m0 - v_rb * (int32_t)g.v_ra : 0;
+        }
         for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
           const uint32_t slot = f & (RAW - 1);
           if (f >= RAW) mbar_wait(&rawfree[slot], ((f / RAW) + 1) & 1u);
@@ -1836,15 +1843,15 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           const int32_t k0 = (int32_t)(kb * KB);
           if (g.v_kin) {
             // A view: {2 ki, ra, ko, rb, b}; the box spans 128 rows of (ra, rb)
-            const uint32_t kbi = (uint32_t)(g.v_kin / KB);
-            const int32_t ki = (int32_t)(kb % kbi) * (2 * KB), ko = (int32_t)(kb / kbi);
-            const int32_t ra = g.v_ra >= BM ? (int32_t)(m0 % g.v_ra) : 0;
-            const int32_t rb = (int32_t)(m0 / g.v_ra);
             asm volatile(
                 "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
                 "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(rawa + slot * L::RAWA_SLOT),
-                "l"(&tmA), "r"(ki), "r"(ra), "r"(ko), "r"(rb), "r"(b), "r"(bar)
+                "l"(&tmA), "r"(v_ki * 2 * KB), "r"(v_ra), "r"(v_ko), "r"(v_rb), "r"(b), "r"(bar)
                 : "memory");
+            if (++v_ki == v_kbi) {
+              v_ki = 0;
+              ++v_ko;
+            }
           } else {
             // A: opA N -> coords {2k, m, b}; opA T -> {2m, k, b}
             const int32_t a0 = g.opA == QF_OP_N ? 2 * k0 : 2 * m0, a1 = g.opA == QF_OP_N ? m0 : k0;
@@ -3413,6 +3420,17 @@ static int g_tc3_variant = 0;
 
 bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
 
+// TMA-fed short-K runs: RAW k-blocks of A (8 KiB each) in flight per CTA.
+// Plain operands stream best 8 deep (1024 x 4096x64x64: 0.75 vs 0.85 ms,
+// 0.89 of HBM); strided views, whose k-blocks sit far apart, 4 deep (0.84 vs
+// 0.92 ms; scripts/view_bench2.py).  Variants 21/22 pin 4/8 for A/B runs.
+static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
+  if (g_tc3_variant == 21) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
+  if (g_tc3_variant == 22) return tc::launch_short<8, 8, 8, 4, 64, 0, 1, true>(g, s);
+  if (g.v_kin) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
+  return tc::launch_short<8, 8, 8, 4, 64, 0, 1, true>(g, s);
+}
+
 // short-K kernel flavour: output-bound shapes (K <= 56) keep the epilogue on
 // the converter warps (more store parallelism); longer K hands it to 4
 // dedicated epilogue warps so conversion, MMA and stores overlap.
@@ -3424,7 +3442,7 @@ static int launch_short_auto(const GemmArgs &g, cudaStream_t s) {
   // TMA-fed runs (one producer warp) when the operands are plain strided
   // views and K >= 32 (1024 x 4096 x {16,32,64} x {32,64}: 0.57-0.68 ms vs
   // 0.74-0.96 ms for the converter-fetch kernels, scripts/smallk_bench.py)
-  if (g.K >= 32 && g.K <= 128 && tc::tma_ok(g)) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
+  if (g.K >= 32 && g.K <= 128 && tc::tma_ok(g)) return launch_short_tma(g, s);
   if (g.N <= 8) return tc::launch_short<8, 8, 16, 4, 8>(g, s);
   if (g.N <= 16) return tc::launch_short<8, 8, 16, 4, 16>(g, s);
   if (g.N <= 32) return tc::launch_short<8, 8, 16, 4, 32>(g, s);
@@ -3461,7 +3479,7 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
                 (long long)g.N);
       return QF_ERR_UNSUPPORTED;
     }
-    return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
+    return launch_short_tma(g, s);
   }
   const bool small_n = g.N <= 64;
   if (g.a_roff) {  // gathered A: only the warp-specialised kernel fetches through tables

@@ -21,6 +21,13 @@ B = torch.randn(nb * K * N, dtype=torch.complex64, device="cuda")
 C = torch.empty(nb * M * N, dtype=torch.complex64, device="cuda")
 lib = _lib.load()
 def rep(name, ms): print(f"{name:40s} {ms:.3f} ms {byts / ms / 1e6:.0f} GB/s", flush=True)
+for var in (21, 22):
+    lib.qf_tc3_set_variant(var)
+    rep(f"plain NN variant {var}", timeit(lambda: tc.gemm_buffer(nb, M, N, K, A, 0, B, 0, C)))
+    ta = tc.Tensor(("@b", "p", "s", "q", "r", "x", "t"), A, (nb, 8, 8, 8, 8, 8, 8))
+    tb = tc.Tensor(("@b", "s", "t", "v", "w"), B, (nb, 8, 8, 8, 8))
+    rep(f"view variant {var}", timeit(lambda: tc.contract(ta, tb)))
+lib.qf_tc3_set_variant(0)
 rep("plain NN (auto)", timeit(lambda: tc.gemm_buffer(nb, M, N, K, A, 0, B, 0, C)))
 # view: A entry [p(8) s(8) q(8) r(8) t(8) x(8)] as rows (p, q, r, x?) ... labels
 dims = (8, 8, 8, 8, 8, 8)
