@@ -52,6 +52,10 @@ extern "C" {
 #define QF_BOFF_EVEN 0x200
 /* same for b_boff in qf_cgemm_c64_ex */
 #define QF_BBOFF_EVEN 0x400
+/* qf_cgemm_c64_ex: store C transposed per entry, C(b, m, n) at
+ * C + b*strideC + n*ldc + m (ldc >= M; N <= 16 CUDA-core engines only,
+ * QF_ERR_UNSUPPORTED otherwise) */
+#define QF_C_TRANS 0x800
 
 /* operand layouts */
 #define QF_OP_N 0        /* A stored [M][K] (lda >= K); B stored [K][N] (ldb >= N) */

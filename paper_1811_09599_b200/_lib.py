@@ -27,6 +27,7 @@ GEMM_AUTO, GEMM_FFMA, GEMM_TC3 = 0, 1, 2
 GATHER_ROWS_UNIT = 0x100  # or'ed into qf_cgemm_c64_gather's mode: roff[r] = roff[0] + r
 BOFF_EVEN = 0x200         # or'ed into qf_cgemm_c64_gather_boff's mode: entry bases even
 BBOFF_EVEN = 0x400        # or'ed into qf_cgemm_c64_ex's mode: B entry bases even
+C_TRANS = 0x800           # or'ed into qf_cgemm_c64_ex's mode: C stored transposed per entry
 OP_N, OP_T = 0, 1
 
 # every exported symbol declared in include/qflex_b200.h

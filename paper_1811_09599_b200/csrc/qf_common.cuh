@@ -59,6 +59,9 @@ struct GemmArgs {
   // unused): k = ko*v_kin + ki with ki innermost and contiguous, row
   // r = rb*v_ra + ra; v_s* are element strides of ra, ko and rb
   int64_t v_kin = 0, v_ra = 0, v_sra = 0, v_kout = 0, v_skout = 0, v_rb = 0, v_srb = 0;
+  // C stored transposed per entry: C(b, m, n) at C + b*sC + n*ldc + m (row-block
+  // and row-stream engines only)
+  bool c_trans = false;
 };
 
 __device__ __forceinline__ int64_t b_batch_off(const GemmArgs &g, int64_t b) {

@@ -626,7 +626,10 @@ __global__ void __launch_bounds__(RB_THREADS)
           }
         }
       }
-      V *cp = C + row * g.ldc + n0;
+      // row-major C: this row's columns; transposed C: column c, row `row`
+      // (consecutive threads write consecutive rows)
+      V *cp = g.c_trans ? C + (int64_t)n0 * g.ldc + row : C + row * g.ldc + n0;
+      const int64_t cstep = g.c_trans ? g.ldc : 1;
 #pragma unroll
       for (int c = 0; c < RB_NG; ++c) {
         if (n0 + c < N) {
@@ -634,11 +637,11 @@ __global__ void __launch_bounds__(RB_THREADS)
           o.x = ar * acc[c].x - ai * acc[c].y;
           o.y = ar * acc[c].y + ai * acc[c].x;
           if (use_beta) {
-            const V cv = cp[c];
+            const V cv = cp[c * cstep];
             o.x += br * cv.x - bi * cv.y;
             o.y += br * cv.y + bi * cv.x;
           }
-          cp[c] = o;
+          cp[c * cstep] = o;
         }
       }
     }
@@ -867,7 +870,23 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     // ---- epilogue
     float2 *C = reinterpret_cast<float2 *>(g.C) + b * g.sC;
     const int rows = (int)max((int64_t)0, min((int64_t)32, g.M - r0));
-    if (!use_beta && N == NN && g.ldc % 2 == 0 &&
+    if (g.c_trans) {  // transposed C: lane = row, one coalesced 256-byte run per column
+      if (lane < rows) {
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          if (n < N) {
+            float2 *cp = C + (int64_t)n * g.ldc + r0 + lane;
+            float2 o = make_float2(ar * acc[n].x - ai * acc[n].y, ar * acc[n].y + ai * acc[n].x);
+            if (use_beta) {
+              const float2 c = *cp;
+              o.x += br_ * c.x - bi_ * c.y;
+              o.y += br_ * c.y + bi_ * c.x;
+            }
+            *cp = o;
+          }
+        }
+      }
+    } else if (!use_beta && N == NN && g.ldc % 2 == 0 &&
         ((reinterpret_cast<uintptr_t>(C + r0 * g.ldc)) & 15) == 0) {
 #pragma unroll
       for (int n = 0; n < NN; n += 2) {
@@ -1162,6 +1181,14 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
                                                                            ws);
     return check_launch("cgemm_skinny_reduce");
   }
+  if (g.c_trans) {  // only the row-block / row-stream epilogues store C transposed
+    QF_REQUIRE(g.K >= 1 && g.N <= 16 && g.K * g.N <= SKN_MAX, "gemm: transposed C needs N <= 16");
+    if constexpr (sizeof(R) == 4) {
+      if (rowstream_eligible(g) && !(g.a_roff ? g.rows_unit : g.opA == QF_OP_T))
+        return gemm_rowstream(g, s);
+    }
+    return gemm_rowblock<R>(g, s);
+  }
   if (gemv_eligible(g)) return gemm_gemv<R>(g, s);
   if (smallkn_eligible(g)) {
     // narrow outputs stream best row by row; wide outputs keep the
@@ -1269,7 +1296,8 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
   QF_REQUIRE((a_roff != nullptr) == (a_coff != nullptr), "gemm_ex: a_roff/a_coff must pair");
   const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
   const bool a_even = (mode & QF_BOFF_EVEN) != 0, b_even = (mode & QF_BBOFF_EVEN) != 0;
-  mode &= ~(QF_GATHER_ROWS_UNIT | QF_BOFF_EVEN | QF_BBOFF_EVEN);
+  const bool c_trans = (mode & QF_C_TRANS) != 0;
+  mode &= ~(QF_GATHER_ROWS_UNIT | QF_BOFF_EVEN | QF_BBOFF_EVEN | QF_C_TRANS);
   // with entry-offset tables the batch strides only key the 16-byte paths
   if (a_boff) strideA = a_even ? 2 : 1;
   if (b_boff) strideB = b_even ? 2 : 1;
@@ -1280,6 +1308,19 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
   qf::GemmArgs g{batch, M, N, K, A, lda, strideA, opA, B, ldb, strideB, opB, C, ldc, strideC,
                  alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
                  rows_unit && a_roff != nullptr, a_boff, b_boff};
+  g.c_trans = c_trans;
+  if (c_trans) {
+    QF_REQUIRE(ldc >= std::max<int64_t>(1, M), "gemm_ex: transposed C needs ldc >= M");
+    if (!(N <= 16 && K >= 1 && K * N <= 4096)) {
+      qf::set_error("gemm_ex: transposed C needs N <= 16 and K*N <= 4096");
+      return QF_ERR_UNSUPPORTED;
+    }
+    g.ldc = std::max<int64_t>(N, 1);  // validate() checks row-major ldc; restored below
+    int st = qf::validate(g);
+    if (st != QF_OK) return st;
+    g.ldc = ldc;
+    return qf::gemm_simt<float>(g, qf::as_stream(stream));
+  }
   int st = qf::validate(g);
   if (st != QF_OK) return st;
   cudaStream_t s = qf::as_stream(stream);

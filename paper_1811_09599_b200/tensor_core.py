@@ -783,7 +783,7 @@ class LateBits:
 _i32 = ctypes.c_int32
 
 
-def contract_late(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Tensor:
+def contract_late(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> Tensor:
     """`contract` for networks whose outputs are sliced late (LateBits).
 
     Both operands without a batch axis and few open outputs between them:
@@ -798,7 +798,7 @@ def contract_late(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Tensor:
         r = _contract_open(a, b, late, tail)
         return r if r is not None else contract(a, b, front=late.rows, tail=tail)
     big, small = (a, b) if late._batched_size(a) >= late._batched_size(b) else (b, a)
-    fused = _contract_sliced(big, small, late, tail)
+    fused = _contract_sliced(big, small, late, tail, lead)
     if fused is not None:
         return fused
     big, small = late.batch(big), late.batch(small)
@@ -878,14 +878,17 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Te
     return Tensor(labels, out, dims)
 
 
-def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Tensor]:
+def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> Optional[Tensor]:
     """One batched GEMM for a late-sliced network: `a` (the bigger operand)
     and `b` each either carry the batch axis or still have open outputs
     (b may also have neither -- broadcast).  An open operand's per-bit-string
     slice is an entry base offset (qf_cgemm_c64_ex a_boff / b_boff), so
     nothing is materialised: the big one is read in place (plain, through
     gathered tables, or as a cut-slice view), the small one is a site tensor
-    with its outputs moved in front (memoised layout).  None if not eligible."""
+    with its outputs moved in front (memoised layout).  `lead`: kept-open cut
+    labels; when they are all of b's free labels the result is stored
+    transposed per entry ([@b, cut, rows]) so that per-path cut slices are
+    contiguous (CUDA-core engines, N <= 16).  None if not eligible."""
     lb = late.label
     if a.buf.dtype != torch.complex64 or not _gather_enabled or a.size >= 2 ** 31:
         return None
@@ -956,7 +959,11 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[
     out = device_buffer(nb * m * n, a.buf.dtype, a.buf.device)
     labels_out = (lb,) + tuple(a_free) + tuple(b_free)
     dims = (nb,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
-    if roff == "tables":
+    c_trans = bool(lead) and bool(b_free) and set(b_free) <= set(lead) and n <= 16
+    if c_trans:
+        labels_out = (lb,) + tuple(b_free) + tuple(a_free)
+        dims = (nb,) + tuple(b.dim_of(l) for l in b_free) + tuple(a.dim_of(l) for l in a_free)
+    if roff == "tables" and not c_trans:
         # batched big operand with scattered summed labels: a TMA-fed strided
         # view when it has one, else offset tables
         view = _a_view(a.labels[1:], a.dims[1:], a_free, k_order) if a_bat else None
@@ -964,6 +971,7 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[
                 nb, m, n, k, a_buf.data_ptr() + 8 * a_off, entry_a, view, B, ldb, sB, opB, out,
                 b_boff, B.size // max(k * n, 1) if bo else 0):
             return Tensor(labels_out, out, dims)
+    if roff == "tables":
         if a_bat:
             roff, coff, ru = _gather_tables(a.dims[1:], a.labels[1:], a_free, k_order,
                                             a.buf.device)
@@ -973,15 +981,26 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[
     tag = ("G" if roff is not None else "NT"[opA]) + ("S" if ao else "") + \
         ("V" if a._data is None else "") + "," + ("S" if bo else "B" if b_bat else "0")
     vp = ctypes.c_void_p
-    with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
-                f"b{nb} m{m} n{n} k{k} {tag}" if _timer else ""):
-        st = lib.qf_cgemm_c64_ex(
-            _gemm_mode | flags, nb, m, n, k, vp(a_buf.data_ptr() + 8 * a_off), lda, entry_a, opA,
-            vp(a_boff.data_ptr() if a_boff is not None else 0),
-            vp(roff.data_ptr() if roff is not None else 0),
-            vp(coff.data_ptr() if coff is not None else 0),
-            vp(B.data.data_ptr()), ldb, sB, opB, vp(b_boff.data_ptr() if b_boff is not None else 0),
-            vp(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+
+    def launch(trans: bool):
+        with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
+                    f"b{nb} m{m} n{n} k{k} {tag}{'^T' if trans else ''}" if _timer else ""):
+            return lib.qf_cgemm_c64_ex(
+                _gemm_mode | flags | (_lib.C_TRANS if trans else 0), nb, m, n, k,
+                vp(a_buf.data_ptr() + 8 * a_off), lda, entry_a, opA,
+                vp(a_boff.data_ptr() if a_boff is not None else 0),
+                vp(roff.data_ptr() if roff is not None else 0),
+                vp(coff.data_ptr() if coff is not None else 0),
+                vp(B.data.data_ptr()), ldb, sB, opB,
+                vp(b_boff.data_ptr() if b_boff is not None else 0),
+                vp(out.data_ptr()), max(m if trans else n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
+                stream_handle())
+
+    st = launch(c_trans)
+    if c_trans and st == _lib.QF_ERR_UNSUPPORTED:    # row-major result after all
+        labels_out = (lb,) + tuple(a_free) + tuple(b_free)
+        dims = (nb,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
+        st = launch(False)
     _lib.check(st, "gemm_ex")
     return Tensor(labels_out, out, dims)
 

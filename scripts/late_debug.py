@@ -10,9 +10,9 @@ eng = qf.AmplitudeEngine(circ, qf.grid_plan(lat, n_cuts=1))
 rng = np.random.Generator(np.random.PCG64(0))
 outs = [format(int(v), "025b") for v in rng.integers(0, 2 ** 25, size=1024)]
 orig = tc.contract_late
-def spy(a, b, late):
+def spy(a, b, late, tail=()):
     print("A", list(zip(a.labels, a.dims)), "\n B", list(zip(b.labels, b.dims)), flush=True)
-    r = orig(a, b, late)
+    r = orig(a, b, late, tail)
     print(" ->", list(zip(r.labels, r.dims)), flush=True)
     return r
 tc.contract_late = spy

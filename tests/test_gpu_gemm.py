@@ -448,3 +448,23 @@ def test_tma_view_with_sliced_site(nb):
     want = tc.contract(ta, late.batch(ts))
     w = want.transpose_to(got.labels).array
     assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+
+
+@pytest.mark.parametrize("nb", [4, 128])
+@pytest.mark.parametrize("perm", [0, 1])
+def test_transposed_store_for_kept_cut(nb, perm):
+    """Slice-late: a kept cut that is the small operand's only free index is
+    stored in front of the rows (qf_cgemm_c64_ex with QF_C_TRANS, row-block /
+    row-stream epilogues) -- same values as the row-major result."""
+    rng = np.random.default_rng(900 + nb + perm)
+    a_labels = ["@b", "p", "q", "s", "t"] if perm == 0 else ["@b", "s", "p", "t", "q"]
+    A = _rand(rng, (nb, 8, 8, 8, 8), np.complex64)
+    S = _rand(rng, (8, 8, 8, 2), np.complex64)                     # s t c out0
+    bits = rng.integers(0, 2, size=(1, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"out0": 0})
+    ta, ts = tc.Tensor(a_labels, A), tc.Tensor(["s", "t", "c", "out0"], S)
+    got = tc.contract_late(ta, ts, late, lead=("c",))
+    assert got.labels[:2] == ("@b", "c")
+    want = tc.contract(ta, late.batch(ts))
+    w = want.transpose_to(got.labels).array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
