@@ -209,6 +209,25 @@ class ClockSampler:
 # the GPU arm
 
 
+def measured_traffic(workload: str, kernel: str, algorithmic_per_launch: float):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    ncu capture of one step (profiles/traffic_<workload>.json, made by
+    scripts/ncu_summary.py traffic), with the algorithmic bytes beside it;
+    None when no capture of this workload/kernel is committed."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        rec = json.load(fh).get("kernels", {}).get(kernel)
+    if rec is None:
+        return None
+    return {"dram_bytes_per_launch": rec["dram_bytes_per_launch"],
+            "algorithmic_bytes_per_launch": round(algorithmic_per_launch),
+            "ratio": round(rec["dram_bytes_per_launch"] / max(algorithmic_per_launch, 1), 3),
+            "source": f"profiles/traffic_{workload}.json (ncu dram__bytes_read.sum + "
+                      f"dram__bytes_write.sum, {rec['launches']} launches of one step)"}
+
+
 def peaks() -> dict:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -360,11 +379,13 @@ def run_gpu(args):
             roof = {"bound": "hbm", "unit": "GB/s", "kernel": dom,
                     "peak_basis": f"hbm_gbs {pk['source']}"}
         roof.update({"achieved": round(achieved, 2), "peak": round(peak, 1),
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4),
+                     "traffic_detail": measured_traffic("config2", dom, d["bytes"] / d["launches"]),
                      "arithmetic_intensity": round(ai, 2), "ridge": round(ridge, 2),
                      "algorithmic": (f"{dom}: 8*m*k*n flops and 8*(m*k + k*n + m*n)*batch bytes "
                                      f"per launch (16 B/element for permutes), summed over "
                                      f"{d['launches']} launches of one step, / their CUDA-event time")})
+        roof["traffic"] = (roof["traffic_detail"] or {}).get("dram_bytes_per_launch")
         clk = clocks.summary()
         cpu = None
         if not args.no_cpu_baseline:

@@ -53,6 +53,39 @@ def full(path):
     return "\n".join(out)
 
 
+def family(kernel_name):
+    """'void tc::cgemm_tc3k_kernel<8, 4>(GemmArgs, ...)' -> 'cgemm_tc3k' (the
+    names bench.py's per-kernel table uses)."""
+    name = kernel_name.split("(")[0].split("<")[0].replace("void ", "").strip()
+    name = name.split("::")[-1]
+    return name[:-len("_kernel")] if name.endswith("_kernel") else name
+
+
+def traffic(path):
+    """Per kernel family of a `--metrics gpu__time_duration.sum,dram__bytes_read.sum,
+    dram__bytes_write.sum --csv` capture: launches, DRAM bytes, time (JSON)."""
+    import json
+    rows = [l for l in open(path) if l.startswith('"')]
+    agg = defaultdict(lambda: {"ids": set(), "dram_read": 0.0, "dram_write": 0.0, "ns": 0.0})
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3,
+             "usecond": 1e3, "nsecond": 1, "ms": 1e6, "msecond": 1e6}
+    for r in csv.DictReader(io.StringIO("".join(rows))):
+        a = agg[family(r["Kernel Name"])]
+        a["ids"].add(r["ID"])
+        v = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1)
+        key = {"dram__bytes_read.sum": "dram_read", "dram__bytes_write.sum": "dram_write",
+               "gpu__time_duration.sum": "ns"}.get(r["Metric Name"])
+        if key:
+            a[key] += v
+    out = {}
+    for k, a in sorted(agg.items(), key=lambda x: -x[1]["ns"]):
+        n = len(a["ids"])
+        out[k] = {"launches": n, "dram_bytes_per_launch": round((a["dram_read"] + a["dram_write"]) / n),
+                  "dram_read": round(a["dram_read"]), "dram_write": round(a["dram_write"]),
+                  "us": round(a["ns"] / 1e3, 1)}
+    return json.dumps(out, indent=1)
+
+
 if __name__ == "__main__":
     kind, path = sys.argv[1], sys.argv[2]
-    print(launches(path) if kind == "launches" else full(path))
+    print({"launches": launches, "full": full, "traffic": traffic}[kind](path))
