@@ -29,9 +29,10 @@ import numpy as np
 
 from . import slices
 from .circuits import Circuit
-from .contraction_plan import ContractionPlan, PlanExecutor, builtin_plan, enumerate_paths
+from .contraction_plan import (ContractionPlan, GroupUnsupported, PlanExecutor, builtin_plan,
+                               enumerate_paths)
 from .network_builder import Net2D, build_3d, contract_time, out_label
-from .tensor_core import accumulate_buffer, device_buffer, torch, zero_buffer
+from .tensor_core import accumulate_buffer, device_buffer, sum_path_axis, torch, zero_buffer
 
 
 @dataclass(frozen=True)
@@ -123,6 +124,37 @@ def _finisher(net: Net2D):
     return lambda t: late.batch(t).data if late.outs(t) else t.data
 
 
+_path_batching = True
+PATH_GROUPS_RUN = [0]   # path groups walked as one batched pass (tests read it)
+
+
+def set_path_batching(enabled: bool) -> bool:
+    """Walk a full group of the last cut's values as one batched pass
+    (PlanExecutor.group_cut) instead of path by path; returns the previous
+    setting.  Same products and sums either way."""
+    global _path_batching
+    prev, _path_batching = _path_batching, bool(enabled)
+    return prev
+
+
+def _path_groups(paths, gi: Optional[int]):
+    """Consecutive runs of `paths` that differ only in cut `gi`."""
+    if gi is None:
+        for p in paths:
+            yield [p]
+        return
+    grp, key = [], None
+    for p in paths:
+        k = tuple(p[:gi]) + tuple(p[gi + 1:])
+        if grp and k != key:
+            yield grp
+            grp = []
+        grp.append(p)
+        key = k
+    if grp:
+        yield grp
+
+
 def _completions(n_open: int, n_c: int, seed: int) -> np.ndarray:
     """The n_c completions of the open region (rq/amplitude_engine.py:159-164)."""
     if n_c == 2 ** n_open:
@@ -179,8 +211,20 @@ class AmplitudeEngine:
         acc = device_buffer(size, torch.complex64 if self.dtype == np.complex64
                             else torch.complex128)
         zero_buffer(acc)
-        for p in shard.take(paths):
-            accumulate_buffer(finish(ex.run(p)), acc, size)
+        gi = ex.group_cut() if _path_batching else None
+        for grp in _path_groups(shard.take(paths), gi):
+            if gi is not None and [p[gi] for p in grp] == list(range(ex.cut_dims[gi])):
+                try:
+                    t, rep = ex.run_group(grp)
+                except GroupUnsupported:
+                    gi = None
+                else:
+                    PATH_GROUPS_RUN[0] += 1
+                    t = sum_path_axis(t, rep, keep_batch=t.dims[0] // rep > 1)
+                    accumulate_buffer(finish(t), acc, size)
+                    continue
+            for p in grp:
+                accumulate_buffer(finish(ex.run(p)), acc, size)
         return acc
 
     def _sum_paths(self, ex: PlanExecutor, paths, finish, size: int):

@@ -582,8 +582,8 @@ __global__ void __launch_bounds__(RB_THREADS)
       for (int j = 0; j < RB_NG; ++j) acc[j] = V{R(0), R(0)};
       const V *arow = g.a_roff ? A + g.a_roff[row]
                                : (g.opA == QF_OP_N ? A + row * g.lda : A + row);
-      for (int k0 = 0; k0 < K; k0 += 8) {
-        V a[8];
+      // software pipeline: the next 8 k of A are in flight while this 8 is used
+      auto load8 = [&](int k0, V *a) {
         if (vec_a && k0 + 8 <= K) {  // row-major A: four 16-byte loads per 8 k
 #pragma unroll
           for (int j = 0; j < 8; j += 2) {
@@ -601,6 +601,14 @@ __global__ void __launch_bounds__(RB_THREADS)
                               : (g.opA == QF_OP_N ? __ldg(arow + k) : __ldg(arow + (int64_t)k * g.lda));
           }
         }
+      };
+      V a_nx[8];
+      load8(0, a_nx);
+      for (int k0 = 0; k0 < K; k0 += 8) {
+        V a[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = a_nx[j];
+        if (k0 + 8 < K) load8(k0 + 8, a_nx);
         if (vec_b && n0 + RB_NG <= N) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -736,25 +744,23 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   const int mode = gat ? (rows_contig ? 0 : 2)
                        : (g.opA == QF_OP_T ? 0 : ((g.lda % 2 == 0 && g.sA % 2 == 0) ? 1 : 2));
 
-  // ---- fetch cursor over (step, chunk)
+  // ---- fetch cursor over (step, chunk); (batch, row) advance incrementally
+  // (no 64-bit division per chunk)
   int64_t f_st = st0;
   int f_ch = 0;
+  int64_t f_b = st0 / steps_per_b;
+  int64_t f_r0 = (st0 - f_b * steps_per_b) * (RS_WARPS * 32) + warp * 32;
+  const int64_t r_end = steps_per_b * (RS_WARPS * 32);
+  const float2 *f_A = Ab + a_batch_off(g, f_b);
   int32_t f_roff = 0;  // gathered: row offset of row `lane` of this warp's 32
-  auto f_base = [&](int64_t st, int64_t &b, int64_t &r0) {
-    b = st / steps_per_b;
-    r0 = (st - b * steps_per_b) * (RS_WARPS * 32) + warp * 32;
-  };
   auto load_roff = [&]() {
     if (!gat || f_st >= st1) return;
-    int64_t b, r0;
-    f_base(f_st, b, r0);
-    f_roff = __ldg(g.a_roff + min(r0 + lane, g.M - 1));
+    f_roff = __ldg(g.a_roff + min(f_r0 + lane, g.M - 1));
   };
   auto fetch = [&](int slot) {
     if (f_st < st1) {
-      int64_t b, r0;
-      f_base(f_st, b, r0);
-      const float2 *A = Ab + a_batch_off(g, b);
+      const int64_t r0 = f_r0;
+      const float2 *A = f_A;
       const int k0 = f_ch * KC;
       const uint32_t dst0 = abuf_u32 + slot * L::ABUF;
       if (mode == 0) {
@@ -805,6 +811,12 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       if (++f_ch == nch) {
         f_ch = 0;
         ++f_st;
+        f_r0 += RS_WARPS * 32;
+        if (f_r0 >= r_end) {
+          f_r0 -= r_end;
+          ++f_b;
+          if (f_st < st1) f_A = Ab + a_batch_off(g, f_b);
+        }
         load_roff();
       }
     }
@@ -817,9 +829,14 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   fetch(0);
   int64_t cur_b = -1;
   int q = 0;
+  int64_t b = st0 / steps_per_b;
+  int64_t r0 = (st0 - b * steps_per_b) * (RS_WARPS * 32) + warp * 32 - RS_WARPS * 32;
   for (int64_t st = st0; st < st1; ++st) {
-    int64_t b, r0;
-    f_base(st, b, r0);
+    r0 += RS_WARPS * 32;
+    if (r0 >= r_end) {
+      r0 -= r_end;
+      ++b;
+    }
     if (b != cur_b) {  // CTA-uniform: every warp walks the same steps
       __syncthreads();
       const float2 *B = reinterpret_cast<const float2 *>(g.B) + b_batch_off(g, b);
@@ -1184,7 +1201,8 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
   if (g.c_trans) {  // only the row-block / row-stream epilogues store C transposed
     QF_REQUIRE(g.K >= 1 && g.N <= 16 && g.K * g.N <= SKN_MAX, "gemm: transposed C needs N <= 16");
     if constexpr (sizeof(R) == 4) {
-      if (rowstream_eligible(g) && !(g.a_roff ? g.rows_unit : g.opA == QF_OP_T))
+      if (rowstream_eligible(g) &&
+          (g_small_engine == 3 || (g_small_engine != 2 && !(g.a_roff ? g.rows_unit : g.opA == QF_OP_T))))
         return gemm_rowstream(g, s);
     }
     return gemm_rowblock<R>(g, s);

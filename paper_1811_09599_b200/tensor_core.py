@@ -878,7 +878,30 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Te
     return Tensor(labels, out, dims)
 
 
-def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> Optional[Tensor]:
+PATH_LABEL = "@p"
+_ARANGE: dict = {}
+
+
+def _path_offsets(off, rep: int, stride: int):
+    """Per-(bit-string, path value) entry bases: off[b] + j*stride, j fastest."""
+    key = (rep, str(off.device))
+    ar = _ARANGE.get(key)
+    if ar is None:
+        ar = _ARANGE[key] = torch.arange(rep, dtype=torch.int64, device=off.device)
+    return (off[:, None] + ar[None, :] * stride).reshape(-1)
+
+
+def contract_late_paths(a: Tensor, b: Tensor, late: LateBits, rep: int, tail=()) -> Optional[Tensor]:
+    """contract_late inside a path-batched walk: batched operands carry
+    nb*rep entries (bit-string major, path value fastest); an operand whose
+    outputs are still open may carry the path value as a leading PATH_LABEL
+    axis, and its per-(bit-string, value) slice is an entry base offset."""
+    big, small = (a, b) if late._batched_size(a) >= late._batched_size(b) else (b, a)
+    return _contract_sliced(big, small, late, tail, (), rep=rep)
+
+
+def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=(),
+                     rep: int = 1) -> Optional[Tensor]:
     """One batched GEMM for a late-sliced network: `a` (the bigger operand)
     and `b` each either carry the batch axis or still have open outputs
     (b may also have neither -- broadcast).  An open operand's per-bit-string
@@ -892,13 +915,18 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> 
     lb = late.label
     if a.buf.dtype != torch.complex64 or not _gather_enabled or a.size >= 2 ** 31:
         return None
-    nb = late.nb
+    nb = late.nb * rep
     ao, bo = late.outs(a), late.outs(b)
     a_bat, b_bat = lb in a.labels, lb in b.labels
     if (a_bat and (ao or a.labels[0] != lb)) or (b_bat and bo) or (not a_bat and not ao):
         return None
-    a_core = [l for l in a.labels if l != lb and l not in ao]
-    b_core = [l for l in b.labels if l != lb and l not in bo]
+    a_p, b_p = PATH_LABEL in a.labels, PATH_LABEL in b.labels
+    if rep == 1 and (a_p or b_p):
+        return None
+    if (a_p and (not ao or a.labels[0] != PATH_LABEL)) or (b_p and (not bo or b.labels[0] != PATH_LABEL)):
+        return None
+    a_core = [l for l in a.labels if l != lb and l not in ao and l != PATH_LABEL]
+    b_core = [l for l in b.labels if l != lb and l not in bo and l != PATH_LABEL]
     bset, aset = set(b_core), set(a_core)
     k_order = [l for l in a_core if l in bset]
     a_free = [l for l in a_core if l not in bset]
@@ -925,12 +953,14 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> 
         a_buf, a_off, entry_a = a.data, 0, 0
     if ao:
         st_a = _strides(a)
-        if all(st_a[l] % 2 == 0 for l in ao):
+        if all(st_a[l] % 2 == 0 for l in ao + ([PATH_LABEL] if a_p else [])):
             flags |= _lib.BOFF_EVEN
-    core_labels = a.labels[1:] if a_bat else tuple(l for l in a.labels if l not in ao)
-    if list(core_labels) == a_free + k_order and (a_bat or list(a.labels) == ao + a_core):
+    a_head = [PATH_LABEL] if a_p else []
+    core_labels = a.labels[1:] if a_bat else tuple(l for l in a.labels
+                                                   if l not in ao and l != PATH_LABEL)
+    if list(core_labels) == a_free + k_order and (a_bat or list(a.labels) == a_head + ao + a_core):
         opA, lda = _lib.OP_N, max(k, 1)
-    elif list(core_labels) == k_order + a_free and (a_bat or list(a.labels) == ao + a_core):
+    elif list(core_labels) == k_order + a_free and (a_bat or list(a.labels) == a_head + ao + a_core):
         opA, lda = _lib.OP_T, max(m, 1)
     else:
         if m > 2 ** 22:
@@ -938,13 +968,21 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> 
         opA, lda, roff = _lib.OP_N, max(k, 1), "tables"
     if ao:
         a_boff = late.offsets(a, ao)
+        if a_p:
+            a_boff = _path_offsets(a_boff, rep, _strides(a)[PATH_LABEL])
+        elif rep > 1:
+            a_boff = _path_offsets(a_boff, rep, 0)
     # ---- B: batched entries, per-bit-string slices, or broadcast
     b_boff = None
     if bo:
-        B = b.transpose_to(tuple(bo + k_order + b_free))
+        B = b.transpose_to(tuple(([PATH_LABEL] if b_p else []) + bo + k_order + b_free))
         opB, sB = _lib.OP_N, 0
         b_boff = late.offsets(B, bo)
-        if all(_strides(B)[l] % 2 == 0 for l in bo):
+        if b_p:
+            b_boff = _path_offsets(b_boff, rep, _strides(B)[PATH_LABEL])
+        elif rep > 1:
+            b_boff = _path_offsets(b_boff, rep, 0)
+        if all(_strides(B)[l] % 2 == 0 for l in bo + ([PATH_LABEL] if b_p else [])):
             flags |= _lib.BBOFF_EVEN
     elif b_bat:
         n_lay, t_lay = [lb] + k_order + b_free, [lb] + b_free + k_order
@@ -1003,6 +1041,130 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=()) -> 
         st = launch(False)
     _lib.check(st, "gemm_ex")
     return Tensor(labels_out, out, dims)
+
+# ---------------------------------------------------------------------------
+# path batching: a cut's values as one more batch dimension
+
+
+_BCAST: dict = {}
+
+
+def _bcast_offsets(n: int, rep: int, entry: int, device):
+    """int64 entry bases (e // rep) * entry, e < n: entry e of a path-batched
+    walk reads entry e // rep of an operand that has no path index."""
+    key = (n, rep, entry, str(device))
+    hit = _BCAST.get(key)
+    if hit is None:
+        hit = torch.div(torch.arange(n, dtype=torch.int64, device=device), rep,
+                        rounding_mode="floor") * entry
+        if len(_BCAST) > 64:
+            _BCAST.clear()
+        _BCAST[key] = hit
+    return hit
+
+
+def contract_bcast(x: Tensor, y: Tensor, rep: int, tail=(), label: str = "@b") -> Optional[Tensor]:
+    """Contract a path-batched operand `x` (leading `label` axis of nb*rep
+    entries, path index fastest) with `y`, which has no path index (leading
+    `label` axis of nb entries, or no batch axis at all): `y` is broadcast
+    over the paths through per-entry base offsets (qf_cgemm_c64_ex a_boff /
+    b_boff), nothing is copied.  Same products as `rep` separate
+    contractions.  None when not expressible (caller falls back)."""
+    if x.buf.dtype != torch.complex64 or y.buf.dtype != torch.complex64 or x.labels[0] != label:
+        return None
+    y_bat = bool(y.labels) and y.labels[0] == label
+    NB = x.dims[0]
+    nb = y.dims[0] if y_bat else 1
+    if NB != nb * rep or any(_is_batch(l) for l in x.labels[1:] + y.labels[int(y_bat):]):
+        return None
+    xc, yc = list(x.labels[1:]), list(y.labels[int(y_bat):])
+    xs, ys = set(xc), set(yc)
+    y_entry = y.size // nb
+    x_entry = x.size // NB
+    big_is_x = x_entry >= y_entry
+    a, b = (x, y) if big_is_x else (y, x)
+    a_core, b_core = (xc, yc) if big_is_x else (yc, xc)
+    bset, aset = (ys, xs) if big_is_x else (xs, ys)
+    k_order = [l for l in a_core if l in bset]
+    a_free = [l for l in a_core if l not in bset]
+    b_free = [l for l in b_core if l not in aset]
+    b_free = [l for l in b_free if l not in tail] + [l for l in b_free if l in tail]
+    for l in k_order:
+        if a.dim_of(l) != b.dim_of(l):
+            raise ValueError(f"dimension mismatch on {l!r}: {a.dim_of(l)} vs {b.dim_of(l)}")
+    m = math.prod(a.dim_of(l) for l in a_free)
+    k = math.prod(a.dim_of(l) for l in k_order)
+    n = math.prod(b.dim_of(l) for l in b_free)
+    a_head = [label] if (big_is_x or y_bat) else []
+    b_head = [label] if (not big_is_x or y_bat) else []
+    if list(a.labels) == a_head + a_free + k_order:
+        A, opA, lda = a, _lib.OP_N, max(k, 1)
+    elif list(a.labels) == a_head + k_order + a_free:
+        A, opA, lda = a, _lib.OP_T, max(m, 1)
+    else:
+        A, opA, lda = a.transpose_to(tuple(a_head + a_free + k_order)), _lib.OP_N, max(k, 1)
+    if list(b.labels) == b_head + k_order + b_free:
+        B, opB, ldb = b, _lib.OP_N, max(n, 1)
+    elif list(b.labels) == b_head + b_free + k_order:
+        B, opB, ldb = b, _lib.OP_T, max(k, 1)
+    else:
+        B, opB, ldb = b.transpose_to(tuple(b_head + k_order + b_free)), _lib.OP_N, max(n, 1)
+    dev = x.buf.device
+    flags = 0
+    a_boff = b_boff = None
+    if big_is_x:
+        sA, sB = m * k, k * n
+        b_boff = _bcast_offsets(NB, rep, k * n if y_bat else 0, dev)
+        if (k * n) % 2 == 0 or not y_bat:
+            flags |= _lib.BBOFF_EVEN
+    else:
+        sA, sB = m * k, k * n
+        a_boff = _bcast_offsets(NB, rep, m * k if y_bat else 0, dev)
+        if (m * k) % 2 == 0 or not y_bat:
+            flags |= _lib.BOFF_EVEN
+    out = device_buffer(NB * m * n, x.buf.dtype, dev)
+    vp = ctypes.c_void_p
+    with _timed("gemm", 8 * NB * m * n * k, 8 * (NB * m * n + (NB if big_is_x else nb) * m * k +
+                                                  (nb if big_is_x else NB) * k * n),
+                f"b{NB} m{m} n{n} k{k} P{rep}" if _timer else ""):
+        st = _lib.load().qf_cgemm_c64_ex(
+            _gemm_mode | flags, NB, m, n, k, vp(A.data.data_ptr()), lda, sA, opA,
+            vp(a_boff.data_ptr() if a_boff is not None else 0), vp(0), vp(0),
+            vp(B.data.data_ptr()), ldb, sB, opB,
+            vp(b_boff.data_ptr() if b_boff is not None else 0),
+            vp(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+    _lib.check(st, "gemm_bcast")
+    labels = (label,) + tuple(a_free) + tuple(b_free)
+    dims = (NB,) + tuple(a.dim_of(l) for l in a_free) + tuple(b.dim_of(l) for l in b_free)
+    return Tensor(labels, out, dims)
+
+
+_ONES: dict = {}
+
+
+def sum_path_axis(t: Tensor, rep: int, keep_batch: bool, label: str = "@b") -> Tensor:
+    """Sum a path-batched tensor (leading `label` axis of nb*rep entries,
+    path index fastest) over its path index: one batched GEMM with a ones
+    row, C[b] (1 x R) = 1 (1 x rep) @ t[b] (rep x R).  keep_batch=False
+    drops the (then size-1) batch axis."""
+    NB = t.dims[0]
+    nb = NB // rep
+    R = t.size // NB
+    key = (rep, str(t.buf.dtype), str(t.buf.device))
+    ones = _ONES.get(key)
+    if ones is None:
+        ones = _ONES[key] = torch.ones(rep, dtype=t.buf.dtype, device=t.buf.device)
+    out = device_buffer(nb * R, t.buf.dtype, t.buf.device)
+    lib = _lib.load()
+    with _timed("gemm", 8 * nb * R * rep, _elem_bytes(out) * (NB * R + nb * R),
+                f"b{nb} m1 n{R} k{rep} sum" if _timer else ""):
+        st = _gemm_call(lib, nb, 1, R, rep, ones, rep, _lib.OP_N, t.data, R, _lib.OP_N, out, 0,
+                        rep * R, R, 1.0, 0.0, None)
+    _lib.check(st, "sum_paths")
+    if keep_batch:
+        return Tensor(t.labels, out, (nb,) + t.dims[1:])
+    return Tensor(t.labels[1:], out, t.dims[1:])
+
 
 # ---------------------------------------------------------------------------
 # permutation API shims (reference signatures; one device pass whatever the plan)

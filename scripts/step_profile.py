@@ -10,6 +10,9 @@ qf.set_gemm_mode(mode)
 if os.environ.get("QF_TC3_VARIANT"):
     from paper_1811_09599_b200 import _lib
     _lib.load().qf_tc3_set_variant(int(os.environ["QF_TC3_VARIANT"]))
+if os.environ.get("QF_SMALL_ENGINE"):
+    from paper_1811_09599_b200 import _lib
+    _lib.load().qf_small_engine(int(os.environ["QF_SMALL_ENGINE"]))
 lat = qf.Lattice.named("grid:5x5"); circ = qf.generate_rqc(lat, "1+24+1", 0)
 eng = qf.AmplitudeEngine(circ, qf.grid_plan(lat, n_cuts=1))
 rng = np.random.Generator(np.random.PCG64(0))

@@ -254,3 +254,35 @@ def test_late_config2_1024_matches_early(golden):
     assert rel_l2(late, early) < 1e-5
     assert (st0.flops, st0.paths_used) == (st1.flops, st1.paths_used)
     assert rel_l2(late[:48], golden_amps(case)) < 1e-4
+
+
+@pytest.mark.parametrize("late", [False, True])
+@pytest.mark.parametrize("idx", range(19))
+def test_path_batching_is_transparent(golden, idx, late):
+    """Walking all values of the last cut as one batched pass (the value an
+    extra batch index, operands without it broadcast) gives the per-path
+    walk's amplitudes and exactly the reference's PathStats."""
+    if idx >= len(golden["amplitudes"]):
+        pytest.skip("no such case")
+    case = golden["amplitudes"][idx]
+    eng = _engine(golden, case)
+    fid = qf.FidelitySpec(case["f"], case["fseed"])
+    from paper_1811_09599_b200 import amplitude_engine as ae
+    prev = qf.set_path_batching(False)
+    try:
+        ref, st0 = eng.amplitudes(case["in_bits"], case["out_bits"], fid, late=late)
+    finally:
+        qf.set_path_batching(prev)
+    qf.set_path_batching(True)
+    n0 = ae.PATH_GROUPS_RUN[0]
+    got, st1 = eng.amplitudes(case["in_bits"], case["out_bits"], fid, late=late)
+    single, _ = eng.amplitude(case["in_bits"], case["out_bits"][0], fid)
+    qf.set_path_batching(prev)
+    assert rel_l2(got, ref) < 1e-5, case["name"]
+    assert rel_l2(got, golden_amps(case)) < _tol(case["dtype"]), case["name"]
+    assert abs(single - golden_amps(case)[0]) <= _tol(case["dtype"]) * 10 * \
+        max(abs(golden_amps(case)[0]), np.linalg.norm(golden_amps(case)) / len(got))
+    assert (st1.paths_total, st1.paths_used, st1.flops) == \
+        (case["paths_total"], case["paths_used"], case["flops"])
+    if case["name"].startswith("config2") and late and case["dtype"] == "complex64":
+        assert ae.PATH_GROUPS_RUN[0] > n0, "config 2 should walk its cut values as one group"

@@ -283,3 +283,15 @@ def test_statevector_pass_plan_covers_each_gate_once():
             assert len(gs) <= sv.MAX_OPS
             for g in gs:
                 assert {n - 1 - q for q in g.qubits} <= set(bits)
+
+
+def test_path_groups_split_on_the_other_cuts():
+    from paper_1811_09599_b200.amplitude_engine import _path_groups
+    paths = [(a, b, c) for a in range(2) for b in range(3) for c in range(2)]
+    groups = list(_path_groups(paths, 1))
+    # groups vary only cut 1; consecutive paths with other digits equal
+    for g in groups:
+        assert len({(p[0], p[2]) for p in g}) == 1
+    assert sum(len(g) for g in groups) == len(paths)
+    assert [len(g) for g in _path_groups([(0, 0), (0, 1), (1, 0), (1, 1)], 1)] == [2, 2]
+    assert [len(g) for g in _path_groups([(0,), (1,), (2,)], None)] == [1, 1, 1]
