@@ -24,6 +24,8 @@
 //      in output order for write locality.
 // Plans (tables) are cached per (dims, perm, elem size, device).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -43,6 +45,7 @@ struct PermParams {
   int n_outer;
   int LA, HB, LB, HA, pitch, T;
   int la_shift, lb_shift;  // log2 if power of two, else -1
+  int skew_q, skew_s;      // vec2 tile: in-row column c sits at c + skew_s * (c >> skew_q)
   int64_t outer_dim[kMaxRank];
   int64_t outer_in[kMaxRank];
   int64_t outer_out[kMaxRank];
@@ -203,9 +206,21 @@ __global__ void __launch_bounds__(kThreads)
         eh = i / LA;
         el = i - eh * LA;
       }
-      cp_async16(tb + eh * pitch + el, sp + s_hin[eh] + el);
+      cp_async16(tb + eh * pitch + el + p.skew_s * (el >> p.skew_q), sp + s_hin[eh] + el);
     }
     cp_async_commit();
+  };
+  // logical tile position (row * LA + column, the f/g tables) -> smem slot
+  auto phys = [&](int pos) {
+    int row, col;
+    if (POW2) {
+      row = pos >> p.la_shift;
+      col = pos & (LA - 1);
+    } else {
+      row = pos / LA;
+      col = pos - row * LA;
+    }
+    return row * pitch + col + p.skew_s * (col >> p.skew_q);
   };
   auto drain = [&](int j, int buf) {  // write tile j out of buf
     float2 *dp = dst2 + s_base[2 * j + 1];
@@ -221,8 +236,8 @@ __global__ void __launch_bounds__(kThreads)
         ul = i - uh * LB;
       }
       const int f = s_f[uh];
-      const float2 a = tb[f + s_g[ul]];
-      const float2 b = tb[f + s_g[ul + 1]];
+      const float2 a = tb[phys(f + s_g[ul])];
+      const float2 b = tb[phys(f + s_g[ul + 1])];
       *reinterpret_cast<float4 *>(dp + s_outk[uh] + ul) = make_float4(a.x, a.y, b.x, b.y);
     }
   };
@@ -429,7 +444,7 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
   }
 
   const int64_t TA = 512 / elem_bytes, TB = 512 / elem_bytes;
-  const int64_t Tmin = 16384 / elem_bytes, Tmax = 32768 / elem_bytes;
+  const int64_t Tmin = 32768 / elem_bytes, Tmax = 32768 / elem_bytes;  // 32 KB tiles (measured: 16 KB tiles ran ~20% slower)
 
   // 3. A = innermost input axes [a_start, r)
   int r = L.rank();
@@ -635,6 +650,51 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
   int pitch = (int)LA + best_pad;
   std::vector<int64_t> f_slot, g_slot;
   pos_tables(pitch, f_slot, g_slot);
+  int skew_q = 30, skew_s = 0;
+  if (elem_bytes == 8 && LA % 2 == 0 && LB % 2 == 0) {
+    // the pair kernel: tables hold LOGICAL positions (pitch LA); the smem
+    // slot of column c in a row is c + s*(c >> q) (+ row padding), chosen by
+    // simulating its two phases: 16-byte cp.async rows in, two 8-byte reads
+    // per output pair out (strided A axes among the output-contiguous ones
+    // would otherwise hit one bank)
+    std::vector<int64_t> f, g;
+    pos_tables((int)LA, f, g);
+    int best = 1 << 30;
+    for (int q = 2; q <= 9; ++q) {
+      for (int sk = 0; sk <= 8; sk += 2) {
+        if (sk == 0 && q != 2) continue;
+        if ((int64_t(1) << q) >= LA && sk) continue;
+        for (int pad = 0; pad <= 16; pad += 2) {
+          const int64_t row_len = LA + (sk ? (int64_t)sk * ((LA - 1) >> q) : 0) + pad;
+          if (HB * row_len * elem_bytes > 44 * 1024) continue;
+          auto ph = [&](int64_t pos) {
+            const int64_t row = pos / LA, col = pos % LA;
+            return (int)(row * row_len + col + (sk ? sk * (col >> q) : 0));
+          };
+          int cost = 0;
+          for (int w = 0; w < 8; ++w) {
+            std::vector<int> ld, st0, st1;
+            for (int l = 0; l < 32; ++l) {
+              const int64_t i = 2 * (w * 32 + l);
+              if (i >= T) break;
+              ld.push_back(ph((i / LA) * LA + i % LA) / 2);  // 16-byte slots
+              st0.push_back(ph(f[i / LB] + g[i % LB]));
+              st1.push_back(ph(f[i / LB] + g[i % LB + 1]));
+            }
+            cost += conflict_cost(ld, 16) + conflict_cost(st0, 8) + conflict_cost(st1, 8);
+          }
+          if (cost < best) {
+            best = cost;
+            skew_q = sk ? q : 30;
+            skew_s = sk;
+            pitch = (int)row_len;
+          }
+        }
+      }
+    }
+    f_slot = f;
+    g_slot = g;
+  }
 
   PermParams &tp = plan.tp;
   memset(&tp, 0, sizeof(tp));
@@ -644,6 +704,8 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
   tp.HA = (int)HA;
   tp.T = (int)T;
   tp.pitch = pitch;
+  tp.skew_q = skew_q;
+  tp.skew_s = skew_s;
   tp.la_shift = ilog2_exact(LA);
   tp.lb_shift = ilog2_exact(LB);
   tp.n_outer = (int)outer_pos.size();
@@ -665,6 +727,10 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
   plan.grid = (int)std::min<int64_t>(tp.ntiles, (int64_t)sm_count() * per_sm);
   plan.kind = PermPlan::kTiled;
   plan.vec2 = vec2;
+  if (getenv("QF_PERM_DEBUG"))
+    fprintf(stderr, "permute plan: rank %d T %lld LA %lld HB %lld LB %lld HA %lld pitch %d skew %d/%d "
+            "outer %d tiles %lld\n", r, (long long)T, (long long)LA, (long long)HB, (long long)LB,
+            (long long)HA, pitch, skew_s, skew_q, tp.n_outer, (long long)tp.ntiles);
   if (vec2) {
     plan.smem = 2 * tile_bytes + (HB + HA) * 8 + 2 * kBaseChunk * 8 + (HA + LB) * 4;
     int per_sm2 = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (plan.smem + 1024)));
@@ -728,7 +794,7 @@ static int launch(const PermPlan &plan, const void *src, void *dst, cudaStream_t
     auto kv = pow2 ? permute_tiled_vec2_kernel<true> : permute_tiled_vec2_kernel<false>;
     static thread_local bool attr_v[2] = {false, false};
     if (!attr_v[pow2]) {
-      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       attr_v[pow2] = true;
     }
     kv<<<plan.grid, kThreads, plan.smem, s>>>((const float4 *)src, (float4 *)dst, plan.tp,
