@@ -257,6 +257,12 @@ int qf_tc3_set_variant(int variant);
  * previous one. */
 int qf_small_engine(int engine);
 
+/* K3 narrow outputs (complex64, N <= 8, K <= 64): 1 = row-stream pipeline
+ * with warp-level tensor cores (mma.sync m16n8k8 TF32, 3xTF32 split), 0 =
+ * its FFMA twin (the default: measured faster); < 0 only queries.  Returns
+ * the previous one.  QF_GEMM_FFMA calls never use the tensor-core twin. */
+int qf_rowmma(int enabled);
+
 /* Name of the last kernel this library launched on the calling thread
  * (static string; "" if none) -- lets profilers attribute timings. */
 const char *qf_last_kernel(void);

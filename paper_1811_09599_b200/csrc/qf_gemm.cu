@@ -40,6 +40,10 @@ __device__ __forceinline__ void cfma(V &acc, const V &a, const V &b) {
   acc.y = fma(a.y, b.x, acc.y);
 }
 
+// (tried: complex64 via two packed FFMA2 (fma.rn.f32x2) per complex MAC --
+// bit-identical but measured slower on every CUDA-core engine, e.g. the
+// config-2 1024 x (4096 x 8 x 64) row-stream GEMM 0.539 -> 0.607 ms)
+
 
 // ---------------------------------------------------------------------------
 // tiled SIMT kernel
@@ -711,26 +715,47 @@ __device__ __forceinline__ void rs_cp16(uint32_t dst, const void *src, bool vali
                : "memory");
 }
 
-template <int NN, int KC>
+template <int NN, int KC, bool MMA = false>
 struct RsLayout {
-  static constexpr int APITCH = KC * 8 + 16;          // staged A row (odd multiple of 16 B)
+  // staged A row: an odd multiple of 16 B (FFMA: lane = row reads whole
+  // rows); 8 words mod 32 for the MMA fragments (lanes 4 rows x 4 k apart)
+  static constexpr int APITCH = MMA ? KC * 8 + 32 : KC * 8 + 16;
   static constexpr int OPITCH = NN * 8 + 16;          // staged C row
   static constexpr int ABUF = 32 * APITCH;
-  static constexpr int WARP = 2 * ABUF + 32 * OPITCH;  // per warp: A ring + C staging
-  static constexpr int BMAX = 1024;                    // complex entries of B[b] (K x NN)
-  static constexpr int SMEM = BMAX * 8 + RS_WARPS * WARP;
+  static constexpr int NSLOT = MMA ? 3 : 2;           // A ring depth per warp
+  static constexpr int WARP = NSLOT * ABUF + 32 * OPITCH;  // per warp: A ring + C staging
+  // B[b]: complex K x NN (FFMA) or TF32 hi/lo fragments (MMA: per 4 k and
+  // 4 columns one float4 per lane, K <= KMAX_MMA)
+  static constexpr int KMAX_MMA = 64;
+  static constexpr int BBYTES = MMA ? (KMAX_MMA / 4) * (NN / 4) * 32 * 16 : 1024 * 8;
+  static constexpr int SMEM = BBYTES + RS_WARPS * WARP;
 };
 
-template <int NN, int KC>
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int NN, int KC, bool MMA = false>
 __global__ void __launch_bounds__(RS_WARPS * 32)
     cgemm_rowstream_kernel(const __grid_constant__ GemmArgs g, int64_t steps_per_b,
                            int64_t steps_per_cta) {
-  using L = RsLayout<NN, KC>;
+  using L = RsLayout<NN, KC, MMA>;
   extern __shared__ __align__(16) unsigned char rs_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float2 *Bs = reinterpret_cast<float2 *>(rs_smem);
-  unsigned char *wsm = rs_smem + L::BMAX * 8 + warp * L::WARP;
-  unsigned char *Ost = wsm + 2 * L::ABUF;
+  unsigned char *wsm = rs_smem + L::BBYTES + warp * L::WARP;
+  unsigned char *Ost = wsm + L::NSLOT * L::ABUF;
   const uint32_t abuf_u32 = static_cast<uint32_t>(__cvta_generic_to_shared(wsm));
   const int K = (int)g.K, N = (int)g.N;
   const int nch = (K + KC - 1) / KC;
@@ -827,6 +852,9 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
   const bool use_beta = (br_ != 0.f || bi_ != 0.f);
   load_roff();
   fetch(0);
+  if constexpr (MMA) {
+    for (int i = 1; i < L::NSLOT - 1; ++i) fetch(i);
+  }
   int64_t cur_b = -1;
   int q = 0;
   int64_t b = st0 / steps_per_b;
@@ -840,12 +868,36 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     if (b != cur_b) {  // CTA-uniform: every warp walks the same steps
       __syncthreads();
       const float2 *B = reinterpret_cast<const float2 *>(g.B) + b_batch_off(g, b);
-      for (int i = threadIdx.x; i < K * NN; i += RS_WARPS * 32) {
-        const int k = i / NN, n = i - k * NN;
-        float2 v = make_float2(0.f, 0.f);
-        if (n < N)
-          v = g.opB == QF_OP_N ? __ldg(B + (int64_t)k * g.ldb + n) : __ldg(B + (int64_t)n * g.ldb + k);
-        Bs[i] = v;
+      if constexpr (MMA) {
+        // real form of the complex product, output columns interleaved
+        // (re, im) and each 4-k step's 8 real rows ordered (Re A of k0..k3,
+        // Im A of k0..k3): lane (gq = lane/4, t = lane%4) of fragment
+        // (kstep, ntile) holds rows (Re A, Im A) of k = 4 kstep + t for real
+        // column 8 ntile + gq -- {b0, b1} hi then lo, TF32
+        const int nfr = nch * (KC / 4) * (NN / 4) * 32;
+        float4 *Bf = reinterpret_cast<float4 *>(rs_smem);
+        for (int i = threadIdx.x; i < nfr; i += RS_WARPS * 32) {
+          const int ln = i & 31, fr = i >> 5;
+          const int nt = fr % (NN / 4), ks = fr / (NN / 4);
+          const int k = 4 * ks + (ln & 3), col = 8 * nt + (ln >> 2);
+          const int n = col >> 1;
+          float2 v = make_float2(0.f, 0.f);
+          if (n < N && k < K)
+            v = g.opB == QF_OP_N ? __ldg(B + (int64_t)k * g.ldb + n) : __ldg(B + (int64_t)n * g.ldb + k);
+          // Re column: (Br, -Bi); Im column: (Bi, Br)
+          const float b0 = (col & 1) ? v.y : v.x, b1 = (col & 1) ? v.x : -v.y;
+          const uint32_t h0 = tf32_rna(b0), h1 = tf32_rna(b1);
+          Bf[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1),
+                              b0 - __uint_as_float(h0), b1 - __uint_as_float(h1));
+        }
+      } else {
+        for (int i = threadIdx.x; i < K * NN; i += RS_WARPS * 32) {
+          const int k = i / NN, n = i - k * NN;
+          float2 v = make_float2(0.f, 0.f);
+          if (n < N)
+            v = g.opB == QF_OP_N ? __ldg(B + (int64_t)k * g.ldb + n) : __ldg(B + (int64_t)n * g.ldb + k);
+          Bs[i] = v;
+        }
       }
       cur_b = b;
       __syncthreads();
@@ -853,6 +905,69 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
     float2 acc[NN];
 #pragma unroll
     for (int n = 0; n < NN; ++n) acc[n] = make_float2(0.f, 0.f);
+    if constexpr (MMA) {
+      // 3xTF32 on the warp-level tensor-core path: the 32 rows are two
+      // m16 tiles, each 4-k step one k8 of the real form
+      float c[2][NN / 4][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NN / 4; ++nt)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) c[mt][nt][j] = 0.f;
+      const int gq = lane >> 2, t = lane & 3;
+      const float4 *Bf = reinterpret_cast<const float4 *>(rs_smem);
+      for (int ch = 0; ch < nch; ++ch, ++q) {
+        fetch((q + L::NSLOT - 1) % L::NSLOT);   // NSLOT - 1 chunks in flight
+        asm volatile("cp.async.wait_group %0;" ::"n"(L::NSLOT - 1) : "memory");
+        __syncwarp();
+        const unsigned char *abuf = wsm + (q % L::NSLOT) * L::ABUF;
+#pragma unroll
+        for (int ks = 0; ks < KC / 4; ++ks) {
+          uint32_t ah[2][4], al[2][4];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const float2 lo = *reinterpret_cast<const float2 *>(
+                abuf + (16 * mt + gq) * L::APITCH + (4 * ks + t) * 8);
+            const float2 hi = *reinterpret_cast<const float2 *>(
+                abuf + (16 * mt + gq + 8) * L::APITCH + (4 * ks + t) * 8);
+            const float av[4] = {lo.x, hi.x, lo.y, hi.y};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              ah[mt][j] = tf32_rna(av[j]);
+              al[mt][j] = __float_as_uint(av[j] - __uint_as_float(ah[mt][j]));
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NN / 4; ++nt) {
+            const float4 bf = Bf[((ch * (KC / 4) + ks) * (NN / 4) + nt) * 32 + lane];
+            const uint32_t bh0 = __float_as_uint(bf.x), bh1 = __float_as_uint(bf.y);
+            const uint32_t bl0 = __float_as_uint(bf.z), bl1 = __float_as_uint(bf.w);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              mma_tf32(c[mt][nt], al[mt], bh0, bh1);
+              mma_tf32(c[mt][nt], ah[mt], bl0, bl1);
+              mma_tf32(c[mt][nt], ah[mt], bh0, bh1);
+            }
+          }
+        }
+        __syncwarp();  // the slot is refilled by a later fetch
+      }
+      // fragments -> staging rows (row = lane's C row) -> acc[] per lane
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NN / 4; ++nt) {
+          *reinterpret_cast<float2 *>(Ost + (16 * mt + gq) * L::OPITCH + (4 * nt + t) * 8) =
+              make_float2(c[mt][nt][0], c[mt][nt][1]);
+          *reinterpret_cast<float2 *>(Ost + (16 * mt + gq + 8) * L::OPITCH + (4 * nt + t) * 8) =
+              make_float2(c[mt][nt][2], c[mt][nt][3]);
+        }
+      __syncwarp();
+#pragma unroll
+      for (int n = 0; n < NN; ++n) acc[n] = *reinterpret_cast<const float2 *>(Ost + lane * L::OPITCH + n * 8);
+      __syncwarp();
+    } else
     for (int ch = 0; ch < nch; ++ch, ++q) {
       fetch((q + 1) & 1);  // next chunk (of this or the next step) into the other slot
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -946,10 +1061,10 @@ bool rowstream_eligible(const GemmArgs &g) {
   return g.N >= 1 && g.N <= 16 && g.K >= 1 && g.K * (g.N <= 8 ? 8 : 16) <= 1024 && g.M >= 32;
 }
 
-template <int NN, int KC>
+template <int NN, int KC, bool MMA = false>
 int rowstream_launch(const GemmArgs &g, cudaStream_t s) {
-  using L = RsLayout<NN, KC>;
-  auto kern = cgemm_rowstream_kernel<NN, KC>;
+  using L = RsLayout<NN, KC, MMA>;
+  auto kern = cgemm_rowstream_kernel<NN, KC, MMA>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
@@ -962,10 +1077,31 @@ int rowstream_launch(const GemmArgs &g, cudaStream_t s) {
   const int64_t per_cta = (steps + ctas - 1) / ctas;
   const int64_t grid = (steps + per_cta - 1) / per_cta;
   kern<<<(unsigned)grid, RS_WARPS * 32, L::SMEM, s>>>(g, steps_per_b, per_cta);
-  return check_launch("cgemm_rowstream");
+  return check_launch(MMA ? "cgemm_rowmma" : "cgemm_rowstream");
+}
+
+// warp-level tensor cores (mma.sync m16n8k8 TF32, 3xTF32 split) inside the
+// row-stream pipeline: N <= 8 outputs, K <= 64.  The FFMA row-stream GEMMs
+// run at 80% issue (ncu), so this cuts their instruction count ~4x -- but it
+// measured SLOWER on the config-2 shapes (1024 x (4096 x 8 x 64): 0.539 ->
+// 0.551 ms, 2 x (8.4M x 8 x 8): 0.404 -> 0.572 ms at one CTA per SM), so it
+// is off by default (qf_rowmma(1) enables it; tests keep it correct)
+static int g_rowmma = 0;
+// QF_GEMM_FFMA calls keep every product on the FFMA pipe (the baseline)
+static thread_local bool t_allow_mma = true;
+struct MmaScope {
+  bool prev;
+  explicit MmaScope(int mode) : prev(t_allow_mma) { t_allow_mma = (mode & 0xff) != QF_GEMM_FFMA; }
+  ~MmaScope() { t_allow_mma = prev; }
+};
+bool rowmma_eligible(const GemmArgs &g) {
+  return g_rowmma && t_allow_mma && g.N >= 1 && g.N <= 8 && g.K >= 1 && g.K <= RsLayout<8, 16, true>::KMAX_MMA &&
+         g.M >= 32;
 }
 
 int gemm_rowstream(const GemmArgs &g, cudaStream_t s) {
+  if (rowmma_eligible(g)) return g.K <= 8 ? rowstream_launch<8, 8, true>(g, s)
+                                          : rowstream_launch<8, 16, true>(g, s);
   if (g.N <= 8) return g.K <= 8 ? rowstream_launch<8, 8>(g, s) : rowstream_launch<8, 16>(g, s);
   return g.K <= 8 ? rowstream_launch<16, 8>(g, s) : rowstream_launch<16, 16>(g, s);
 }
@@ -1202,7 +1338,8 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
     QF_REQUIRE(g.K >= 1 && g.N <= 16 && g.K * g.N <= SKN_MAX, "gemm: transposed C needs N <= 16");
     if constexpr (sizeof(R) == 4) {
       if (rowstream_eligible(g) &&
-          (g_small_engine == 3 || (g_small_engine != 2 && !(g.a_roff ? g.rows_unit : g.opA == QF_OP_T))))
+          (g_small_engine == 3 || (g_small_engine != 2 && (rowmma_eligible(g) ||
+                                                          !(g.a_roff ? g.rows_unit : g.opA == QF_OP_T)))))
         return gemm_rowstream(g, s);
     }
     return gemm_rowblock<R>(g, s);
@@ -1217,7 +1354,8 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
       // gathers) and K > 8 the row-block kernel's direct loads are as
       // coalesced and run at higher occupancy (measured 0.74 vs 0.89 ms)
       const bool rows_direct = (g.a_roff ? g.rows_unit : g.opA == QF_OP_T) && g.K > 8;
-      if (rowstream_eligible(g) && (g_small_engine == 3 || (g_small_engine == 0 && !rows_direct)))
+      if (rowstream_eligible(g) &&
+          (g_small_engine == 3 || (g_small_engine == 0 && (!rows_direct || rowmma_eligible(g)))))
         return gemm_rowstream(g, s);
     }
     const bool rowblock = g_small_engine == 0 ? g.N <= 16 : g_small_engine == 2;
@@ -1244,6 +1382,7 @@ int qf_cgemm_c64(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const
                  int64_t lda, int64_t strideA, int opA, const void *B, int64_t ldb, int64_t strideB,
                  int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re, float alpha_im,
                  float beta_re, float beta_im, void *stream) {
+  qf::MmaScope mma_scope(mode);
   qf::GemmArgs g{batch, M, N, K, A, lda, strideA, opA, B, ldb, strideB, opB, C, ldc, strideC,
                  alpha_re, alpha_im, beta_re, beta_im};
   int st = qf::validate(g);
@@ -1260,6 +1399,7 @@ int qf_cgemm_c64_gather(int mode, int64_t batch, int64_t M, int64_t N, int64_t K
                         const void *B, int64_t ldb, int64_t strideB, int opB, void *C, int64_t ldc,
                         int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                         float beta_im, void *stream) {
+  qf::MmaScope mma_scope(mode);
   QF_REQUIRE(a_roff != nullptr && a_coff != nullptr, "gather gemm: offset tables are NULL");
   const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
   mode &= ~QF_GATHER_ROWS_UNIT;
@@ -1280,6 +1420,7 @@ int qf_cgemm_c64_gather_boff(int mode, int64_t batch, int64_t M, int64_t N, int6
                              const int32_t *a_coff, const void *B, int64_t ldb, int64_t strideB,
                              int opB, void *C, int64_t ldc, int64_t strideC, float alpha_re,
                              float alpha_im, float beta_re, float beta_im, void *stream) {
+  qf::MmaScope mma_scope(mode);
   QF_REQUIRE((a_roff != nullptr) == (a_coff != nullptr) && (a_boff != nullptr || batch == 0),
              "gather gemm: offset tables are NULL");
   const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
@@ -1311,6 +1452,7 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
                     int64_t strideB, int opB, const int64_t *b_boff, void *C, int64_t ldc,
                     int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                     float beta_im, void *stream) {
+  qf::MmaScope mma_scope(mode);
   QF_REQUIRE((a_roff != nullptr) == (a_coff != nullptr), "gemm_ex: a_roff/a_coff must pair");
   const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
   const bool a_even = (mode & QF_BOFF_EVEN) != 0, b_even = (mode & QF_BBOFF_EVEN) != 0;
@@ -1375,6 +1517,12 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
   int st = qf::validate(g);
   if (st != QF_OK) return st;
   return qf::gemm_tc3(g, qf::as_stream(stream));
+}
+
+int qf_rowmma(int enabled) {
+  int prev = qf::g_rowmma;
+  if (enabled >= 0) qf::g_rowmma = enabled ? 1 : 0;
+  return prev;
 }
 
 int qf_small_engine(int engine) {

@@ -468,3 +468,27 @@ def test_transposed_store_for_kept_cut(nb, perm):
     want = tc.contract(ta, late.batch(ts))
     w = want.transpose_to(got.labels).array
     assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(3, 4096, 8, 64), (1, 32768, 8, 8), (5, 1000, 8, 64),
+                                   (7, 333, 5, 24), (2, 100, 3, 7), (4, 64, 1, 1),
+                                   (2, 4096, 8, 33), (1, 96, 7, 64), (300, 256, 8, 16)])
+@pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
+@pytest.mark.parametrize("ab", [(1.0, 0.0), (0.5 - 1j, 0.25 + 0.5j)])
+def test_rowmma_narrow_outputs(shape, ops, ab):
+    """N <= 8, K <= 64: the row-stream pipeline on warp-level tensor cores
+    (mma.sync TF32, 3xTF32) -- every layout, alpha/beta, ragged K and rows."""
+    lib = _lib.load()
+    prev = lib.qf_rowmma(1)
+    try:
+        assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_AUTO, alpha=ab[0], beta=ab[1]) < 1e-5
+        gemv = shape[2] <= 4 and ops[0] == 0 and shape[3] >= 32   # warp-per-row GEMV first
+        if shape[1] >= 32 and not gemv:
+            assert lib.qf_last_kernel() == b"cgemm_rowmma"
+        lib.qf_rowmma(0)
+        assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_AUTO, alpha=ab[0], beta=ab[1]) < 1e-5
+        lib.qf_rowmma(1)
+        _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_FFMA)
+        assert lib.qf_last_kernel() != b"cgemm_rowmma"      # the FFMA baseline stays FFMA
+    finally:
+        lib.qf_rowmma(prev)
