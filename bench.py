@@ -380,7 +380,8 @@ def run_gpu(args):
                     "peak_basis": f"hbm_gbs {pk['source']}"}
         roof.update({"achieved": round(achieved, 2), "peak": round(peak, 1),
                      "frac": round(achieved / peak, 4),
-                     "traffic_detail": measured_traffic("config2", dom, d["bytes"] / d["launches"]),
+                     "traffic_detail": measured_traffic(args.workload, dom,
+                                                        d["bytes"] / d["launches"]),
                      "arithmetic_intensity": round(ai, 2), "ridge": round(ridge, 2),
                      "algorithmic": (f"{dom}: 8*m*k*n flops and 8*(m*k + k*n + m*n)*batch bytes "
                                      f"per launch (16 B/element for permutes), summed over "

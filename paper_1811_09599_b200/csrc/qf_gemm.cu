@@ -251,6 +251,94 @@ __global__ void __launch_bounds__(STHREADS)
   if (kl == 0 && p < P) ((V *)ws)[(b * nsplit + split) * P + p] = red[tid];
 }
 
+// Row-contiguous A (opA N) with many outputs: the mapping above puts the
+// output index on consecutive lanes, i.e. every lane in a different row (one
+// sector per lane).  Here a warp owns one row m at a time and its lanes walk
+// k with 16-byte loads (whole 512-byte runs per request); the N <= 4 columns
+// of B are read alongside.  Same workspace layout and second pass.
+template <int NC>
+__global__ void __launch_bounds__(STHREADS)
+    cgemm_skinny_rows_kernel(const __grid_constant__ GemmArgs g, int64_t kchunk, int nsplit,
+                             void *ws) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t split = blockIdx.x, b = blockIdx.y;
+  const float2 *A = (const float2 *)g.A + a_batch_off(g, b);
+  const float2 *B = (const float2 *)g.B + b_batch_off(g, b);
+  const int64_t k0 = split * kchunk, k1 = min(g.K, k0 + kchunk);
+  const int N = (int)g.N;
+  const bool vec = g.lda % 2 == 0 && g.sA % 2 == 0 && k0 % 2 == 0 && !g.a_boff &&
+                   ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0);
+  for (int64_t m = warp; m < g.M; m += STHREADS / 32) {
+    const float2 *ap = A + m * g.lda;
+    float2 acc[NC], acc2[NC];
+#pragma unroll
+    for (int n = 0; n < NC; ++n) acc[n] = acc2[n] = make_float2(0.f, 0.f);
+    auto bval = [&](int64_t k, int n) {
+      return g.opB == QF_OP_N ? __ldg(B + k * g.ldb + n) : __ldg(B + (int64_t)n * g.ldb + k);
+    };
+    int64_t k = k0 + 2 * lane;
+    if (vec) {
+      // four 16-byte loads in flight per lane
+      for (; k + 193 < k1; k += 256) {
+        float4 a4[4];
+        float2 b4[4][2][NC];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a4[u] = __ldg(reinterpret_cast<const float4 *>(ap + k + 64 * u));
+#pragma unroll
+          for (int n = 0; n < NC; ++n) {
+            if (n < N) {
+              b4[u][0][n] = bval(k + 64 * u, n);
+              b4[u][1][n] = bval(k + 64 * u + 1, n);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int n = 0; n < NC; ++n)
+            if (n < N) {
+              cfma(acc[n], make_float2(a4[u].x, a4[u].y), b4[u][0][n]);
+              cfma(acc2[n], make_float2(a4[u].z, a4[u].w), b4[u][1][n]);
+            }
+      }
+      for (; k + 1 < k1; k += 64) {
+        const float4 a2 = __ldg(reinterpret_cast<const float4 *>(ap + k));
+#pragma unroll
+        for (int n = 0; n < NC; ++n) {
+          if (n < N) {
+            cfma(acc[n], make_float2(a2.x, a2.y), bval(k, n));
+            cfma(acc2[n], make_float2(a2.z, a2.w), bval(k + 1, n));
+          }
+        }
+      }
+      if (k < k1) {
+#pragma unroll
+        for (int n = 0; n < NC; ++n)
+          if (n < N) cfma(acc[n], __ldg(ap + k), bval(k, n));
+      }
+    } else {
+      for (k = k0 + lane; k < k1; k += 32) {
+        const float2 a = __ldg(ap + k);
+#pragma unroll
+        for (int n = 0; n < NC; ++n)
+          if (n < N) cfma(acc[n], a, bval(k, n));
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NC; ++n) {
+      float x = acc[n].x + acc2[n].x, y = acc[n].y + acc2[n].y;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        x += __shfl_xor_sync(0xffffffffu, x, o);
+        y += __shfl_xor_sync(0xffffffffu, y, o);
+      }
+      if (lane == 0 && n < N)
+        ((float2 *)ws)[(b * nsplit + split) * (g.M * N) + m * N + n] = make_float2(x, y);
+    }
+  }
+}
+
 template <typename R>
 __global__ void cgemm_skinny_reduce(const __grid_constant__ GemmArgs g, int P, int nsplit,
                                     const void *ws) {
@@ -1320,14 +1408,24 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
     nsplit = std::min<int64_t>(nsplit, (g.K + min_chunk - 1) / min_chunk);
     nsplit = std::max<int64_t>(1, std::min<int64_t>(nsplit, 4096));
     int64_t kchunk = (g.K + nsplit - 1) / nsplit;
+    const bool rows = sizeof(R) == 4 && g.opA == QF_OP_N && !g.a_roff && P >= 8 && g.N <= 4;
+    if (rows) kchunk = (kchunk + 63) / 64 * 64;   // 16-byte aligned chunks
     nsplit = (g.K + kchunk - 1) / kchunk;
     QF_REQUIRE(g.batch <= 65535, "gemm: skinny batch %lld exceeds 65535", (long long)g.batch);
     int st = QF_OK;
     void *ws = workspace(g.batch * nsplit * P * (int64_t)sizeof(typename C2<R>::T), s, &st);
     if (st != QF_OK) return st;
     dim3 grid((unsigned)nsplit, (unsigned)g.batch);
-    cgemm_skinny_kernel<R><<<grid, STHREADS, 0, s>>>(g, (int)P, Ppad, kchunk, (int)nsplit, ws);
-    int rc = check_launch("cgemm_skinny");
+    int rc;
+    if (rows) {
+      // many rows: warp-per-row with lanes along k (see cgemm_skinny_rows_kernel)
+      if (g.N == 1) cgemm_skinny_rows_kernel<1><<<grid, STHREADS, 0, s>>>(g, kchunk, (int)nsplit, ws);
+      else cgemm_skinny_rows_kernel<4><<<grid, STHREADS, 0, s>>>(g, kchunk, (int)nsplit, ws);
+      rc = check_launch("cgemm_skinny_rows");
+    } else {
+      cgemm_skinny_kernel<R><<<grid, STHREADS, 0, s>>>(g, (int)P, Ppad, kchunk, (int)nsplit, ws);
+      rc = check_launch("cgemm_skinny");
+    }
     if (rc != QF_OK) return rc;
     int64_t total = g.batch * P;
     cgemm_skinny_reduce<R><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(g, (int)P, (int)nsplit,

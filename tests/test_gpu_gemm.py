@@ -492,3 +492,12 @@ def test_rowmma_narrow_outputs(shape, ops, ab):
         assert lib.qf_last_kernel() != b"cgemm_rowmma"      # the FFMA baseline stays FFMA
     finally:
         lib.qf_rowmma(prev)
+
+
+@pytest.mark.parametrize("shape", [(1, 64, 1, 1 << 20), (2, 16, 4, 5000), (1, 200, 1, 777),
+                                   (3, 8, 3, 4096), (1, 256, 1, 300)])
+@pytest.mark.parametrize("ops", [(0, 0), (0, 1)])
+def test_skinny_many_rows(shape, ops):
+    """M*N <= 256 outputs, long K, row-contiguous A: warp-per-row split-K."""
+    assert _gemm(*shape, *ops, np.complex64) < 1e-5
+    assert _gemm(*shape, *ops, np.complex64, alpha=0.5 + 1j, beta=-0.25) < 1e-5
