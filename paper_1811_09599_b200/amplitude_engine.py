@@ -305,14 +305,27 @@ class AmplitudeEngine:
         """Order in which a late-sliced batch is walked: bit-strings sorted by
         their qubits in the order the plan first consumes them, so entries
         that share an open prefix are adjacent and re-read it from L2."""
-        seq = []
-        for step in self.plan.steps():
-            for x in step.inputs:
-                if x[:1] == "t" and x[1:].isdigit() and int(x[1:]) not in seq:
-                    seq.append(int(x[1:]))
-        seq += [q for q in range(self.circuit.n) if q not in seq]
+        seq = self.__dict__.get("_consume_seq")
+        if seq is None:
+            seq = []
+            for step in self.plan.steps():
+                for x in step.inputs:
+                    if x[:1] == "t" and x[1:].isdigit() and int(x[1:]) not in seq:
+                        seq.append(int(x[1:]))
+            seq += [q for q in range(self.circuit.n) if q not in seq]
+            seq = self._consume_seq = np.array(seq, dtype=np.int64)
         bits = np.asarray(bits)
-        return np.lexsort([bits[:, q] for q in reversed(seq)])
+        # the bits in plan order packed into <= 62-bit integer keys (most
+        # significant first): one stable argsort instead of n lexsort keys
+        cols = bits[:, seq].astype(np.int64)
+        keys = []
+        for lo in range(0, cols.shape[1], 62):
+            blk = cols[:, lo:lo + 62]
+            w = np.left_shift(np.int64(1), np.arange(blk.shape[1] - 1, -1, -1, dtype=np.int64))
+            keys.append(blk @ w)
+        if len(keys) == 1:
+            return np.argsort(keys[0], kind="stable")
+        return np.lexsort(keys[::-1])
 
     def _graph_runner(self, in_bits, batch: int, fidelity: FidelitySpec,
                       late: bool = False) -> "_GraphRunner":

@@ -295,3 +295,20 @@ def test_path_groups_split_on_the_other_cuts():
     assert sum(len(g) for g in groups) == len(paths)
     assert [len(g) for g in _path_groups([(0, 0), (0, 1), (1, 0), (1, 1)], 1)] == [2, 2]
     assert [len(g) for g in _path_groups([(0,), (1,), (2,)], None)] == [1, 1, 1]
+
+
+@pytest.mark.parametrize("name,n", [("grid:5x5", 25), ("bristlecone-70", 70)])
+def test_batch_order_is_plan_order_lexsort(name, n):
+    """The packed-key walk order equals a lexsort over the bits in the order
+    the plan first consumes the qubits (ties keep input order)."""
+    import numpy as np
+    import paper_1811_09599_b200 as qf
+    lat = qf.Lattice.named(name)
+    circ = qf.generate_rqc(lat, "1+8+1", 0)
+    eng = qf.AmplitudeEngine(circ, qf.builtin_plan(lat) if n == 70 else qf.grid_plan(lat, n_cuts=1))
+    bits = np.random.default_rng(1).integers(0, 2, size=(777, n)).astype(np.int32)
+    bits[5] = bits[9]                       # a duplicate: stable order
+    order = eng.batch_order(bits)
+    seq = eng._consume_seq
+    assert sorted(seq.tolist()) == list(range(n))
+    assert (order == np.lexsort([bits[:, q] for q in reversed(seq)])).all()
