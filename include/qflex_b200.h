@@ -257,6 +257,22 @@ int qf_tc3_set_variant(int variant);
  * previous one. */
 int qf_small_engine(int engine);
 
+/*
+ * Batched GEMM whose A is read in ROW BLOCKS (complex64, N <= 16, K*N <= 4096;
+ * CUDA-core row engines): A(b, r, k) = A + b*strideA + (r / rows_per_block) *
+ * block_stride + r % rows_per_block + k*lda, i.e. a big operand laid out
+ * [outer rows][k][inner rows] contracted over its middle labels in place
+ * (replaces the permute + GEMM of `contract`, rq/tensor_core.py:411-417, for
+ * operands with too many rows for offset tables).  B and C as qf_cgemm_c64.
+ * QF_ERR_UNSUPPORTED outside that shape range.
+ */
+int qf_cgemm_c64_rowblocks(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
+                           const void *A, int64_t rows_per_block, int64_t block_stride,
+                           int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                           int64_t strideB, int opB, void *C, int64_t ldc, int64_t strideC,
+                           float alpha_re, float alpha_im, float beta_re, float beta_im,
+                           void *stream);
+
 /* K3 narrow outputs (complex64, N <= 8, K <= 64): 1 = row-stream pipeline
  * with warp-level tensor cores (mma.sync m16n8k8 TF32, 3xTF32 split), 0 =
  * its FFMA twin (the default: measured faster); < 0 only queries.  Returns

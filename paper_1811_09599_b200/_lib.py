@@ -38,7 +38,7 @@ EXPORTS = (
     "qf_cgemm_c64_view", "qf_sv_basis", "qf_sv_apply", "qf_sv_gather",
     "qf_accumulate",
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
-    "qf_small_engine", "qf_rowmma",
+    "qf_small_engine", "qf_rowmma", "qf_cgemm_c64_rowblocks",
     "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
 )
 
@@ -124,6 +124,10 @@ def _declare(lib):
     lib.qf_tc3_set_variant.argtypes = [ctypes.c_int]
     lib.qf_small_engine.argtypes = [ctypes.c_int]
     lib.qf_rowmma.argtypes = [ctypes.c_int]
+    lib.qf_cgemm_c64_rowblocks.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64, _c_void_p, _i64,
+                                           _i64, _i64, _i64, _c_void_p, _i64, _i64, ctypes.c_int,
+                                           _c_void_p, _i64, _i64, ctypes.c_float, ctypes.c_float,
+                                           ctypes.c_float, ctypes.c_float, _c_void_p]
     lib.qf_last_kernel.restype = ctypes.c_char_p
     lib.qf_last_kernel.argtypes = []
     lib.qf_workspace_reserve.argtypes = [_i64, _c_void_p]

@@ -62,7 +62,17 @@ struct GemmArgs {
   // C stored transposed per entry: C(b, m, n) at C + b*sC + n*ldc + m (row-block
   // and row-stream engines only)
   bool c_trans = false;
+  // opA = T in row blocks (row-block / row-stream engines only): row r at
+  // (r / a_rin) * a_rstride + r % a_rin, k at k * lda -- a big operand laid
+  // out [outer rows][k][inner rows] read in place (no permute)
+  int64_t a_rin = 0, a_rstride = 0;
 };
+
+__device__ __forceinline__ int64_t a_row_base(const GemmArgs &g, int64_t r) {
+  if (!g.a_rin) return r;
+  const int64_t q = r / g.a_rin;
+  return q * g.a_rstride + (r - q * g.a_rin);
+}
 
 __device__ __forceinline__ int64_t b_batch_off(const GemmArgs &g, int64_t b) {
   return g.b_boff ? __ldg(g.b_boff + b) : b * g.sB;
@@ -74,7 +84,7 @@ __device__ __forceinline__ int64_t a_batch_off(const GemmArgs &g, int64_t b) {
 
 __device__ __forceinline__ int64_t a_offset(const GemmArgs &g, int64_t r, int64_t k) {
   if (g.a_roff) return (int64_t)g.a_roff[r] + g.a_coff[k];
-  return g.opA == QF_OP_N ? r * g.lda + k : k * g.lda + r;
+  return g.opA == QF_OP_N ? r * g.lda + k : k * g.lda + a_row_base(g, r);
 }
 
 }  // namespace qf

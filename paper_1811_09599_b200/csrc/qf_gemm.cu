@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(RB_THREADS)
 #pragma unroll
       for (int j = 0; j < RB_NG; ++j) acc[j] = V{R(0), R(0)};
       const V *arow = g.a_roff ? A + g.a_roff[row]
-                               : (g.opA == QF_OP_N ? A + row * g.lda : A + row);
+                               : (g.opA == QF_OP_N ? A + row * g.lda : A + a_row_base(g, row));
       // software pipeline: the next 8 k of A are in flight while this 8 is used
       auto load8 = [&](int k0, V *a) {
         if (vec_a && k0 + 8 <= K) {  // row-major A: four 16-byte loads per 8 k
@@ -878,11 +878,12 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
       const uint32_t dst0 = abuf_u32 + slot * L::ABUF;
       if (mode == 0) {
         const bool rok = r0 + lane < g.M;
+        const int64_t f_rbase = a_row_base(g, r0);   // 32 rows never straddle a row block
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
           const bool ok = rok && k0 + k < K;
           const float2 *src = gat ? A + f_roff + (ok ? __ldg(g.a_coff + k0 + k) : 0)
-                                  : A + (int64_t)(ok ? k0 + k : 0) * g.lda + r0 + lane;
+                                  : A + (int64_t)(ok ? k0 + k : 0) * g.lda + f_rbase + lane;
           rs_cp8(dst0 + lane * L::APITCH + k * 8, ok ? src : Ab, ok);
         }
       } else if (mode == 1) {
@@ -1146,6 +1147,7 @@ __global__ void __launch_bounds__(RS_WARPS * 32)
 }
 
 bool rowstream_eligible(const GemmArgs &g) {
+  if (g.a_rin && (g.a_rin % 32 || g.opA != QF_OP_T)) return false;
   return g.N >= 1 && g.N <= 16 && g.K >= 1 && g.K * (g.N <= 8 ? 8 : 16) <= 1024 && g.M >= 32;
 }
 
@@ -1323,7 +1325,13 @@ int validate(const GemmArgs &g) {
   QF_REQUIRE(g.opA == QF_OP_N || g.opA == QF_OP_T, "gemm: opA must be N or T");
   QF_REQUIRE(g.opB == QF_OP_N || g.opB == QF_OP_T, "gemm: opB must be N or T");
   QF_REQUIRE(g.ldc >= std::max<int64_t>(1, g.N), "gemm: ldc < N");
-  QF_REQUIRE(g.lda >= std::max<int64_t>(1, g.opA == QF_OP_N ? g.K : g.M), "gemm: lda too small");
+  if (g.a_rin) {
+    QF_REQUIRE(g.opA == QF_OP_T && g.a_rin >= 1 && g.lda >= g.a_rin &&
+                   g.a_rstride >= g.lda * std::max<int64_t>(g.K, 1),
+               "gemm: row blocks need opA T, lda >= rows per block, block stride >= lda*K");
+  } else {
+    QF_REQUIRE(g.lda >= std::max<int64_t>(1, g.opA == QF_OP_N ? g.K : g.M), "gemm: lda too small");
+  }
   QF_REQUIRE(g.ldb >= std::max<int64_t>(1, g.opB == QF_OP_N ? g.N : g.K), "gemm: ldb too small");
   return QF_OK;
 }
@@ -1615,6 +1623,30 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
   int st = qf::validate(g);
   if (st != QF_OK) return st;
   return qf::gemm_tc3(g, qf::as_stream(stream));
+}
+
+int qf_cgemm_c64_rowblocks(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
+                           const void *A, int64_t rows_per_block, int64_t block_stride,
+                           int64_t lda, int64_t strideA, const void *B, int64_t ldb,
+                           int64_t strideB, int opB, void *C, int64_t ldc, int64_t strideC,
+                           float alpha_re, float alpha_im, float beta_re, float beta_im,
+                           void *stream) {
+  qf::MmaScope mma_scope(mode);
+  qf::GemmArgs g{batch, M, N, K, A, lda, strideA, QF_OP_T, B, ldb, strideB, opB, C, ldc, strideC,
+                 alpha_re, alpha_im, beta_re, beta_im};
+  g.a_rin = rows_per_block;
+  g.a_rstride = block_stride;
+  QF_REQUIRE(rows_per_block >= 1, "gemm_rowblocks: rows_per_block must be >= 1");
+  int st = qf::validate(g);
+  if (st != QF_OK) return st;
+  if (batch == 0 || M == 0 || N == 0) return QF_OK;
+  if (!(N <= 16 && K >= 1 && K * N <= 4096)) {
+    qf::set_error("gemm_rowblocks: needs N <= 16 and K*N <= 4096 (CUDA-core row engines)");
+    return QF_ERR_UNSUPPORTED;
+  }
+  cudaStream_t s = qf::as_stream(stream);
+  if (qf::g_small_engine != 2 && qf::rowstream_eligible(g) && K <= 8) return qf::gemm_rowstream(g, s);
+  return qf::gemm_rowblock<float>(g, s);
 }
 
 int qf_rowmma(int enabled) {

@@ -816,6 +816,29 @@ def _zero_offsets(n: int, device):
     return z
 
 
+def _row_blocks(big: Tensor, a_free, k_order, n: int) -> Optional[int]:
+    """Rows per block when `big` is laid out [outer free][summed][inner free]
+    with the free labels in memory order (so A(r, k) = (r / rin) * rin*K +
+    r % rin + k*rin, qf_cgemm_c64_rowblocks), the summed labels contiguous
+    and in the GEMM's k order, and the shape within the row engines' range."""
+    if big.buf.dtype != torch.complex64 or not k_order or n > 16:
+        return None
+    labels = list(big.labels)
+    ks = labels.index(k_order[0])
+    if labels[ks:ks + len(k_order)] != list(k_order):
+        return None
+    if labels[:ks] + labels[ks + len(k_order):] != list(a_free):
+        return None
+    inner = labels[ks + len(k_order):]
+    if not inner:
+        return None
+    rin = math.prod(big.dim_of(l) for l in inner)
+    k = math.prod(big.dim_of(l) for l in k_order)
+    if rin % 32 or k * n > 4096:
+        return None
+    return rin
+
+
 def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Tensor]:
     """Both operands with open outputs, no batch axis yet: the smaller
     operand's open outputs become the GEMM batch (its slices side by side,
@@ -863,6 +886,16 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Te
                 ctypes.c_void_p(coff.data_ptr()), ctypes.c_void_p(B.data.data_ptr()), max(n, 1),
                 k * n, _lib.OP_N, ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n,
                 1.0, 0.0, 0.0, 0.0, stream_handle())
+    elif _row_blocks(big, a_free, k_order, n) is not None:
+        # [outer rows][k][inner rows]: read in place in row blocks, no permute
+        rin = _row_blocks(big, a_free, k_order, n)
+        with _timed("gemm", 8 * nbat * m * n * k, 8 * (m * k + nbat * (k * n + m * n)),
+                    detail + " R" if _timer else ""):
+            st = lib.qf_cgemm_c64_rowblocks(
+                _gemm_mode, nbat, m, n, k, ctypes.c_void_p(big.data.data_ptr()), rin, rin * k, rin,
+                0, ctypes.c_void_p(B.data.data_ptr()), max(n, 1), k * n, _lib.OP_N,
+                ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
+                stream_handle())
     else:
         # (too many rows for offset tables) one permute, then batch stride 0
         A = big.transpose_to(tuple(a_free + k_order))

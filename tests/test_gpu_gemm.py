@@ -501,3 +501,48 @@ def test_skinny_many_rows(shape, ops):
     """M*N <= 256 outputs, long K, row-contiguous A: warp-per-row split-K."""
     assert _gemm(*shape, *ops, np.complex64) < 1e-5
     assert _gemm(*shape, *ops, np.complex64, alpha=0.5 + 1j, beta=-0.25) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(2, 8192, 8, 8, 64), (1, 4096, 3, 5, 32), (3, 2048, 16, 16, 256),
+                                   (2, 96, 8, 64, 32), (1, 1000, 8, 8, 40)])
+def test_rowblocks_gemm(shape):
+    """A read in row blocks ([outer rows][k][inner rows], qf_cgemm_c64_rowblocks)."""
+    import ctypes
+    nb, M, N, K, rin = shape
+    if M % rin:
+        M = (M // rin + 1) * rin
+    rng = np.random.default_rng(7)
+    A = _rand(rng, (M // rin, K, rin), np.complex64)          # broadcast over the batch
+    B = _rand(rng, (nb, K, N), np.complex64)
+    dA, dB = torch.from_numpy(A.reshape(-1)).cuda(), torch.from_numpy(B.reshape(-1)).cuda()
+    dC = torch.empty(nb * M * N, dtype=torch.complex64, device="cuda")
+    lib = _lib.load()
+    st = lib.qf_cgemm_c64_rowblocks(0, nb, M, N, K, ctypes.c_void_p(dA.data_ptr()), rin, rin * K,
+                                    rin, 0, ctypes.c_void_p(dB.data_ptr()), N, K * N, 0,
+                                    ctypes.c_void_p(dC.data_ptr()), N, M * N, 1.0, 0.0, 0.0, 0.0,
+                                    tc.stream_handle())
+    _lib.check(st, "rowblocks")
+    a2 = A.transpose(0, 2, 1).reshape(M, K).astype(np.complex128)    # rows = (outer, inner)
+    want = np.einsum("mk,bkn->bmn", a2, B.astype(np.complex128))
+    got = dC.cpu().numpy().reshape(nb, M, N)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
+
+
+def test_open_step_with_too_many_rows_reads_row_blocks():
+    """_contract_open beyond the offset-table limit: [outer][k][inner] big
+    operand read in place (no permute) -- same result as the permuted path."""
+    rng = np.random.default_rng(11)
+    big = tc.Tensor(["o0", "a", "b", "c", "k", "d", "e"],
+                    _rand(rng, (2, 64, 64, 16, 8, 8, 8), np.complex64))   # 2^23 rows x k 8
+    small = tc.Tensor(["out1", "k", "n"], _rand(rng, (2, 8, 8), np.complex64))
+    bits = torch.zeros((2, 4), dtype=torch.int32, device="cuda")
+    late = tc.LateBits(bits, {"o0": 0, "out1": 1}, limit=2 ** 20)
+    with tc.KernelTimer() as kt:
+        got = tc._contract_open(big, small, late)
+    kinds = kt.summary()
+    assert "permute" not in kinds
+    want = np.einsum("oabckde,pkn->poabcden", big.array, small.array)
+    w = np.moveaxis(want, 0, 0)   # labels: out1, o0, a, b, c, d, e, n
+    assert got.labels == ("out1", "o0", "a", "b", "c", "d", "e", "n")
+    g = got.array
+    assert np.linalg.norm(g - w) / np.linalg.norm(w) < 1e-5
