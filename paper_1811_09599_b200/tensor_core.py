@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -873,6 +874,8 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Te
     out = device_buffer(nbat * m * n, big.data.dtype, big.data.device)
     lib = _lib.load()
     detail = f"b{nbat} m{m} n{n} k{k} O" if _timer else ""
+    if _timer is not None and os.environ.get("QF_DEBUG_LAYOUT"):
+        detail += f" BIG{list(zip(big.labels, big.dims))} free{a_free} k{k_order} SMALL{list(zip(small.labels, small.dims))} so{so} sfree{s_free}"
     if m <= 2 ** 22 and list(big.labels) != a_free + k_order:
         # big operand read in place through offset tables, broadcast over the batch
         roff, coff, rows_unit = _gather_tables(big.dims, big.labels, a_free, k_order,
@@ -1051,6 +1054,8 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=(),
         flags |= _lib.GATHER_ROWS_UNIT if ru else 0
     tag = ("G" if roff is not None else "NT"[opA]) + ("S" if ao else "") + \
         ("V" if a._data is None else "") + "," + ("S" if bo else "B" if b_bat else "0")
+    if _timer is not None and os.environ.get("QF_DEBUG_LAYOUT"):
+        tag += f" A{list(zip(a.labels, a.dims))} free{a_free} k{k_order} ao{ao} B{list(zip(b.labels, b.dims))} bfree{b_free} bo{bo}"
     vp = ctypes.c_void_p
 
     def launch(trans: bool):

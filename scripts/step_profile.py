@@ -27,6 +27,9 @@ for kind, a, b, flops, nbytes, *rest in kt.records:
     key = f"{kind} {rest[0]}  [{rest[1] if len(rest) > 1 else ''}]"
     d = s.setdefault(key, {"launches": 0, "ms": 0.0, "flops": 0, "bytes": 0})
     d["launches"] += 1; d["ms"] += a.elapsed_time(b); d["flops"] += flops; d["bytes"] += nbytes
+if os.environ.get("QF_ORDER"):
+    for kind, a, b, flops, nbytes, *rest in kt.records:
+        print(f"ORDER {a.elapsed_time(b):7.3f} ms {kind} {rest[0]} [{rest[1] if len(rest) > 1 else ''}]")
 tot = sum(d["ms"] for d in s.values())
 print(f"mode={mode} batch={nb} total kernel ms {tot:.2f}")
 for k, d in sorted(s.items(), key=lambda x: -x[1]["ms"])[:40]:
