@@ -633,7 +633,8 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--shard", choices=["bitstrings", "slices"], default="bitstrings")
     ap.add_argument("--gemm", choices=["auto", "ffma", "tc3"], default=None)
-    ap.add_argument("--cpu-sample", type=int, default=64)
+    ap.add_argument("--cpu-sample", type=int, default=1024,
+                    help="bit-strings timed on the host cores (default: the whole config-2 step, ~2 s wall on 16 cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["config2", "config1", "permute", "config4", "config5"],
                     default="config2",
