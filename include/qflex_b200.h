@@ -178,6 +178,21 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
                     float beta_im, void *stream);
 
 /*
+ * qf_cgemm_c64_ex with B slice count: when every b_boff[b] is a whole
+ * [K][N] slice (a multiple of K*N) of a B buffer holding b_nslice slices,
+ * the TMA-fed tensor-core kernel reads B by slice coordinate (the per-entry
+ * site-tensor slices of the batched amplitude walk).  b_nslice = 0: as
+ * qf_cgemm_c64_ex.  Replaces the same contract() call as qf_cgemm_c64_ex
+ * (rq/tensor_core.py:391-419 with the fixes of rq/network_builder.py:134-149).
+ */
+int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                     int64_t lda, int64_t strideA, int opA, const int64_t *a_boff,
+                     const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
+                     int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice, void *C,
+                     int64_t ldc, int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                     float beta_im, void *stream);
+
+/*
  * Strided-view A for the TMA-fed tensor-core kernel (no offset tables): the
  * big operand of a contraction whose shared labels are its innermost index
  * (kin, contiguous, kin % 8 == 0) and at most one more index (kout), with its

@@ -1273,6 +1273,82 @@ __global__ void __launch_bounds__(GV_THREADS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// batched dot products (M = N = 1, many entries): the path sums of the
+// amplitude walk -- C[b] = alpha * <A[b], B[b]> over K contiguous complex
+// entries.  A warp per entry, four 16-byte loads of A and of B in flight per
+// lane, one warp reduction, no workspace pass (the split-K skinny kernel +
+// its reduction ran 8192 x 4096 at 3.8 TB/s).
+
+constexpr int DOT_THREADS = 256;
+
+__global__ void __launch_bounds__(DOT_THREADS)
+    cdot_batched_kernel(const __grid_constant__ GemmArgs g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * (DOT_THREADS / 32) + (threadIdx.x >> 5);
+  if (b >= g.batch) return;
+  const float4 *A = reinterpret_cast<const float4 *>(reinterpret_cast<const float2 *>(g.A) + a_batch_off(g, b));
+  const float4 *B = reinterpret_cast<const float4 *>(reinterpret_cast<const float2 *>(g.B) + b_batch_off(g, b));
+  const int64_t n2 = g.K / 2;  // complex pairs
+  float re0 = 0.f, im0 = 0.f, re1 = 0.f, im1 = 0.f;
+  int64_t i = lane;
+  for (; i + 96 < n2; i += 128) {
+    float4 a[4], w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a[j] = __ldcs(A + i + 32 * j);
+      w[j] = __ldg(B + i + 32 * j);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      re0 = fmaf(a[j].x, w[j].x, re0); re0 = fmaf(-a[j].y, w[j].y, re0);
+      im0 = fmaf(a[j].x, w[j].y, im0); im0 = fmaf(a[j].y, w[j].x, im0);
+      re1 = fmaf(a[j].z, w[j].z, re1); re1 = fmaf(-a[j].w, w[j].w, re1);
+      im1 = fmaf(a[j].z, w[j].w, im1); im1 = fmaf(a[j].w, w[j].z, im1);
+    }
+  }
+  for (; i < n2; i += 32) {
+    const float4 a = __ldcs(A + i), w = __ldg(B + i);
+    re0 = fmaf(a.x, w.x, re0); re0 = fmaf(-a.y, w.y, re0);
+    im0 = fmaf(a.x, w.y, im0); im0 = fmaf(a.y, w.x, im0);
+    re1 = fmaf(a.z, w.z, re1); re1 = fmaf(-a.w, w.w, re1);
+    im1 = fmaf(a.z, w.w, im1); im1 = fmaf(a.w, w.z, im1);
+  }
+  float re = re0 + re1, im = im0 + im1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  if (lane == 0) {
+    float2 *C = reinterpret_cast<float2 *>(g.C) + b * g.sC;
+    const float ar = (float)g.ar, ai = (float)g.ai, br = (float)g.br, bi = (float)g.bi;
+    float2 o = make_float2(ar * re - ai * im, ar * im + ai * re);
+    if (br != 0.f || bi != 0.f) {
+      const float2 c = *C;
+      o.x += br * c.x - bi * c.y;
+      o.y += br * c.y + bi * c.x;
+    }
+    *C = o;
+  }
+}
+
+// both operands contiguous, 16-byte aligned entries, enough entries to
+// fill the machine with a warp each
+bool dot_eligible(const GemmArgs &g) {
+  if (g.M != 1 || g.N != 1 || g.K < 64 || g.K % 2 || g.a_roff || g.opA != QF_OP_N) return false;
+  if (!(g.opB == QF_OP_T || g.ldb == 1)) return false;   // B[b] = K contiguous entries
+  if (g.batch < 4 * (int64_t)sm_count()) return false;
+  if (g.sA % 2 || g.sB % 2) return false;                // entry bases even (or even b_boff)
+  return ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) == 0;
+}
+
+int gemm_dot(const GemmArgs &g, cudaStream_t s) {
+  const int64_t grid = (g.batch + DOT_THREADS / 32 - 1) / (DOT_THREADS / 32);
+  cdot_batched_kernel<<<(unsigned)grid, DOT_THREADS, 0, s>>>(g);
+  return check_launch("cdot_batched");
+}
+
 bool gemv_eligible(const GemmArgs &g) {
   return g.N <= 4 && (g.opA == QF_OP_N || g.a_roff) && g.K >= 32 && g.M >= 32;
 }
@@ -1406,6 +1482,9 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
     return check_launch("cgemm_scale");
   }
   int64_t P = g.M * g.N;
+  if constexpr (sizeof(R) == 4) {
+    if (dot_eligible(g)) return gemm_dot(g, s);
+  }
   if (P <= 256 && g.K >= 256) {
     int Ppad = 1;
     while (Ppad < P) Ppad <<= 1;
@@ -1558,7 +1637,20 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
                     int64_t strideB, int opB, const int64_t *b_boff, void *C, int64_t ldc,
                     int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                     float beta_im, void *stream) {
+  return qf_cgemm_c64_ex2(mode, batch, M, N, K, A, lda, strideA, opA, a_boff, a_roff, a_coff, B,
+                          ldb, strideB, opB, b_boff, 0, C, ldc, strideC, alpha_re, alpha_im,
+                          beta_re, beta_im, stream);
+}
+
+int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                     int64_t lda, int64_t strideA, int opA, const int64_t *a_boff,
+                     const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
+                     int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice, void *C,
+                     int64_t ldc, int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                     float beta_im, void *stream) {
   qf::MmaScope mma_scope(mode);
+  QF_REQUIRE(b_nslice >= 0 && (b_nslice == 0 || b_boff != nullptr),
+             "gemm_ex2: b_nslice needs b_boff");
   QF_REQUIRE((a_roff != nullptr) == (a_coff != nullptr), "gemm_ex: a_roff/a_coff must pair");
   const bool rows_unit = (mode & QF_GATHER_ROWS_UNIT) != 0;
   const bool a_even = (mode & QF_BOFF_EVEN) != 0, b_even = (mode & QF_BBOFF_EVEN) != 0;
@@ -1574,6 +1666,9 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
   qf::GemmArgs g{batch, M, N, K, A, lda, strideA, opA, B, ldb, strideB, opB, C, ldc, strideC,
                  alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
                  rows_unit && a_roff != nullptr, a_boff, b_boff};
+  // b_boff values are whole [K][N] slices of a buffer of b_nslice of them:
+  // lets the TMA-fed kernel address B by slice coordinate
+  g.b_nslice = b_nslice;
   g.c_trans = c_trans;
   if (c_trans) {
     QF_REQUIRE(ldc >= std::max<int64_t>(1, M), "gemm_ex: transposed C needs ldc >= M");

@@ -1083,18 +1083,20 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=(),
     if _timer is not None and os.environ.get("QF_DEBUG_LAYOUT"):
         tag += f" A{list(zip(a.labels, a.dims))} free{a_free} k{k_order} ao{ao} B{list(zip(b.labels, b.dims))} bfree{b_free} bo{bo}"
     vp = ctypes.c_void_p
+    # site-tensor slices picked per entry are whole [K][N] blocks of B
+    b_nslice = B.size // max(k * n, 1) if bo else 0
 
     def launch(trans: bool):
         with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
                     f"b{nb} m{m} n{n} k{k} {tag}{'^T' if trans else ''}" if _timer else ""):
-            return lib.qf_cgemm_c64_ex(
+            return lib.qf_cgemm_c64_ex2(
                 _gemm_mode | flags | (_lib.C_TRANS if trans else 0), nb, m, n, k,
                 vp(a_buf.data_ptr() + 8 * a_off), lda, entry_a, opA,
                 vp(a_boff.data_ptr() if a_boff is not None else 0),
                 vp(roff.data_ptr() if roff is not None else 0),
                 vp(coff.data_ptr() if coff is not None else 0),
                 vp(B.data.data_ptr()), ldb, sB, opB,
-                vp(b_boff.data_ptr() if b_boff is not None else 0),
+                vp(b_boff.data_ptr() if b_boff is not None else 0), b_nslice,
                 vp(out.data_ptr()), max(m if trans else n, 1), m * n, 1.0, 0.0, 0.0, 0.0,
                 stream_handle())
 

@@ -546,3 +546,14 @@ def test_open_step_with_too_many_rows_reads_row_blocks():
     assert got.labels == ("out1", "o0", "a", "b", "c", "d", "e", "n")
     g = got.array
     assert np.linalg.norm(g - w) / np.linalg.norm(w) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [(1024, 1, 1, 4096), (700, 1, 1, 64), (600, 1, 1, 1000),
+                                   (2048, 1, 1, 130), (600, 1, 1, 999)])
+@pytest.mark.parametrize("ops", [(0, 0), (0, 1)])
+@pytest.mark.parametrize("ab", [(1.0, 0.0), (0.5 - 1j, 0.25 + 0.5j)])
+def test_batched_dot_products(shape, ops, ab):
+    """M = N = 1 with many entries: the warp-per-entry dot kernel (odd K and
+    short K fall back to the split-K kernel) against float64."""
+    assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_FFMA, alpha=ab[0], beta=ab[1]) < 1e-5
+    assert _gemm(*shape, *ops, np.complex64, alpha=ab[0], beta=ab[1]) < 1e-5
