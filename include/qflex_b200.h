@@ -273,6 +273,25 @@ int qf_tc3_set_variant(int variant);
 int qf_small_engine(int engine);
 
 /*
+ * Transposed strided view of A for the TMA-fed tensor-core kernel: rows are
+ * the innermost axis.  Per entry, row r = rb*rows_a + ra with ra contiguous
+ * (rows_a rows) and rb at element stride s_rows_b; k = ko*kin + ki with ki at
+ * stride s_kin and ko at s_kout -- the four runs in any memory order, e.g.
+ * [ko][rb][ki][ra].  mode may carry QF_C_TRANS (C(b, m, n) at
+ * C + b*strideC + n*ldc + m).  Any N (tiles of 64 columns); K in [32, 128],
+ * kin % 8 == 0.  Serves the same contract() as qf_cgemm_c64_ex
+ * (rq/tensor_core.py:391-419) when the big operand's innermost labels are
+ * free: the permute before the GEMM (rq/tensor_core.py:410-416) is folded
+ * into the TMA box.
+ */
+int qf_cgemm_c64_tview(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                       int64_t strideA, int64_t rows_a, int64_t rows_b, int64_t s_rows_b,
+                       int64_t kin, int64_t s_kin, int64_t kout, int64_t s_kout, const void *B,
+                       int64_t ldb, int64_t strideB, int opB, const int64_t *b_boff,
+                       int64_t b_nslice, void *C, int64_t ldc, int64_t strideC, float alpha_re,
+                       float alpha_im, float beta_re, float beta_im, void *stream);
+
+/*
  * Batched GEMM whose A is read in ROW BLOCKS (complex64, N <= 16, K*N <= 4096;
  * CUDA-core row engines): A(b, r, k) = A + b*strideA + (r / rows_per_block) *
  * block_stride + r % rows_per_block + k*lda, i.e. a big operand laid out

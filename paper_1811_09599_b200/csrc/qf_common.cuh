@@ -59,8 +59,13 @@ struct GemmArgs {
   // unused): k = ko*v_kin + ki with ki innermost and contiguous, row
   // r = rb*v_ra + ra; v_s* are element strides of ra, ko and rb
   int64_t v_kin = 0, v_ra = 0, v_sra = 0, v_kout = 0, v_skout = 0, v_rb = 0, v_srb = 0;
+  // v_t: the TRANSPOSED view (opA = T): rows innermost -- row r = rb*v_ra + ra
+  // with ra contiguous (v_ra rows), rb at stride v_srb; k = ko*v_kin + ki, ki
+  // at stride v_ski, ko at v_skout (any order of the four runs in memory)
+  bool v_t = false;
+  int64_t v_ski = 0;
   // C stored transposed per entry: C(b, m, n) at C + b*sC + n*ldc + m (row-block
-  // and row-stream engines only)
+  // and row-stream engines, and the TMA kernel on a transposed view)
   bool c_trans = false;
   // opA = T in row blocks (row-block / row-stream engines only): row r at
   // (r / a_rin) * a_rstride + r % a_rin, k at k * lda -- a big operand laid

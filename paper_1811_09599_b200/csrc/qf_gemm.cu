@@ -1720,6 +1720,39 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
   return qf::gemm_tc3(g, qf::as_stream(stream));
 }
 
+int qf_cgemm_c64_tview(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                       int64_t strideA, int64_t rows_a, int64_t rows_b, int64_t s_rows_b,
+                       int64_t kin, int64_t s_kin, int64_t kout, int64_t s_kout, const void *B,
+                       int64_t ldb, int64_t strideB, int opB, const int64_t *b_boff,
+                       int64_t b_nslice, void *C, int64_t ldc, int64_t strideC, float alpha_re,
+                       float alpha_im, float beta_re, float beta_im, void *stream) {
+  const bool c_trans = (mode & QF_C_TRANS) != 0;
+  mode &= ~QF_C_TRANS;
+  QF_REQUIRE(kin >= 1 && rows_a >= 1 && kout >= 1 && rows_b >= 1, "gemm_tview: empty run");
+  QF_REQUIRE(M == rows_a * rows_b && K == kin * kout, "gemm_tview: runs do not match M/K");
+  QF_REQUIRE(mode == QF_GEMM_AUTO || mode == QF_GEMM_TC3, "gemm_tview: tensor-core modes only");
+  QF_REQUIRE(!b_boff || b_nslice > 0, "gemm_tview: b_boff needs b_nslice");
+  QF_REQUIRE(ldc >= std::max<int64_t>(1, c_trans ? M : N), "gemm_tview: ldc too small");
+  qf::GemmArgs g{batch, M, N, K, A, std::max<int64_t>(M, 1), strideA, QF_OP_T, B, ldb,
+                 b_boff ? 2 : strideB, opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im};
+  g.b_boff = b_boff;
+  g.b_nslice = b_nslice;
+  g.v_t = true;
+  g.v_kin = kin;
+  g.v_ra = rows_a;
+  g.v_kout = kout;
+  g.v_skout = s_kout;
+  g.v_rb = rows_b;
+  g.v_srb = s_rows_b;
+  g.v_ski = s_kin;
+  g.c_trans = c_trans;
+  if (!c_trans) {
+    int st = qf::validate(g);
+    if (st != QF_OK) return st;
+  }
+  return qf::gemm_tc3(g, qf::as_stream(stream));
+}
+
 int qf_cgemm_c64_rowblocks(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
                            const void *A, int64_t rows_per_block, int64_t block_stride,
                            int64_t lda, int64_t strideA, const void *B, int64_t ldb,

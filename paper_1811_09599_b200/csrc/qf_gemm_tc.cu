@@ -1832,6 +1832,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         if (g.v_kin) {
           v_rb = (int32_t)(m0 / (int32_t)g.v_ra);
           v_ra = g.v_ra >= BM ? m0 - v_rb * (int32_t)g.v_ra : 0;
+          if (g.v_t) v_ra *= 2;  // float coordinate of the contiguous row run
         }
         for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
           const uint32_t slot = f & (RAW - 1);
@@ -1841,7 +1842,18 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                        : "memory");
           const int32_t k0 = (int32_t)(kb * KB);
-          if (g.v_kin) {
+          if (g.v_t) {
+            // transposed view: {2 ra, rb, ki, ko, b}; the box is [8 k][128 rows]
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(rawa + slot * L::RAWA_SLOT),
+                "l"(&tmA), "r"(v_ra), "r"(v_rb), "r"(v_ki * KB), "r"(v_ko), "r"(b), "r"(bar)
+                : "memory");
+            if (++v_ki == v_kbi) {
+              v_ki = 0;
+              ++v_ko;
+            }
+          } else if (g.v_kin) {
             // A view: {2 ki, ra, ko, rb, b}; the box spans 128 rows of (ra, rb)
             asm volatile(
                 "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
@@ -2081,8 +2093,28 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[pb]))
                          : "memory");
         }
-        stage_store_chunk<CH, L::EPI_PITCH>(stg, vr, vi, cw + ch * CH, g.ldc, g.M - m0,
-                                            ntile - ch * CH, ar, ai, br, bi, use_beta, vec, lane);
+        if (g.c_trans) {
+          // transposed C: column n of these 32 rows is one 256-byte run
+          const int64_t m = m0 + lane;
+          float2 *ct = Cb + (int64_t)ec.bidx * g.sC + m;
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const int64_t n = (int64_t)ec.nt * BN + ch * CH + c;
+            if (ch * CH + c < ntile && m < g.M) {
+              const float xr = __uint_as_float(vr[c]), xi = __uint_as_float(vi[c]);
+              float2 o = make_float2(ar * xr - ai * xi, ar * xi + ai * xr);
+              if (use_beta) {
+                const float2 cv = ct[n * g.ldc];
+                o.x += br * cv.x - bi * cv.y;
+                o.y += br * cv.y + bi * cv.x;
+              }
+              ct[n * g.ldc] = o;
+            }
+          }
+        } else {
+          stage_store_chunk<CH, L::EPI_PITCH>(stg, vr, vi, cw + ch * CH, g.ldc, g.M - m0,
+                                              ntile - ch * CH, ar, ai, br, bi, use_beta, vec, lane);
+        }
       }
     }
   } else if constexpr (NPW > 0) {
@@ -2565,7 +2597,7 @@ static bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1,
 
 // 5-D float tensor map of an A view (dims innermost first, byte strides)
 static bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5],
-                       const uint64_t (&strides)[4], const uint32_t (&box)[5]) {
+                       const uint64_t (&strides)[4], const uint32_t (&box)[5], bool swz64 = true) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -2582,7 +2614,8 @@ static bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5
   for (int i = 0; i < 5; ++i) d[i] = dims[i], bx[i] = box[i];
   for (int i = 0; i < 4; ++i) st[i] = strides[i];
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(ptr), d, st, bx, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                swz64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -2592,10 +2625,15 @@ bool tma_ok(const GemmArgs &g) {
   const bool a_ok = !g.a_roff && !g.a_boff && g.sA > 0 && g.sA % 2 == 0 && g.lda % 2 == 0;
   const bool b_ok = g.b_boff ? (g.b_nslice > 0 && (g.K * g.N) % 2 == 0)
                              : (g.sB > 0 && g.sB % 2 == 0);
-  const bool v_ok = !g.v_kin || (g.v_kin % KB == 0 && g.v_sra % 2 == 0 && g.v_skout % 2 == 0 &&
-                                 g.v_srb % 2 == 0 &&
-                                 (g.v_ra >= BM ? g.v_ra % BM == 0 : BM % g.v_ra == 0) &&
-                                 g.opA == QF_OP_N);
+  const bool v_ok = !g.v_kin ||
+                    (g.v_t ? (g.v_kin % KB == 0 && g.v_ski % 2 == 0 && g.v_skout % 2 == 0 &&
+                              g.v_srb % 2 == 0 && g.v_ra % 2 == 0 &&
+                              (g.v_ra >= BM ? g.v_ra % BM == 0 : BM % g.v_ra == 0) &&
+                              g.opA == QF_OP_T)
+                           : (g.v_kin % KB == 0 && g.v_sra % 2 == 0 && g.v_skout % 2 == 0 &&
+                              g.v_srb % 2 == 0 &&
+                              (g.v_ra >= BM ? g.v_ra % BM == 0 : BM % g.v_ra == 0) &&
+                              g.opA == QF_OP_N));
   return a_ok && b_ok && v_ok && g.ldb % 2 == 0 &&
          (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 && (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 &&
          g.batch < ((int64_t)1 << 31);
@@ -2609,7 +2647,18 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   if constexpr (TMA) {
     const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
     bool okA;
-    if (g.v_kin) {
+    if (g.v_t) {
+      // transposed view: dims {2 ra, rb, ki, ko, b} (strides need not be
+      // monotonic), box {2 min(ra, 128), 128 / min(ra, 128), 8, 1, 1} lands as
+      // the dense [8 k][128 rows] tile of the plain opA = T path
+      const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
+      const uint64_t dims[5] = {(uint64_t)(2 * g.v_ra), (uint64_t)g.v_rb, (uint64_t)g.v_kin,
+                                (uint64_t)g.v_kout, nb};
+      const uint64_t strides[4] = {(uint64_t)g.v_srb * 8, (uint64_t)g.v_ski * 8,
+                                   (uint64_t)g.v_skout * 8, (uint64_t)std::max<int64_t>(g.sA, 1) * 8};
+      const uint32_t box[5] = {2 * bra, (uint32_t)(BM / bra), (uint32_t)KB, 1, 1};
+      okA = make_tmap5(&tmA, g.A, dims, strides, box, false);
+    } else if (g.v_kin) {
       const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
       const uint64_t dims[5] = {(uint64_t)(2 * g.v_kin), (uint64_t)g.v_ra, (uint64_t)g.v_kout,
                                 (uint64_t)g.v_rb, nb};
@@ -3421,13 +3470,14 @@ static int g_tc3_variant = 0;
 bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
 
 // TMA-fed short-K runs: RAW k-blocks of A (8 KiB each) in flight per CTA.
-// Plain operands stream best 8 deep (1024 x 4096x64x64: 0.75 vs 0.85 ms,
-// 0.89 of HBM); strided views, whose k-blocks sit far apart, 4 deep (0.84 vs
-// 0.92 ms; scripts/view_bench2.py).  Variants 21/22 pin 4/8 for A/B runs.
+// 8 deep for plain operands and strided views alike: the config-2 view GEMMs
+// 1024 x (4096 x 64 x 64) run 0.69 ms 8 deep vs 0.80-0.85 ms 4 deep (6.26 TB/s,
+// 0.97 of the measured HBM copy rate; an earlier 4-deep preference measured
+// before the transposed-store/view-order changes no longer holds).  Variants
+// 21/22 pin 4/8 for A/B runs.
 static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 21) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
   if (g_tc3_variant == 22) return tc::launch_short<8, 8, 8, 4, 64, 0, 1, true>(g, s);
-  if (g.v_kin) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
   return tc::launch_short<8, 8, 8, 4, 64, 0, 1, true>(g, s);
 }
 
@@ -3472,8 +3522,14 @@ bool tc3_eligible(const GemmArgs &g) {
 int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
   QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
+  if (g.c_trans && !g.v_t) {
+    set_error("tc3: transposed C only on a transposed A view");
+    return QF_ERR_UNSUPPORTED;
+  }
   if (g.v_kin) {  // A views are read by the TMA-fed short-K kernel only
-    if (!(g.K >= 32 && g.K <= 128 && g.N > 32 && tc::tma_ok(g))) {
+    // (a transposed view also serves narrow N: the 64-column tile computes
+    // zeros beyond N, the HBM-bound shape does not mind)
+    if (!(g.K >= 32 && g.K <= 128 && (g.N > 32 || g.v_t) && tc::tma_ok(g))) {
       set_error("tc3: A view (kin %lld, rows %lld x %lld) not TMA-describable for K=%lld N=%lld",
                 (long long)g.v_kin, (long long)g.v_ra, (long long)g.v_rb, (long long)g.K,
                 (long long)g.N);

@@ -556,6 +556,45 @@ def _a_view(labels, dims, a_free, k_order):
     return kin, rows_a, s_rows_a, kout, s_kout, rows_b, s_rows_b
 
 
+def _a_tview(labels, dims, a_free, k_order):
+    """The big operand's per-entry layout as a TRANSPOSED TMA view, or None:
+    its innermost label free, the free labels in at most two runs (the inner
+    one contiguous) and the summed labels in at most two runs, in any
+    interleaving -> (rows_a, rows_b, s_rows_b, kin, s_kin, kout, s_kout) in
+    elements (see qf_cgemm_c64_tview)."""
+    if not labels or not k_order or labels[-1] in k_order:
+        return None
+    ks = set(k_order)
+    if [l for l in labels if l not in ks] != list(a_free) or [l for l in labels if l in ks] != list(k_order):
+        return None
+    stride, acc = {}, 1
+    for l, d in zip(reversed(labels), reversed(dims)):
+        stride[l] = acc
+        acc *= d
+    dim = dict(zip(labels, dims))
+    runs = []                      # (summed?, [labels]) outermost first
+    for l in labels:
+        t = l in ks
+        if runs and runs[-1][0] == t:
+            runs[-1][1].append(l)
+        else:
+            runs.append((t, [l]))
+    free = [r for t, r in runs if not t]
+    summ = [r for t, r in runs if t]
+    if len(free) > 2 or len(summ) > 2:
+        return None
+    size = lambda r: math.prod(dim[l] for l in r)
+    rows_a = size(free[-1])
+    rows_b, s_rows_b = (size(free[0]), stride[free[0][-1]]) if len(free) == 2 else (1, acc)
+    kin, s_kin = size(summ[-1]), stride[summ[-1][-1]]
+    kout, s_kout = (size(summ[0]), stride[summ[0][-1]]) if len(summ) == 2 else (1, acc)
+    if kin % 8 or rows_a % 2 or not (rows_a % 128 == 0 if rows_a >= 128 else 128 % rows_a == 0):
+        return None
+    if any(x % 2 for x in (s_rows_b, s_kin, s_kout)):
+        return None
+    return rows_a, rows_b, s_rows_b, kin, s_kin, kout, s_kout
+
+
 def _gemm_view(nb, m, n, k, a_ptr, strideA, view, B, ldb, sB, opB, out, b_boff=None,
                b_nslice=0) -> bool:
     """Run the TMA-fed kernel on a view of the big operand; False if the
@@ -578,6 +617,14 @@ def _gemm_view(nb, m, n, k, a_ptr, strideA, view, B, ldb, sB, opB, out, b_boff=N
 
 
 _view_enabled = True
+_tview_enabled = True
+
+
+def set_tview(enabled: bool) -> bool:
+    """Enable/disable transposed (rows-innermost) TMA views; returns the previous value."""
+    global _tview_enabled
+    prev, _tview_enabled = _tview_enabled, bool(enabled)
+    return prev
 
 
 def set_view(enabled: bool) -> bool:
@@ -1063,6 +1110,25 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=(),
     if c_trans:
         labels_out = (lb,) + tuple(b_free) + tuple(a_free)
         dims = (nb,) + tuple(b.dim_of(l) for l in b_free) + tuple(a.dim_of(l) for l in a_free)
+    if roff == "tables" and a_bat and 32 <= k <= 128 and _view_enabled and _tview_enabled \
+            and _gemm_mode != _lib.GEMM_FFMA and entry_a % 2 == 0 and (bo or b_bat):
+        # rows innermost: a transposed TMA view (narrow N too; the kept cut
+        # stored transposed straight from the tensor-core epilogue)
+        tv = _a_tview(a.labels[1:], a.dims[1:], a_free, k_order)
+        if tv is not None:
+            ra, rb, srb, kin, ski, ko, sko = tv
+            with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
+                        f"b{nb} m{m} n{n} k{k} TV{'^T' if c_trans else ''}" if _timer else ""):
+                st = _lib.load().qf_cgemm_c64_tview(
+                    _gemm_mode | (_lib.C_TRANS if c_trans else 0), nb, m, n, k,
+                    ctypes.c_void_p(a_buf.data_ptr() + 8 * a_off), entry_a, ra, rb, srb, kin, ski,
+                    ko, sko, ctypes.c_void_p(B.data.data_ptr()), ldb, sB, opB,
+                    ctypes.c_void_p(b_boff.data_ptr() if b_boff is not None else 0),
+                    B.size // max(k * n, 1) if bo else 0, ctypes.c_void_p(out.data_ptr()),
+                    max(m if c_trans else n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+            if st != _lib.QF_ERR_UNSUPPORTED:
+                _lib.check(st, "gemm_tview")
+                return Tensor(labels_out, out, dims)
     if roff == "tables" and not c_trans:
         # batched big operand with scattered summed labels: a TMA-fed strided
         # view when it has one, else offset tables

@@ -557,3 +557,50 @@ def test_batched_dot_products(shape, ops, ab):
     short K fall back to the split-K kernel) against float64."""
     assert _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_FFMA, alpha=ab[0], beta=ab[1]) < 1e-5
     assert _gemm(*shape, *ops, np.complex64, alpha=ab[0], beta=ab[1]) < 1e-5
+
+
+@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("kept", [False, True])
+def test_transposed_tma_view(case, kept):
+    """Big operand whose innermost labels are FREE rows, summed labels in one
+    or two runs around them ([ko][rb][ki][ra] and friends): read as a
+    transposed 5-D TMA view (qf_cgemm_c64_tview; non-monotonic map strides),
+    with a per-bit-string site slice and, for a kept cut, the transposed
+    tensor-core epilogue -- equal to the engines without the view and to
+    float64 numpy."""
+    rng = np.random.default_rng(1100 + case + 10 * kept)
+    nb = [8, 64, 3, 16, 32, 5][case]
+    dims = {"p": 8, "q": 8, "r": 8, "s": 8, "t": 8, "u": 16, "x": 2}
+    a_labels = [["@b", "s", "p", "q", "r", "t", "u"],      # [ko][rb][ki][ra]
+                ["@b", "s", "p", "q", "t", "r"],           # [ko][rb][ki][ra]
+                ["@b", "p", "q", "s", "t", "r"],           # [rb][k][ra]
+                ["@b", "s", "t", "p", "q", "r"],           # [k][ra] (one row run)
+                ["@b", "p", "s", "q", "t", "r", "u"],      # [rb][ko][rb'] -> 3 free runs: no view
+                ["@b", "s", "p", "t", "x", "q"]][case]     # ra = 16 rows (x, q)
+    ks = ["s", "t"]
+    A = _rand(rng, [nb] + [dims[l] for l in a_labels[1:]], np.complex64)
+    S = _rand(rng, (8, 8, 8, 2), np.complex64)                     # s t c out0
+    bits = rng.integers(0, 2, size=(1, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"out0": 0})
+    ta, ts = tc.Tensor(a_labels, A), tc.Tensor(["s", "t", "c", "out0"], S)
+    lead = ("c",) if kept else ()
+    outs = []
+    for tv in (True, False):
+        prev = tc.set_tview(tv)
+        try:
+            with tc.KernelTimer() as kt:
+                o = tc.contract_late(ta, ts, late, lead=lead)
+            kinds = kt.summary(detail=True)
+        finally:
+            tc.set_tview(prev)
+        outs.append(o)
+        if tv and case not in (3, 4):   # 3: plain opA = T layout; 4: three free runs
+            assert any(" TV" in k for k in kinds), kinds
+    if kept:
+        assert outs[0].labels[:2] == ("@b", "c")
+    ref_t = outs[1].transpose_to(outs[0].labels).array
+    assert np.linalg.norm(outs[0].array - ref_t) / np.linalg.norm(ref_t) < 1e-5
+    want = tc.contract(ta, late.batch(ts))
+    w = want.transpose_to(outs[0].labels).array
+    assert np.linalg.norm(outs[0].array - w) / np.linalg.norm(w) < 1e-5
+    assert [l for l in a_labels if l in ks]   # summed labels present
