@@ -1611,8 +1611,9 @@ __device__ __forceinline__ void stage_store_chunk(uint8_t *stg, const uint32_t (
 template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN, int CK_ = 0, int NPW_ = 0,
           bool TMA_ = false>
 struct LayoutK {
-  static_assert(NPW_ == 0 || (NPW_ == (TMA_ ? 1 : 4) && NE == 4 && BN_ == 64),
-                "producer warps (4 cp.async or 1 TMA) need epilogue/promotion warps and 64-column tiles");
+  static_assert(NPW_ == 0 || (NPW_ == (TMA_ ? 1 : 4) && NE == 4 && (BN_ == 64 || (TMA_ && BN_ == 32))),
+                "producer warps (4 cp.async or 1 TMA) need epilogue/promotion warps and 64-column "
+                "tiles (32 with TMA)");
 
   static constexpr int NPW = NPW_;                   // producer (fetch) warps
   static constexpr int RPITCH = 80;                  // producer mode: raw row = 8 complex + 16 B
@@ -2166,9 +2167,9 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           }
           if (!breuse) {
             if (g.opB == QF_OP_N) {  // [8 k][64 n] dense
-              const float2 y0 = *reinterpret_cast<const float2 *>(rB + b_k * 512 + b_n * 8);
+              const float2 y0 = *reinterpret_cast<const float2 *>(rB + b_k * (BN * 8) + b_n * 8);
               if constexpr (BE == 2) {
-                const float2 y1 = *reinterpret_cast<const float2 *>(rB + (b_k + 1) * 512 + b_n * 8);
+                const float2 y1 = *reinterpret_cast<const float2 *>(rB + (b_k + 1) * (BN * 8) + b_n * 8);
                 bb4 = make_float4(y0.x, y0.y, y1.x, y1.y);
               } else {
                 bb2 = y0;
@@ -2675,8 +2676,8 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
     const uint64_t nbs = g.b_boff ? (uint64_t)g.b_nslice : nb;
     const int64_t sbs = g.b_boff ? g.K * g.N : std::max<int64_t>(g.sB, 1);
     const bool okB = g.opB == QF_OP_N
-                         ? make_tmap(&tmB, g.B, 2 * g.N, g.K, nbs, g.ldb * 8, sbs * 8, 128, 8, false)
-                         : make_tmap(&tmB, g.B, 2 * g.K, g.N, nbs, g.ldb * 8, sbs * 8, 16, 64, true);
+                         ? make_tmap(&tmB, g.B, 2 * g.N, g.K, nbs, g.ldb * 8, sbs * 8, 2 * BN, 8, false)
+                         : make_tmap(&tmB, g.B, 2 * g.K, g.N, nbs, g.ldb * 8, sbs * 8, 16, BN, true);
     if (!okA || !okB) {
       set_error("tc3k: cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld)", (long long)g.M,
                 (long long)g.N, (long long)g.K);
@@ -3478,6 +3479,11 @@ bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
 static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant == 21) return tc::launch_short<8, 4, 8, 4, 64, 0, 1, true>(g, s);
   if (g_tc3_variant == 22) return tc::launch_short<8, 8, 8, 4, 64, 0, 1, true>(g, s);
+  // narrow outputs (a transposed view with N <= 32): 32-column tiles halve
+  // the padded MMA work, which otherwise paces the HBM-bound tile
+  if (g_tc3_variant == 24 && g.N <= 32) return tc::launch_short<8, 8, 16, 4, 32, 0, 1, true>(g, s);
+  if (g_tc3_variant == 25) return tc::launch_short<8, 8, 16, 4, 64, 0, 1, true>(g, s);
+  if (g.N <= 32 && g_tc3_variant != 23) return tc::launch_short<8, 8, 8, 4, 32, 0, 1, true>(g, s);
   return tc::launch_short<8, 8, 8, 4, 64, 0, 1, true>(g, s);
 }
 
