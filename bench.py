@@ -209,11 +209,13 @@ class ClockSampler:
 # the GPU arm
 
 
-def measured_traffic(workload: str, kernel: str, algorithmic_per_launch: float):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed
-    ncu capture of one step (profiles/traffic_<workload>.json, made by
-    scripts/ncu_summary.py traffic), with the algorithmic bytes beside it;
-    None when no capture of this workload/kernel is committed."""
+def measured_traffic(workload: str, kernel: str, algorithmic_per_step: float, launches: int):
+    """DRAM bytes (read + write) of `kernel` over one step from the committed
+    ncu capture (profiles/traffic_<workload>.json, made by
+    scripts/make_traffic_json.py), beside the algorithmic bytes of the same
+    step; per launch = per step / the launches this bench times (a kernel
+    timed as one record may be several ncu launches).  None when no capture
+    of this workload/kernel is committed."""
     path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     if not os.path.exists(path):
         return None
@@ -221,11 +223,12 @@ def measured_traffic(workload: str, kernel: str, algorithmic_per_launch: float):
         rec = json.load(fh).get("kernels", {}).get(kernel)
     if rec is None:
         return None
-    return {"dram_bytes_per_launch": rec["dram_bytes_per_launch"],
-            "algorithmic_bytes_per_launch": round(algorithmic_per_launch),
-            "ratio": round(rec["dram_bytes_per_launch"] / max(algorithmic_per_launch, 1), 3),
+    dram = rec["dram_read"] + rec["dram_write"]
+    return {"dram_bytes_per_step": round(dram), "algorithmic_bytes_per_step": round(algorithmic_per_step),
+            "dram_bytes_per_launch": round(dram / max(launches, 1)),
+            "ratio": round(dram / max(algorithmic_per_step, 1), 3),
             "source": f"profiles/traffic_{workload}.json (ncu dram__bytes_read.sum + "
-                      f"dram__bytes_write.sum, {rec['launches']} launches of one step)"}
+                      f"dram__bytes_write.sum over {rec['launches']} ncu launches of one step)"}
 
 
 def peaks() -> dict:
@@ -380,8 +383,8 @@ def run_gpu(args):
                     "peak_basis": f"hbm_gbs {pk['source']}"}
         roof.update({"achieved": round(achieved, 2), "peak": round(peak, 1),
                      "frac": round(achieved / peak, 4),
-                     "traffic_detail": measured_traffic(args.workload, dom,
-                                                        d["bytes"] / d["launches"]),
+                     "traffic_detail": measured_traffic(args.workload, dom, d["bytes"],
+                                                        d["launches"]),
                      "arithmetic_intensity": round(ai, 2), "ridge": round(ridge, 2),
                      "algorithmic": (f"{dom}: 8*m*k*n flops and 8*(m*k + k*n + m*n)*batch bytes "
                                      f"per launch (16 B/element for permutes), summed over "

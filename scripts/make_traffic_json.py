@@ -1,0 +1,17 @@
+"""profiles/traffic_<workload>.json from an ncu `--metrics gpu__time_duration.sum,
+dram__bytes_read.sum,dram__bytes_write.sum --csv` capture of one step
+(bench.py reads it for the roofline's measured-traffic field)."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from ncu_summary import traffic
+
+csv_path, workload, raw_name = sys.argv[1], sys.argv[2], sys.argv[3]
+out = {"source": "ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+                 "dram__bytes_write.sum --clock-control none --csv python scripts/ncu_c2_step.py (one "
+                 "config-2 step, 1024 bit-strings, graph replay); summarised by "
+                 f"scripts/make_traffic_json.py; raw csv profiles/{raw_name}",
+       "workload": workload, "kernels": json.loads(traffic(csv_path))}
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+with open(os.path.join(root, "profiles", f"traffic_{workload}.json"), "w") as f:
+    json.dump(out, f, indent=1)
+print(json.dumps(out["kernels"], indent=1)[:2000])
