@@ -1000,6 +1000,116 @@ def _path_offsets(off, rep: int, stride: int):
     return (off[:, None] + ar[None, :] * stride).reshape(-1)
 
 
+class ShapeOnly:
+    """Labels and dims of a tensor that is never materialised (the fused
+    intermediate of contract_late_expand), for flop/memory accounting."""
+    __slots__ = ("labels", "dims", "itemsize")
+
+    def __init__(self, labels, dims, itemsize: int = 8):
+        self.labels, self.dims, self.itemsize = tuple(labels), tuple(dims), itemsize
+
+    @property
+    def nbytes(self) -> int:
+        return math.prod(self.dims) * self.itemsize
+
+
+_expand_enabled = True
+
+
+def set_expand(enabled: bool) -> bool:
+    """Enable/disable the re-associated (acc . op) . op2 of expand_plan; returns the previous value."""
+    global _expand_enabled
+    prev, _expand_enabled = _expand_enabled, bool(enabled)
+    return prev
+
+
+def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()):
+    """Whether (acc . op) . op2 runs re-associated as acc . (op . op2): acc
+    batched [@b][rb][ko][j] (j = the labels shared with op, innermost; ko =
+    the labels op2 sums, right before j), op and op2 sites with open outputs
+    sharing only ki.  The reference contracts acc with op first, widening
+    each bit-string's 2^18-entry intermediate by op's free labels before op2
+    sums them away again; op . op2 is tiny (one block per combination of the
+    two sites' open outputs), and acc . (op . op2) is ONE batched GEMM
+    [rb] x [(ko, j)] x [(ra, w_free)] per bit-string with the right block
+    picked per entry (b_boff / b_nslice) -- the wide intermediate is never
+    written.  Returns the plan dict or None."""
+    if (late is None or not _expand_enabled or acc.buf.dtype != torch.complex64
+            or op.buf.dtype != torch.complex64 or op2.buf.dtype != torch.complex64):
+        return None
+    lb = late.label
+    if not acc.labels or acc.labels[0] != lb or late.outs(acc) or acc._data is None:
+        return None
+    bo, bo2 = late.outs(op), late.outs(op2)
+    if not bo or not bo2 or lb in op.labels or lb in op2.labels:
+        return None
+    if any(_is_batch(l) for l in acc.labels[1:] + op.labels + op2.labels):
+        return None
+    core = list(acc.labels[1:])
+    cset, oset, o2set = set(core), set(op.labels), set(op2.labels)
+    j = [l for l in core if l in oset]
+    if not j or core[-len(j):] != j or any(l in o2set for l in j) or acc.size >= 2 ** 31:
+        return None
+    rows = core[:-len(j)]
+    ko = [l for l in rows if l in o2set]
+    if not ko or rows[-len(ko):] != ko:
+        return None
+    rb = rows[:-len(ko)]
+    ki = [l for l in op.labels if l in o2set]
+    if not ki or any(l in cset for l in ki) or set(bo) & set(bo2):
+        return None
+    ra = [l for l in op.labels if l not in cset and l not in o2set and l not in bo]
+    w_free = [l for l in op2.labels if l not in cset and l not in oset and l not in bo2]
+    w_free = [l for l in w_free if l not in tail2] + [l for l in w_free if l in tail2]
+    if not rb or not w_free:
+        return None
+    dim = dict(zip(acc.labels, acc.dims))
+    dim.update(zip(op.labels, op.dims))
+    dim.update(zip(op2.labels, op2.dims))
+    P = lambda ls: math.prod(dim[l] for l in ls)
+    M, K, N, nb = P(rb), P(ko) * P(j), P(ra) * P(w_free), acc.dims[0]
+    # the re-associated product must not cost more than the reference's two
+    # contractions, and the per-combination blocks must stay small
+    fused = M * K * N
+    plain = M * P(ko) * P(j) * P(ra) * P(ki) + M * P(ra) * P(ko) * P(ki) * P(w_free)
+    if fused > 1.25 * plain or 2 ** (len(bo) + len(bo2)) * K * N > 2 ** 22 or M < 128:
+        return None
+    u_lab = rb + ko + ra + ki
+    u = ShapeOnly((lb,) + tuple(u_lab), (nb,) + tuple(dim[l] for l in u_lab))
+    return {"j": j, "rb": rb, "ko": ko, "ra": ra, "ki": ki, "w_free": w_free, "bo": bo,
+            "bo2": bo2, "M": M, "K": K, "N": N, "nb": nb, "u": u,
+            "labels": (lb,) + tuple(rb + ra + w_free),
+            "dims": (nb,) + tuple(dim[l] for l in rb + ra + w_free)}
+
+
+def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", plan: dict):
+    """Run an expand_plan: V = op . op2 (every open-output combination, a few
+    blocks of [(ko, j)] x [(ra, w_free)]), then acc . V as one batched GEMM
+    whose B block is chosen per bit-string (qf_cgemm_c64_ex2 b_boff /
+    b_nslice: a TMA slice coordinate).  None if the library declines."""
+    V = contract(op, op2)
+    V = V.transpose_to(tuple(plan["bo"] + plan["bo2"] + plan["ko"] + plan["j"] + plan["ra"] +
+                             plan["w_free"]))
+    off = late.offsets(V, plan["bo"] + plan["bo2"])
+    M, N, K, nb = plan["M"], plan["N"], plan["K"], plan["nb"]
+    a_buf, a_off, entry = acc.raw()
+    out = device_buffer(nb * M * N, acc.buf.dtype, acc.buf.device)
+    flags = _lib.BBOFF_EVEN if (K * N) % 2 == 0 else 0
+    with _timed("gemm", 8 * nb * M * N * K, 8 * nb * (M * K + K * N + M * N),
+                f"b{nb} m{M} n{N} k{K} X" if _timer else ""):
+        st = _lib.load().qf_cgemm_c64_ex2(
+            _gemm_mode | flags, nb, M, N, K, ctypes.c_void_p(a_buf.data_ptr() + 8 * a_off),
+            max(K, 1), entry, _lib.OP_N, ctypes.c_void_p(0), ctypes.c_void_p(0),
+            ctypes.c_void_p(0), ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
+            ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
+            ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,
+            stream_handle())
+    if st == _lib.QF_ERR_UNSUPPORTED:
+        return None
+    _lib.check(st, "gemm_expand")
+    return Tensor(plan["labels"], out, plan["dims"])
+
+
 def contract_late_paths(a: Tensor, b: Tensor, late: LateBits, rep: int, tail=()) -> Optional[Tensor]:
     """contract_late inside a path-batched walk: batched operands carry
     nb*rep entries (bit-string major, path value fastest); an operand whose

@@ -604,3 +604,37 @@ def test_transposed_tma_view(case, kept):
     w = want.transpose_to(outs[0].labels).array
     assert np.linalg.norm(outs[0].array - w) / np.linalg.norm(w) < 1e-5
     assert [l for l in a_labels if l in ks]   # summed labels present
+
+
+@pytest.mark.parametrize("nb", [4, 130])
+@pytest.mark.parametrize("ra", [8, 16])
+def test_reassociated_expansion_matches_two_contractions(nb, ra):
+    """(T . S) . W run as T . (S . W) (expand_plan / contract_late_expand: one
+    batched GEMM per bit-string with its block of S . W picked by TMA slice
+    coordinate; the wide T . S intermediate is never written) -- equal to
+    the two late-sliced contractions and to float64 numpy."""
+    rng = np.random.default_rng(1300 + nb + ra)
+    T = _rand(rng, (nb, 8, 16, 8, 8), np.complex64)              # @b p q r(ko) s(j)
+    S = _rand(rng, (8, ra, 8, 2), np.complex64)                  # s(j) t(ra) u(ki) out0
+    W = _rand(rng, (8, 8, 4, 16, 2), np.complex64)               # r(ko) u(ki) v w out1
+    bits = rng.integers(0, 2, size=(2, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"out0": 0, "out1": 1})
+    tt = tc.Tensor(["@b", "p", "q", "r", "s"], T)
+    ts = tc.Tensor(["s", "t", "u", "out0"], S)
+    tw = tc.Tensor(["r", "u", "v", "w", "out1"], W)
+    plan = tc.expand_plan(tt, ts, tw, late)
+    assert plan is not None
+    with tc.KernelTimer() as kt:
+        got = tc.contract_late_expand(tt, ts, tw, late, plan)
+    assert got is not None and any(" X" in k for k in kt.summary(detail=True))
+    u = tc.contract_late(tt, ts, late, tail=("r", "u", "v", "w", "out1"))
+    want = tc.contract_late(u, tw, late)
+    assert got.labels == want.labels
+    w = want.array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+    sb = np.take_along_axis(S[None].repeat(nb, 0), bits[0][:, None, None, None, None], 4)[..., 0]
+    wb = np.take_along_axis(W[None].repeat(nb, 0), bits[1][:, None, None, None, None, None], 5)[..., 0]
+    ref = np.einsum("bpqrs,bstu,bruvw->bpqtvw", T.astype(np.complex128), sb.astype(np.complex128),
+                    wb.astype(np.complex128))
+    g = got.transpose_to(("@b", "p", "q", "t", "v", "w")).array
+    assert np.linalg.norm(g - ref) / np.linalg.norm(ref) < 1e-5
