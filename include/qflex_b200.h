@@ -213,6 +213,21 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
                       float beta_im, void *stream);
 
 /*
+ * qf_cgemm_c64_view with per-entry A slices: entry b reads the view at
+ * A + a_boff[b], every a_boff[b] a multiple of strideA (whole entries of a
+ * buffer holding a_nslice of them; a bit-string's slice of a tensor whose
+ * outputs are still open) -- a TMA slice coordinate.  a_boff = NULL: as
+ * qf_cgemm_c64_view.
+ */
+int qf_cgemm_c64_view2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                       int64_t strideA, const int64_t *a_boff, int64_t a_nslice, int64_t kin,
+                       int64_t rows_a, int64_t s_rows_a, int64_t kout, int64_t s_kout,
+                       int64_t rows_b, int64_t s_rows_b, const void *B, int64_t ldb,
+                       int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice,
+                       void *C, int64_t ldc, int64_t strideC, float alpha_re, float alpha_im,
+                       float beta_re, float beta_im, void *stream);
+
+/*
  * GPU state-vector simulator (complex128), the verification twin of the
  * reference's dense simulator (rq/oracle.py:51-74, kernels
  * rq/_kernels.py:162-271).  Bit p of a state index is qubit n-1-p (qubit 0 =

@@ -35,7 +35,7 @@ EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_info", "qf_permute", "qf_permute_c64",
     "qf_gather_axis", "qf_fix_axis", "qf_cgemm_c64", "qf_cgemm_c64_gather", "qf_zgemm_c128",
     "qf_bit_offsets", "qf_gather_rows", "qf_cgemm_c64_gather_boff", "qf_cgemm_c64_ex",
-    "qf_cgemm_c64_ex2", "qf_cgemm_c64_tview",
+    "qf_cgemm_c64_ex2", "qf_cgemm_c64_tview", "qf_cgemm_c64_view2",
     "qf_cgemm_c64_view", "qf_sv_basis", "qf_sv_apply", "qf_sv_gather",
     "qf_accumulate",
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
@@ -107,6 +107,12 @@ def _declare(lib):
                                      ctypes.c_float, _c_void_p]
     lib.qf_cgemm_c64_tview.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64, _c_void_p, _i64,
                                        _i64, _i64, _i64, _i64, _i64, _i64, _i64,
+                                       _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p, _i64,
+                                       _c_void_p, _i64, _i64,
+                                       ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                       ctypes.c_float, _c_void_p]
+    lib.qf_cgemm_c64_view2.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64, _c_void_p, _i64,
+                                       _c_void_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
                                        _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p, _i64,
                                        _c_void_p, _i64, _i64,
                                        ctypes.c_float, ctypes.c_float, ctypes.c_float,

@@ -71,6 +71,10 @@ struct GemmArgs {
   // (r / a_rin) * a_rstride + r % a_rin, k at k * lda -- a big operand laid
   // out [outer rows][k][inner rows] read in place (no permute)
   int64_t a_rin = 0, a_rstride = 0;
+  // a_boff values are whole entries (multiples of sA) of an A buffer holding
+  // a_nslice of them: the TMA-fed kernel reads entry b at slice coordinate
+  // a_boff[b] / sA (a bit-string's slice of a tensor whose outputs are open)
+  int64_t a_nslice = 0;
 };
 
 __device__ __forceinline__ int64_t a_row_base(const GemmArgs &g, int64_t r) {

@@ -1693,13 +1693,13 @@ int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, c
   return qf::gemm_simt<float>(g, s);
 }
 
-int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
-                      int64_t strideA, int64_t kin, int64_t rows_a, int64_t s_rows_a,
-                      int64_t kout, int64_t s_kout, int64_t rows_b, int64_t s_rows_b,
-                      const void *B, int64_t ldb, int64_t strideB, int opB,
-                      const int64_t *b_boff, int64_t b_nslice, void *C, int64_t ldc,
-                      int64_t strideC, float alpha_re, float alpha_im, float beta_re,
-                      float beta_im, void *stream) {
+int qf_cgemm_c64_view2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                       int64_t strideA, const int64_t *a_boff, int64_t a_nslice, int64_t kin,
+                       int64_t rows_a, int64_t s_rows_a, int64_t kout, int64_t s_kout,
+                       int64_t rows_b, int64_t s_rows_b, const void *B, int64_t ldb,
+                       int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice,
+                       void *C, int64_t ldc, int64_t strideC, float alpha_re, float alpha_im,
+                       float beta_re, float beta_im, void *stream) {
   QF_REQUIRE(kin >= 1 && rows_a >= 1 && kout >= 1 && rows_b >= 1, "gemm_view: empty run");
   QF_REQUIRE(M == rows_a * rows_b && K == kin * kout, "gemm_view: runs do not match M/K");
   QF_REQUIRE(mode == QF_GEMM_AUTO || mode == QF_GEMM_TC3, "gemm_view: tensor-core modes only");
@@ -1708,6 +1708,9 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
                  b_boff ? 2 : strideB, opB, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im};
   g.b_boff = b_boff;
   g.b_nslice = b_nslice;
+  QF_REQUIRE(!a_boff || a_nslice > 0, "gemm_view2: a_boff needs a_nslice");
+  g.a_boff = a_boff;        // whole entries of strideA elements, TMA slice coordinates
+  g.a_nslice = a_boff ? a_nslice : 0;
   g.v_kin = kin;
   g.v_ra = rows_a;
   g.v_sra = s_rows_a;
@@ -1718,6 +1721,19 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
   int st = qf::validate(g);
   if (st != QF_OK) return st;
   return qf::gemm_tc3(g, qf::as_stream(stream));
+}
+
+int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
+                      int64_t strideA, int64_t kin, int64_t rows_a, int64_t s_rows_a,
+                      int64_t kout, int64_t s_kout, int64_t rows_b, int64_t s_rows_b,
+                      const void *B, int64_t ldb, int64_t strideB, int opB,
+                      const int64_t *b_boff, int64_t b_nslice, void *C, int64_t ldc,
+                      int64_t strideC, float alpha_re, float alpha_im, float beta_re,
+                      float beta_im, void *stream) {
+  return qf_cgemm_c64_view2(mode, batch, M, N, K, A, strideA, nullptr, 0, kin, rows_a, s_rows_a,
+                            kout, s_kout, rows_b, s_rows_b, B, ldb, strideB, opB, b_boff,
+                            b_nslice, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im,
+                            stream);
 }
 
 int qf_cgemm_c64_tview(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,

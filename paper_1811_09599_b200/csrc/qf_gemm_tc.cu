@@ -1827,6 +1827,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         const int32_t m0 = (int32_t)(pc.mt * BM), n0 = (int32_t)(pc.nt * BN), b = (int32_t)pc.bidx;
         const int32_t bslice =
             g.b_boff ? (int32_t)(__ldg(g.b_boff + pc.bidx) / (g.K * g.N)) : b;
+        const int32_t aslice = g.a_boff ? (int32_t)(__ldg(g.a_boff + pc.bidx) / g.sA) : b;
         // A view: row coordinates of this tile, k-block -> (ki, ko) counters
         int32_t v_ra = 0, v_rb = 0, v_ki = 0, v_ko = 0;
         const int32_t v_kbi = g.v_kin ? (int32_t)(g.v_kin / KB) : 1;
@@ -1859,7 +1860,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             asm volatile(
                 "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
                 "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(rawa + slot * L::RAWA_SLOT),
-                "l"(&tmA), "r"(v_ki * 2 * KB), "r"(v_ra), "r"(v_ko), "r"(v_rb), "r"(b), "r"(bar)
+                "l"(&tmA), "r"(v_ki * 2 * KB), "r"(v_ra), "r"(v_ko), "r"(v_rb), "r"(aslice), "r"(bar)
                 : "memory");
             if (++v_ki == v_kbi) {
               v_ki = 0;
@@ -1871,7 +1872,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             asm volatile(
                 "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
                 "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(rawa + slot * L::RAWA_SLOT),
-                "l"(&tmA), "r"(a0), "r"(a1), "r"(b), "r"(bar)
+                "l"(&tmA), "r"(a0), "r"(a1), "r"(aslice), "r"(bar)
                 : "memory");
           }
           if (!breuse) {
@@ -2623,7 +2624,8 @@ static bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5
 // TMA needs 16-byte global strides and A/B entries addressable by coordinates
 // (no offset tables; B entry offsets only as whole [K][N] slices)
 bool tma_ok(const GemmArgs &g) {
-  const bool a_ok = !g.a_roff && !g.a_boff && g.sA > 0 && g.sA % 2 == 0 && g.lda % 2 == 0;
+  const bool a_ok = !g.a_roff && (!g.a_boff || g.a_nslice > 0) && g.sA > 0 && g.sA % 2 == 0 &&
+                    g.lda % 2 == 0;
   const bool b_ok = g.b_boff ? (g.b_nslice > 0 && (g.K * g.N) % 2 == 0)
                              : (g.sB > 0 && g.sB % 2 == 0);
   const bool v_ok = !g.v_kin ||
@@ -2647,6 +2649,7 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   CUtensorMap tmA{}, tmB{};
   if constexpr (TMA) {
     const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
+    const uint64_t na = g.a_boff ? (uint64_t)g.a_nslice : nb;   // A entries addressable
     bool okA;
     if (g.v_t) {
       // transposed view: dims {2 ra, rb, ki, ko, b} (strides need not be
@@ -2654,7 +2657,7 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
       // the dense [8 k][128 rows] tile of the plain opA = T path
       const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
       const uint64_t dims[5] = {(uint64_t)(2 * g.v_ra), (uint64_t)g.v_rb, (uint64_t)g.v_kin,
-                                (uint64_t)g.v_kout, nb};
+                                (uint64_t)g.v_kout, na};
       const uint64_t strides[4] = {(uint64_t)g.v_srb * 8, (uint64_t)g.v_ski * 8,
                                    (uint64_t)g.v_skout * 8, (uint64_t)std::max<int64_t>(g.sA, 1) * 8};
       const uint32_t box[5] = {2 * bra, (uint32_t)(BM / bra), (uint32_t)KB, 1, 1};
@@ -2662,15 +2665,15 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
     } else if (g.v_kin) {
       const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
       const uint64_t dims[5] = {(uint64_t)(2 * g.v_kin), (uint64_t)g.v_ra, (uint64_t)g.v_kout,
-                                (uint64_t)g.v_rb, nb};
+                                (uint64_t)g.v_rb, na};
       const uint64_t strides[4] = {(uint64_t)g.v_sra * 8, (uint64_t)g.v_skout * 8,
                                    (uint64_t)g.v_srb * 8, (uint64_t)std::max<int64_t>(g.sA, 1) * 8};
       const uint32_t box[5] = {16, bra, 1, (uint32_t)(BM / bra), 1};
       okA = make_tmap5(&tmA, g.A, dims, strides, box);
     } else {
       okA = g.opA == QF_OP_N
-                ? make_tmap(&tmA, g.A, 2 * g.K, g.M, nb, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 16, 128, true)
-                : make_tmap(&tmA, g.A, 2 * g.M, g.K, nb, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 256, 8, false);
+                ? make_tmap(&tmA, g.A, 2 * g.K, g.M, na, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 16, 128, true)
+                : make_tmap(&tmA, g.A, 2 * g.M, g.K, na, g.lda * 8, std::max<int64_t>(g.sA, 1) * 8, 256, 8, false);
     }
     // B entries: strided batch, or b_nslice whole [K][N] slices picked per entry
     const uint64_t nbs = g.b_boff ? (uint64_t)g.b_nslice : nb;
@@ -3533,9 +3536,9 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
     return QF_ERR_UNSUPPORTED;
   }
   if (g.v_kin) {  // A views are read by the TMA-fed short-K kernel only
-    // (a transposed view also serves narrow N: the 64-column tile computes
-    // zeros beyond N, the HBM-bound shape does not mind)
-    if (!(g.K >= 32 && g.K <= 128 && (g.N > 32 || g.v_t) && tc::tma_ok(g))) {
+    // (narrow N runs 32-column tiles that compute zeros beyond N; the
+    // HBM-bound shapes do not mind)
+    if (!(g.K >= 32 && g.K <= 128 && tc::tma_ok(g))) {
       set_error("tc3: A view (kin %lld, rows %lld x %lld) not TMA-describable for K=%lld N=%lld",
                 (long long)g.v_kin, (long long)g.v_ra, (long long)g.v_rb, (long long)g.K,
                 (long long)g.N);

@@ -1038,10 +1038,12 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
             or op.buf.dtype != torch.complex64 or op2.buf.dtype != torch.complex64):
         return None
     lb = late.label
-    if not acc.labels or acc.labels[0] != lb or late.outs(acc) or acc._data is None:
-        return None
     bo, bo2 = late.outs(op), late.outs(op2)
     if not bo or not bo2 or lb in op.labels or lb in op2.labels:
+        return None
+    if acc.labels and lb not in acc.labels and late.outs(acc):
+        return _expand_plan_open(acc, op, op2, late, tail2, bo, bo2)
+    if not acc.labels or acc.labels[0] != lb or late.outs(acc) or acc._data is None:
         return None
     if any(_is_batch(l) for l in acc.labels[1:] + op.labels + op2.labels):
         return None
@@ -1082,16 +1084,90 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
             "dims": (nb,) + tuple(dim[l] for l in rb + ra + w_free)}
 
 
+def _expand_plan_open(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2, bo, bo2):
+    """expand_plan when acc still has open outputs (leading its layout): each
+    bit-string's slice of acc is read in place as a TMA view at a slice
+    coordinate (qf_cgemm_c64_view2), times its block of op . op2."""
+    lb = late.label
+    ao = late.outs(acc)
+    if _gemm_mode == _lib.GEMM_FFMA:   # the view kernel is tensor-core only
+        return None
+    if (acc._data is None or set(acc.labels[:len(ao)]) != set(ao) or acc.size >= 2 ** 31
+            or any(_is_batch(l) for l in acc.labels + op.labels + op2.labels)):
+        return None
+    core, cdims = list(acc.labels[len(ao):]), list(acc.dims[len(ao):])
+    cset, oset, o2set = set(core), set(op.labels), set(op2.labels)
+    j = [l for l in core if l in oset]
+    ko = [l for l in core if l in o2set]
+    ki = [l for l in op.labels if l in o2set]
+    if not j or not ko or not ki or set(j) & set(ko) or any(l in cset for l in ki):
+        return None
+    if set(bo) & set(bo2) or set(ao) & (set(bo) | set(bo2)):
+        return None
+    k_order = [l for l in core if l in set(j) | set(ko)]
+    rows = [l for l in core if l not in set(k_order)]
+    view = _a_view(core, cdims, rows, k_order)
+    if view is None or not rows:
+        return None
+    ra = [l for l in op.labels if l not in cset and l not in o2set and l not in bo]
+    w_free = [l for l in op2.labels if l not in cset and l not in oset and l not in bo2]
+    w_free = [l for l in w_free if l not in tail2] + [l for l in w_free if l in tail2]
+    if not w_free:
+        return None
+    dim = dict(zip(acc.labels, acc.dims))
+    dim.update(zip(op.labels, op.dims))
+    dim.update(zip(op2.labels, op2.dims))
+    P = lambda ls: math.prod(dim[l] for l in ls)
+    M, K, N, nb = P(rows), P(k_order), P(ra) * P(w_free), late.nb
+    # the reference order keeps acc . op open (once per output combination)
+    # while that is cheaper than per bit-string; only fuse where the second
+    # contraction would be sliced per bit-string anyway, and where the fused
+    # per-bit-string product costs no more than both contractions
+    comb1 = 2 ** (len(ao) + len(bo))
+    if comb1 > late.limit or comb1 * 2 ** len(bo2) <= late.limit:
+        return None
+    fused = nb * M * K * N
+    plain = comb1 * M * P(ko) * P(j) * P(ra) * P(ki) + nb * M * P(ra) * P(ko) * P(ki) * P(w_free)
+    if (fused > 1.25 * plain or 2 ** (len(bo) + len(bo2)) * K * N > 2 ** 22 or M < 128
+            or not 32 <= K <= 128):
+        return None
+    u_lab = ao + rows + ko + bo + ra + ki
+    u = ShapeOnly(tuple(u_lab), tuple(dim[l] for l in u_lab))
+    return {"open": True, "view": view, "ao": ao, "k_order": k_order, "j": j, "rb": rows,
+            "ko": ko, "ra": ra, "ki": ki, "w_free": w_free, "bo": bo, "bo2": bo2, "M": M,
+            "K": K, "N": N, "nb": nb, "u": u, "labels": (lb,) + tuple(rows + ra + w_free),
+            "dims": (nb,) + tuple(dim[l] for l in rows + ra + w_free)}
+
+
 def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", plan: dict):
     """Run an expand_plan: V = op . op2 (every open-output combination, a few
     blocks of [(ko, j)] x [(ra, w_free)]), then acc . V as one batched GEMM
     whose B block is chosen per bit-string (qf_cgemm_c64_ex2 b_boff /
     b_nslice: a TMA slice coordinate).  None if the library declines."""
+    k_order = plan["k_order"] if plan.get("open") else plan["ko"] + plan["j"]
     V = contract(op, op2)
-    V = V.transpose_to(tuple(plan["bo"] + plan["bo2"] + plan["ko"] + plan["j"] + plan["ra"] +
-                             plan["w_free"]))
+    V = V.transpose_to(tuple(plan["bo"] + plan["bo2"] + k_order + plan["ra"] + plan["w_free"]))
     off = late.offsets(V, plan["bo"] + plan["bo2"])
     M, N, K, nb = plan["M"], plan["N"], plan["K"], plan["nb"]
+    if plan.get("open"):
+        # each bit-string's slice of acc read in place as a TMA view
+        aoff = late.offsets(acc, plan["ao"])
+        entry = acc.size // (2 ** len(plan["ao"]))
+        kin, ra, sra, ko, sko, rb, srb = plan["view"]
+        out = device_buffer(nb * M * N, acc.buf.dtype, acc.buf.device)
+        with _timed("gemm", 8 * nb * M * N * K, 8 * nb * (M * K + K * N + M * N),
+                    f"b{nb} m{M} n{N} k{K} XO" if _timer else ""):
+            st = _lib.load().qf_cgemm_c64_view2(
+                _gemm_mode, nb, M, N, K, ctypes.c_void_p(acc.data.data_ptr()), entry,
+                ctypes.c_void_p(aoff.data_ptr()), 2 ** len(plan["ao"]), kin, ra, sra, ko, sko,
+                rb, srb, ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
+                ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
+                ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,
+                stream_handle())
+        if st == _lib.QF_ERR_UNSUPPORTED:
+            return None
+        _lib.check(st, "gemm_expand_open")
+        return Tensor(plan["labels"], out, plan["dims"])
     a_buf, a_off, entry = acc.raw()
     out = device_buffer(nb * M * N, acc.buf.dtype, acc.buf.device)
     flags = _lib.BBOFF_EVEN if (K * N) % 2 == 0 else 0

@@ -638,3 +638,45 @@ def test_reassociated_expansion_matches_two_contractions(nb, ra):
                     wb.astype(np.complex128))
     g = got.transpose_to(("@b", "p", "q", "t", "v", "w")).array
     assert np.linalg.norm(g - ref) / np.linalg.norm(ref) < 1e-5
+
+
+@pytest.mark.parametrize("nb", [8, 200])
+@pytest.mark.parametrize("ra", [1, 4])
+def test_reassociated_expansion_open_operand(nb, ra):
+    """expand_plan with acc still carrying open outputs: each bit-string's
+    slice of acc read in place as a TMA view at a slice coordinate
+    (qf_cgemm_c64_view2 a_boff / a_nslice), times its block of S . W --
+    equal to the two late contractions and to float64 numpy."""
+    rng = np.random.default_rng(1400 + nb + ra)
+    A = _rand(rng, (2, 2, 8, 16, 8, 8, 8), np.complex64)        # o0 o1 p q j r ko
+    s_lab = ["j", "u", "out2"] if ra == 1 else ["j", "t", "u", "out2"]
+    S = _rand(rng, (8, 8, 2) if ra == 1 else (8, ra, 8, 2), np.complex64)
+    W = _rand(rng, (8, 8, 8, 2), np.complex64)                  # ko u w out3
+    bits = rng.integers(0, 2, size=(4, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"o0": 0, "o1": 1, "out2": 2, "out3": 3},
+                       limit=8)
+    ta = tc.Tensor(["o0", "o1", "p", "q", "j", "r", "ko"], A)
+    ts, tw = tc.Tensor(s_lab, S), tc.Tensor(["ko", "u", "w", "out3"], W)
+    plan = tc.expand_plan(ta, ts, tw, late)
+    assert plan is not None and plan.get("open")
+    with tc.KernelTimer() as kt:
+        got = tc.contract_late_expand(ta, ts, tw, late, plan)
+    assert got is not None and any(" XO" in k for k in kt.summary(detail=True))
+    u = tc.contract_late(ta, ts, late, tail=("ko", "u", "w", "out3"))
+    want = tc.contract_late(u, tw, late)
+    w = want.transpose_to(got.labels).array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+    o = bits.T
+    ab = A[o[:, 0], o[:, 1]]                                      # b p q j r ko
+    sb = S[..., o[:, 2]]
+    sb = np.moveaxis(sb, -1, 0)
+    wb = np.moveaxis(W[..., o[:, 3]], -1, 0)
+    if ra == 1:
+        ref = np.einsum("bpqjrk,bju,bkuw->bpqrw", ab.astype(np.complex128),
+                        sb.astype(np.complex128), wb.astype(np.complex128))
+        g = got.transpose_to(("@b", "p", "q", "r", "w")).array
+    else:
+        ref = np.einsum("bpqjrk,bjtu,bkuw->bpqrtw", ab.astype(np.complex128),
+                        sb.astype(np.complex128), wb.astype(np.complex128))
+        g = got.transpose_to(("@b", "p", "q", "r", "t", "w")).array
+    assert np.linalg.norm(g - ref) / np.linalg.norm(ref) < 1e-5
