@@ -82,7 +82,8 @@ def _oracle_worker(args):
     return time.perf_counter() - t0
 
 
-def cpu_oracle_rate(circuit_text: str, plan_text: str, outs: list, procs: int) -> dict:
+def cpu_oracle_rate(circuit_text: str, plan_text: str, outs: list, procs: int,
+                    of: str = "the 1024 config-2 bit-strings") -> dict:
     """Amplitudes/s of the numpy oracle with `procs` single-threaded worker
     processes (spawned with every BLAS/OpenMP pool pinned to 1 thread)."""
     import multiprocessing as mp
@@ -107,7 +108,7 @@ def cpu_oracle_rate(circuit_text: str, plan_text: str, outs: list, procs: int) -
                 os.environ[k] = v
     return {"value": len(outs) / wall, "unit": "amplitudes/s", "cores": len(chunks),
             "kind": "port", "seconds": wall,
-            "sample": f"{len(outs)} of the 1024 config-2 bit-strings, oracle/rqc_oracle.py "
+            "sample": f"{len(outs)} of {of}, oracle/rqc_oracle.py "
                       f"(numpy restatement of the reference), {len(chunks)} processes x 1 thread"}
 
 
@@ -366,36 +367,60 @@ def run_gpu(args):
                           "share": round(d["ms"] / total, 4),
                           "tflops": round(d["flops"] / d["ms"] / 1e9, 2) if d["ms"] else None,
                           "gbs": round(d["bytes"] / d["ms"] / 1e6, 1) if d["ms"] else None}
-        dom = max(kerns, key=lambda k: kerns[k]["ms"])   # dominant CUDA kernel of the step
-        d = kerns[dom]
         tensor_peak = pk["tf32_tflops"] / 3                # 3xTF32 complex ceiling
         ridge = tensor_peak * 1e12 / (pk["hbm_gbs"] * 1e9)
-        ai = d["flops"] / max(d["bytes"], 1)
-        if d["flops"] and "tc3" in dom and ai >= ridge:
-            achieved = d["flops"] / d["ms"] / 1e9
-            peak = tensor_peak
-            roof = {"bound": "tensor", "unit": "TFLOP/s", "kernel": dom,
-                    "peak_basis": "cuBLAS TF32 measured (profiles/measured_tf32.json) / 3 (3xTF32)"}
-        else:
-            achieved = d["bytes"] / d["ms"] / 1e6
-            peak = pk["hbm_gbs"]
-            roof = {"bound": "hbm", "unit": "GB/s", "kernel": dom,
-                    "peak_basis": f"hbm_gbs {pk['source']}"}
-        roof.update({"achieved": round(achieved, 2), "peak": round(peak, 1),
-                     "frac": round(achieved / peak, 4),
-                     "traffic_detail": measured_traffic(args.workload, dom, d["bytes"],
-                                                        d["launches"]),
-                     "arithmetic_intensity": round(ai, 2), "ridge": round(ridge, 2),
-                     "algorithmic": (f"{dom}: 8*m*k*n flops and 8*(m*k + k*n + m*n)*batch bytes "
-                                     f"per launch (16 B/element for permutes), summed over "
-                                     f"{d['launches']} launches of one step, / their CUDA-event time")})
+        # launches grouped by (CUDA kernel, the roofline that bounds the
+        # launch's shape: tensor if its algorithmic flop/byte >= the ridge);
+        # the dominant group is the one with the most time in the step
+        groups = {}
+        for kind, a, b, flops, nbytes, *rest in kt.records:
+            name = rest[1] if len(rest) > 1 and rest[1] else kind
+            bnd = "tensor" if flops and "tc3" in name and flops / max(nbytes, 1) >= ridge else "hbm"
+            g = groups.setdefault((name, bnd), {"launches": 0, "ms": 0.0, "flops": 0, "bytes": 0})
+            g["launches"] += 1
+            g["ms"] += a.elapsed_time(b)
+            g["flops"] += flops
+            g["bytes"] += nbytes
+
+        def roof_of(key):
+            name, bnd = key
+            g = groups[key]
+            if bnd == "tensor":
+                achieved, peak = g["flops"] / g["ms"] / 1e9, tensor_peak
+                r = {"bound": "tensor", "unit": "TFLOP/s", "kernel": name,
+                     "peak_basis": "cuBLAS TF32 measured (profiles/measured_tf32.json) / 3 (3xTF32)"}
+            else:
+                achieved, peak = g["bytes"] / g["ms"] / 1e6, pk["hbm_gbs"]
+                r = {"bound": "hbm", "unit": "GB/s", "kernel": name,
+                     "peak_basis": f"hbm_gbs {pk['source']}"}
+            r.update({"achieved": round(achieved, 2), "peak": round(peak, 1),
+                      "frac": round(achieved / peak, 4), "launches": g["launches"],
+                      "ms": round(g["ms"], 4),
+                      "arithmetic_intensity": round(g["flops"] / max(g["bytes"], 1), 2)})
+            return r
+
+        dkey = max(groups, key=lambda k: groups[k]["ms"])
+        dom, d = dkey[0], groups[dkey]
+        roof = roof_of(dkey)
+        fam = kerns.get(dom, d)
+        roof.update({"traffic_detail": measured_traffic(args.workload, dom, fam["bytes"],
+                                                        fam["launches"]),
+                     "ridge": round(ridge, 2),
+                     "algorithmic": (f"{dom} launches whose shape is {dkey[1]}-bound (flop/byte "
+                                     f"{'>=' if dkey[1] == 'tensor' else '<'} ridge): 8*m*k*n "
+                                     f"flops and 8*(m*k + k*n + m*n)*batch bytes per launch, "
+                                     f"summed over the {d['launches']} such launches of one step, "
+                                     f"/ their CUDA-event time"),
+                     "other_bound": [roof_of(k) for k in sorted(groups, key=lambda k: -groups[k]["ms"])
+                                     if k != dkey and k[0] == dom]})
+        # DRAM bytes per launch over the whole kernel family (ncu cannot split it by bound)
         roof["traffic"] = (roof["traffic_detail"] or {}).get("dram_bytes_per_launch")
         clk = clocks.summary()
         cpu = None
         if not args.no_cpu_baseline:
             sample = max(8, min(len(outs), int(args.cpu_sample)))
             cpu = cpu_oracle_rate(qf.write_circuit(circ), qf.format_plan(plan), outs[:sample],
-                                  host_cores())
+                                  host_cores(), f"the {len(outs)} {args.workload} bit-strings")
         result = {
             "metric": "amplitudes/s", "value": round(value, 2), "unit": "amplitudes/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -610,7 +635,8 @@ def run_reference(args):
     sample = max(cores, min(N_BITSTRINGS, int(args.cpu_sample)))
     rates = []
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_rate(qf.write_circuit(circ), qf.format_plan(plan), outs[:sample], cores)
+        r = cpu_oracle_rate(qf.write_circuit(circ), qf.format_plan(plan), outs[:sample], cores,
+                            f"the {N_BITSTRINGS} {wl} bit-strings")
         if i >= args.warmup:
             rates.append(r)
     secs = sum(r["seconds"] for r in rates)
