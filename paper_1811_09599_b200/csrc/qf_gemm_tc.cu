@@ -3538,12 +3538,16 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.v_kin) {  // A views are read by the TMA-fed short-K kernel only
     // (narrow N runs 32-column tiles that compute zeros beyond N; the
     // HBM-bound shapes do not mind)
-    if (!(g.K >= 32 && g.K <= 128 && tc::tma_ok(g))) {
+    // long K (N-views): the promoted long-K kernel with its TMA producer
+    // (plain row-major epilogue only)
+    const bool long_k = g.K > 128 && !g.v_t && !g.c_trans && g.N > 32;
+    if (!(g.K >= 32 && (g.K <= 128 || long_k) && tc::tma_ok(g))) {
       set_error("tc3: A view (kin %lld, rows %lld x %lld) not TMA-describable for K=%lld N=%lld",
                 (long long)g.v_kin, (long long)g.v_ra, (long long)g.v_rb, (long long)g.K,
                 (long long)g.N);
       return QF_ERR_UNSUPPORTED;
     }
+    if (g.K > 128) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
     return launch_short_tma(g, s);
   }
   const bool small_n = g.N <= 64;

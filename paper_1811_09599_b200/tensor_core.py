@@ -519,29 +519,45 @@ def _permute_pays(bt: int, m: int, k: int, n: int) -> bool:
 
 def _a_view(labels, dims, a_free, k_order):
     """The big operand's per-entry layout as a TMA-describable view, or None:
-    its innermost label summed (kin, contiguous, dim % 8 == 0), at most one
-    more summed label (kout), and its free labels (in memory order) in at
-    most two runs around kout.  -> (kin, rows_a, s_rows_a, kout, s_kout,
-    rows_b, s_rows_b) in elements (see qf_cgemm_c64_view)."""
-    if not k_order or not labels or labels[-1] != k_order[-1] or len(k_order) > 2:
+    its summed labels in at most two runs of adjacent labels, the inner run
+    innermost and contiguous (kin entries, kin % 8 == 0), and its free labels
+    (in memory order) in at most two runs around the outer summed run.
+    -> (kin, rows_a, s_rows_a, kout, s_kout, rows_b, s_rows_b) in elements
+    (see qf_cgemm_c64_view)."""
+    if not k_order or not labels or labels[-1] != k_order[-1]:
         return None
     if [l for l in labels if l not in k_order] != list(a_free):
+        return None
+    if [l for l in labels if l in k_order] != list(k_order):
         return None
     dim = dict(zip(labels, dims))
     stride, acc = {}, 1
     for l, d in zip(reversed(labels), reversed(dims)):
         stride[l] = acc
         acc *= d
-    kin = dim[k_order[-1]]
+    ks = set(k_order)
+    runs, prev = [], None                 # runs of adjacent summed labels
+    for p, l in enumerate(labels):
+        if l in ks:
+            if prev is not None and prev == p - 1:
+                runs[-1].append(l)
+            else:
+                runs.append([l])
+            prev = p
+    if len(runs) > 2:
+        return None
+    inner = runs[-1]
+    kin = math.prod(dim[l] for l in inner)
     if kin % 8:
         return None
-    if len(k_order) == 2:
-        ko = k_order[0]
-        pos = labels.index(ko)
-        run_b, run_a = labels[:pos], labels[pos + 1:-1]
-        kout, s_kout = dim[ko], stride[ko]
+    first_inner = labels.index(inner[0])
+    if len(runs) == 2:
+        outer = runs[0]
+        p0, p1 = labels.index(outer[0]), labels.index(outer[-1])
+        run_b, run_a = labels[:p0], labels[p1 + 1:first_inner]
+        kout, s_kout = math.prod(dim[l] for l in outer), stride[outer[-1]]
     else:
-        run_b, run_a = (), labels[:-1]
+        run_b, run_a = (), labels[:first_inner]
         kout, s_kout = 1, kin
     if not run_a:
         return None            # summed labels contiguous: a plain layout
@@ -1047,16 +1063,21 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
         return None
     if any(_is_batch(l) for l in acc.labels[1:] + op.labels + op2.labels):
         return None
-    core = list(acc.labels[1:])
+    core, cdims = list(acc.labels[1:]), list(acc.dims[1:])
     cset, oset, o2set = set(core), set(op.labels), set(op2.labels)
     j = [l for l in core if l in oset]
-    if not j or core[-len(j):] != j or any(l in o2set for l in j) or acc.size >= 2 ** 31:
+    ko = [l for l in core if l in o2set]
+    if not j or not ko or set(j) & set(ko) or acc.size >= 2 ** 31:
         return None
-    rows = core[:-len(j)]
-    ko = [l for l in rows if l in o2set]
-    if not ko or rows[-len(ko):] != ko:
-        return None
-    rb = rows[:-len(ko)]
+    # A = acc's entries with k = its labels summed by op or op2 (memory
+    # order): a plain row-major operand, or a TMA view of one
+    k_order = [l for l in core if l in set(j) | set(ko)]
+    rb = [l for l in core if l not in set(k_order)]
+    view = None
+    if core != rb + k_order:
+        view = _a_view(core, cdims, rb, k_order)
+        if view is None or _gemm_mode == _lib.GEMM_FFMA:
+            return None
     ki = [l for l in op.labels if l in o2set]
     if not ki or any(l in cset for l in ki) or set(bo) & set(bo2):
         return None
@@ -1079,7 +1100,8 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
     u_lab = rb + ko + ra + ki
     u = ShapeOnly((lb,) + tuple(u_lab), (nb,) + tuple(dim[l] for l in u_lab))
     return {"j": j, "rb": rb, "ko": ko, "ra": ra, "ki": ki, "w_free": w_free, "bo": bo,
-            "bo2": bo2, "M": M, "K": K, "N": N, "nb": nb, "u": u,
+            "bo2": bo2, "M": M, "K": K, "N": N, "nb": nb, "u": u, "k_order": k_order,
+            "view": view,
             "labels": (lb,) + tuple(rb + ra + w_free),
             "dims": (nb,) + tuple(dim[l] for l in rb + ra + w_free)}
 
@@ -1144,7 +1166,7 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
     blocks of [(ko, j)] x [(ra, w_free)]), then acc . V as one batched GEMM
     whose B block is chosen per bit-string (qf_cgemm_c64_ex2 b_boff /
     b_nslice: a TMA slice coordinate).  None if the library declines."""
-    k_order = plan["k_order"] if plan.get("open") else plan["ko"] + plan["j"]
+    k_order = plan["k_order"]
     V = contract(op, op2)
     V = V.transpose_to(tuple(plan["bo"] + plan["bo2"] + k_order + plan["ra"] + plan["w_free"]))
     off = late.offsets(V, plan["bo"] + plan["bo2"])
@@ -1170,6 +1192,22 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
         return Tensor(plan["labels"], out, plan["dims"])
     a_buf, a_off, entry = acc.raw()
     out = device_buffer(nb * M * N, acc.buf.dtype, acc.buf.device)
+    if plan.get("view") is not None:
+        # batched entries read as a TMA view (k split around a free run)
+        kin, ra, sra, ko, sko, rb, srb = plan["view"]
+        with _timed("gemm", 8 * nb * M * N * K, 8 * nb * (M * K + K * N + M * N),
+                    f"b{nb} m{M} n{N} k{K} XV" if _timer else ""):
+            st = _lib.load().qf_cgemm_c64_view2(
+                _gemm_mode, nb, M, N, K, ctypes.c_void_p(a_buf.data_ptr() + 8 * a_off), entry,
+                ctypes.c_void_p(0), 0, kin, ra, sra, ko, sko, rb, srb,
+                ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
+                ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
+                ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,
+                stream_handle())
+        if st == _lib.QF_ERR_UNSUPPORTED:
+            return None
+        _lib.check(st, "gemm_expand_view")
+        return Tensor(plan["labels"], out, plan["dims"])
     flags = _lib.BBOFF_EVEN if (K * N) % 2 == 0 else 0
     with _timed("gemm", 8 * nb * M * N * K, 8 * nb * (M * K + K * N + M * N),
                 f"b{nb} m{M} n{N} k{K} X" if _timer else ""):

@@ -680,3 +680,31 @@ def test_reassociated_expansion_open_operand(nb, ra):
                         sb.astype(np.complex128), wb.astype(np.complex128))
         g = got.transpose_to(("@b", "p", "q", "r", "t", "w")).array
     assert np.linalg.norm(g - ref) / np.linalg.norm(ref) < 1e-5
+
+
+@pytest.mark.parametrize("nb", [4, 64])
+@pytest.mark.parametrize("wide", [False, True])
+def test_reassociated_expansion_view_operand(nb, wide):
+    """expand_plan on a batched operand whose summed labels straddle its rows
+    ([@b][ko][p][q][j...]): acc read as a TMA view (qf_cgemm_c64_view2; K up
+    to 512 through the promoted long-K kernel) times its block of S . W."""
+    rng = np.random.default_rng(1500 + nb + wide)
+    jd = (8, 8) if wide else (8,)
+    A = _rand(rng, (nb, 8, 8, 16) + jd, np.complex64)           # @b r(ko) p q j..
+    j_lab = ["j1", "j2"] if wide else ["j1"]
+    S = _rand(rng, jd + (8, 8, 2), np.complex64)                # j.. t(ra) u(ki) out0
+    W = _rand(rng, (8, 8, 8, 2), np.complex64)                  # r(ko) u(ki) v out1
+    bits = rng.integers(0, 2, size=(2, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(), {"out0": 0, "out1": 1})
+    ta = tc.Tensor(["@b", "r", "p", "q"] + j_lab, A)
+    ts = tc.Tensor(j_lab + ["t", "u", "out0"], S)
+    tw = tc.Tensor(["r", "u", "v", "out1"], W)
+    plan = tc.expand_plan(ta, ts, tw, late)
+    assert plan is not None and plan["view"] is not None
+    with tc.KernelTimer() as kt:
+        got = tc.contract_late_expand(ta, ts, tw, late, plan)
+    assert got is not None and any(" XV" in k for k in kt.summary(detail=True))
+    u = tc.contract_late(ta, ts, late, tail=("r", "u", "v", "out1"))
+    want = tc.contract_late(u, tw, late)
+    w = want.transpose_to(got.labels).array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
