@@ -178,7 +178,10 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
                     float beta_im, void *stream);
 
 /*
- * qf_cgemm_c64_ex with B slice count: when every b_boff[b] is a whole
+ * qf_cgemm_c64_ex with slice counts: a_nslice > 0 declares every a_boff[b] a
+ * whole entry (a multiple of strideA) of an A buffer holding a_nslice of
+ * them, addressed by the TMA kernel as a slice coordinate; likewise, when
+ * every b_boff[b] is a whole
  * [K][N] slice (a multiple of K*N) of a B buffer holding b_nslice slices,
  * the TMA-fed tensor-core kernel reads B by slice coordinate (the per-entry
  * site-tensor slices of the batched amplitude walk).  b_nslice = 0: as
@@ -187,7 +190,7 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
  */
 int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
                      int64_t lda, int64_t strideA, int opA, const int64_t *a_boff,
-                     const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
+                     int64_t a_nslice, const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
                      int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice, void *C,
                      int64_t ldc, int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                      float beta_im, void *stream);
@@ -216,16 +219,20 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
  * qf_cgemm_c64_view with per-entry A slices: entry b reads the view at
  * A + a_boff[b], every a_boff[b] a multiple of strideA (whole entries of a
  * buffer holding a_nslice of them; a bit-string's slice of a tensor whose
- * outputs are still open) -- a TMA slice coordinate.  a_boff = NULL: as
- * qf_cgemm_c64_view.
+ * outputs are still open) -- a TMA slice coordinate.  c_nblk > 0 stores C
+ * in column blocks: column n of row m at C + b*strideC + (n / c_nblk) *
+ * c_bstride + m*ldc + n % c_nblk (several open-output values computed side
+ * by side, each landing as its own [M][c_nblk] block; K <= 128).
+ * a_boff = NULL, c_nblk = 0: as qf_cgemm_c64_view.
  */
 int qf_cgemm_c64_view2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
                        int64_t strideA, const int64_t *a_boff, int64_t a_nslice, int64_t kin,
                        int64_t rows_a, int64_t s_rows_a, int64_t kout, int64_t s_kout,
                        int64_t rows_b, int64_t s_rows_b, const void *B, int64_t ldb,
                        int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice,
-                       void *C, int64_t ldc, int64_t strideC, float alpha_re, float alpha_im,
-                       float beta_re, float beta_im, void *stream);
+                       void *C, int64_t ldc, int64_t strideC, int64_t c_nblk, int64_t c_bstride,
+                       float alpha_re, float alpha_im, float beta_re, float beta_im,
+                       void *stream);
 
 /*
  * GPU state-vector simulator (complex128), the verification twin of the

@@ -100,7 +100,7 @@ def _declare(lib):
                                     ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                     ctypes.c_float, _c_void_p]
     lib.qf_cgemm_c64_ex2.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64,
-                                     _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p, _c_void_p,
+                                     _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p, _i64, _c_void_p,
                                      _c_void_p, _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p,
                                      _i64, _c_void_p, _i64, _i64,
                                      ctypes.c_float, ctypes.c_float, ctypes.c_float,
@@ -114,7 +114,7 @@ def _declare(lib):
     lib.qf_cgemm_c64_view2.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64, _c_void_p, _i64,
                                        _c_void_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
                                        _c_void_p, _i64, _i64, ctypes.c_int, _c_void_p, _i64,
-                                       _c_void_p, _i64, _i64,
+                                       _c_void_p, _i64, _i64, _i64, _i64,
                                        ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                        ctypes.c_float, _c_void_p]
     lib.qf_cgemm_c64_view.argtypes = [ctypes.c_int, _i64, _i64, _i64, _i64, _c_void_p, _i64,

@@ -75,6 +75,11 @@ struct GemmArgs {
   // a_nslice of them: the TMA-fed kernel reads entry b at slice coordinate
   // a_boff[b] / sA (a bit-string's slice of a tensor whose outputs are open)
   int64_t a_nslice = 0;
+  // C in column blocks (TMA short-K kernel): column n of row m of entry b at
+  // C + b*sC + (n / c_nblk) * c_bstride + m * ldc + n % c_nblk -- the
+  // outputs of several open-output values computed side by side land as
+  // separate [M][c_nblk] blocks (ldc = c_nblk)
+  int64_t c_nblk = 0, c_bstride = 0;
 };
 
 __device__ __forceinline__ int64_t a_row_base(const GemmArgs &g, int64_t r) {

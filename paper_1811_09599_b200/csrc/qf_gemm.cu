@@ -1637,14 +1637,14 @@ int qf_cgemm_c64_ex(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, co
                     int64_t strideB, int opB, const int64_t *b_boff, void *C, int64_t ldc,
                     int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                     float beta_im, void *stream) {
-  return qf_cgemm_c64_ex2(mode, batch, M, N, K, A, lda, strideA, opA, a_boff, a_roff, a_coff, B,
-                          ldb, strideB, opB, b_boff, 0, C, ldc, strideC, alpha_re, alpha_im,
+  return qf_cgemm_c64_ex2(mode, batch, M, N, K, A, lda, strideA, opA, a_boff, 0, a_roff, a_coff,
+                          B, ldb, strideB, opB, b_boff, 0, C, ldc, strideC, alpha_re, alpha_im,
                           beta_re, beta_im, stream);
 }
 
 int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,
                      int64_t lda, int64_t strideA, int opA, const int64_t *a_boff,
-                     const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
+                     int64_t a_nslice, const int32_t *a_roff, const int32_t *a_coff, const void *B, int64_t ldb,
                      int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice, void *C,
                      int64_t ldc, int64_t strideC, float alpha_re, float alpha_im, float beta_re,
                      float beta_im, void *stream) {
@@ -1657,7 +1657,9 @@ int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, c
   const bool c_trans = (mode & QF_C_TRANS) != 0;
   mode &= ~(QF_GATHER_ROWS_UNIT | QF_BOFF_EVEN | QF_BBOFF_EVEN | QF_C_TRANS);
   // with entry-offset tables the batch strides only key the 16-byte paths
-  if (a_boff) strideA = a_even ? 2 : 1;
+  // (a_nslice > 0: a_boff are whole entries of strideA elements, kept)
+  QF_REQUIRE(a_nslice == 0 || (a_boff && strideA > 0 && !a_roff), "gemm_ex2: a_nslice needs a_boff");
+  if (a_boff && !a_nslice) strideA = a_even ? 2 : 1;
   if (b_boff) strideB = b_even ? 2 : 1;
   if (a_roff) {
     lda = std::max<int64_t>(K, 1);
@@ -1667,8 +1669,9 @@ int qf_cgemm_c64_ex2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, c
                  alpha_re, alpha_im, beta_re, beta_im, a_roff, a_coff,
                  rows_unit && a_roff != nullptr, a_boff, b_boff};
   // b_boff values are whole [K][N] slices of a buffer of b_nslice of them:
-  // lets the TMA-fed kernel address B by slice coordinate
+  // lets the TMA-fed kernel address B by slice coordinate (and A likewise)
   g.b_nslice = b_nslice;
+  g.a_nslice = a_nslice;
   g.c_trans = c_trans;
   if (c_trans) {
     QF_REQUIRE(ldc >= std::max<int64_t>(1, M), "gemm_ex: transposed C needs ldc >= M");
@@ -1698,8 +1701,9 @@ int qf_cgemm_c64_view2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
                        int64_t rows_a, int64_t s_rows_a, int64_t kout, int64_t s_kout,
                        int64_t rows_b, int64_t s_rows_b, const void *B, int64_t ldb,
                        int64_t strideB, int opB, const int64_t *b_boff, int64_t b_nslice,
-                       void *C, int64_t ldc, int64_t strideC, float alpha_re, float alpha_im,
-                       float beta_re, float beta_im, void *stream) {
+                       void *C, int64_t ldc, int64_t strideC, int64_t c_nblk, int64_t c_bstride,
+                       float alpha_re, float alpha_im, float beta_re, float beta_im,
+                       void *stream) {
   QF_REQUIRE(kin >= 1 && rows_a >= 1 && kout >= 1 && rows_b >= 1, "gemm_view: empty run");
   QF_REQUIRE(M == rows_a * rows_b && K == kin * kout, "gemm_view: runs do not match M/K");
   QF_REQUIRE(mode == QF_GEMM_AUTO || mode == QF_GEMM_TC3, "gemm_view: tensor-core modes only");
@@ -1711,6 +1715,14 @@ int qf_cgemm_c64_view2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
   QF_REQUIRE(!a_boff || a_nslice > 0, "gemm_view2: a_boff needs a_nslice");
   g.a_boff = a_boff;        // whole entries of strideA elements, TMA slice coordinates
   g.a_nslice = a_boff ? a_nslice : 0;
+  if (c_nblk) {
+    QF_REQUIRE(c_nblk >= 1 && N % c_nblk == 0 && ldc >= c_nblk && c_bstride >= M * ldc &&
+                   strideC >= (N / c_nblk) * c_bstride,
+               "gemm_view2: column blocks must tile N and not overlap");
+    g.c_nblk = c_nblk;
+    g.c_bstride = c_bstride;
+    g.ldc = std::max<int64_t>(N, 1);   // validate() checks a row-major ldc; restored below
+  }
   g.v_kin = kin;
   g.v_ra = rows_a;
   g.v_sra = s_rows_a;
@@ -1720,6 +1732,7 @@ int qf_cgemm_c64_view2(int mode, int64_t batch, int64_t M, int64_t N, int64_t K,
   g.v_srb = s_rows_b;
   int st = qf::validate(g);
   if (st != QF_OK) return st;
+  if (c_nblk) g.ldc = ldc;
   return qf::gemm_tc3(g, qf::as_stream(stream));
 }
 
@@ -1732,8 +1745,8 @@ int qf_cgemm_c64_view(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, 
                       float beta_im, void *stream) {
   return qf_cgemm_c64_view2(mode, batch, M, N, K, A, strideA, nullptr, 0, kin, rows_a, s_rows_a,
                             kout, s_kout, rows_b, s_rows_b, B, ldb, strideB, opB, b_boff,
-                            b_nslice, C, ldc, strideC, alpha_re, alpha_im, beta_re, beta_im,
-                            stream);
+                            b_nslice, C, ldc, strideC, 0, 0, alpha_re, alpha_im, beta_re,
+                            beta_im, stream);
 }
 
 int qf_cgemm_c64_tview(int mode, int64_t batch, int64_t M, int64_t N, int64_t K, const void *A,

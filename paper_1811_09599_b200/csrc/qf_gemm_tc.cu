@@ -2095,7 +2095,27 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[pb]))
                          : "memory");
         }
-        if (g.c_trans) {
+        if (g.c_nblk) {
+          // column blocks: this lane's row, c_nblk consecutive columns per block
+          const int64_t m = m0 + lane;
+          float2 *cb = Cb + (int64_t)ec.bidx * g.sC + m * g.ldc;
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const int64_t n = (int64_t)ec.nt * BN + ch * CH + c;
+            if (ch * CH + c < ntile && m < g.M) {
+              const int64_t q = n / g.c_nblk;
+              const float xr = __uint_as_float(vr[c]), xi = __uint_as_float(vi[c]);
+              float2 o = make_float2(ar * xr - ai * xi, ar * xi + ai * xr);
+              float2 *cp = cb + q * g.c_bstride + (n - q * g.c_nblk);
+              if (use_beta) {
+                const float2 cv = *cp;
+                o.x += br * cv.x - bi * cv.y;
+                o.y += br * cv.y + bi * cv.x;
+              }
+              *cp = o;
+            }
+          }
+        } else if (g.c_trans) {
           // transposed C: column n of these 32 rows is one 256-byte run
           const int64_t m = m0 + lane;
           float2 *ct = Cb + (int64_t)ec.bidx * g.sC + m;
@@ -3531,6 +3551,10 @@ bool tc3_eligible(const GemmArgs &g) {
 int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
   QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
+  if (g.c_nblk && (!g.v_kin || g.K > 128 || g.c_trans)) {
+    set_error("tc3: column-blocked C only on the short-K view kernel");
+    return QF_ERR_UNSUPPORTED;
+  }
   if (g.c_trans && !g.v_t) {
     set_error("tc3: transposed C only on a transposed A view");
     return QF_ERR_UNSUPPORTED;

@@ -1184,7 +1184,7 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
                 ctypes.c_void_p(aoff.data_ptr()), 2 ** len(plan["ao"]), kin, ra, sra, ko, sko,
                 rb, srb, ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
                 ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
-                ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,
+                ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 0, 0, 1.0, 0.0, 0.0, 0.0,
                 stream_handle())
         if st == _lib.QF_ERR_UNSUPPORTED:
             return None
@@ -1202,7 +1202,7 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
                 ctypes.c_void_p(0), 0, kin, ra, sra, ko, sko, rb, srb,
                 ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
                 ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
-                ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,
+                ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 0, 0, 1.0, 0.0, 0.0, 0.0,
                 stream_handle())
         if st == _lib.QF_ERR_UNSUPPORTED:
             return None
@@ -1213,7 +1213,7 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
                 f"b{nb} m{M} n{N} k{K} X" if _timer else ""):
         st = _lib.load().qf_cgemm_c64_ex2(
             _gemm_mode | flags, nb, M, N, K, ctypes.c_void_p(a_buf.data_ptr() + 8 * a_off),
-            max(K, 1), entry, _lib.OP_N, ctypes.c_void_p(0), ctypes.c_void_p(0),
+            max(K, 1), entry, _lib.OP_N, ctypes.c_void_p(0), 0, ctypes.c_void_p(0),
             ctypes.c_void_p(0), ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
             ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
             ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,
@@ -1382,7 +1382,7 @@ def _contract_sliced(a: Tensor, b: Tensor, late: LateBits, tail=(), lead=(),
             return lib.qf_cgemm_c64_ex2(
                 _gemm_mode | flags | (_lib.C_TRANS if trans else 0), nb, m, n, k,
                 vp(a_buf.data_ptr() + 8 * a_off), lda, entry_a, opA,
-                vp(a_boff.data_ptr() if a_boff is not None else 0),
+                vp(a_boff.data_ptr() if a_boff is not None else 0), 0,
                 vp(roff.data_ptr() if roff is not None else 0),
                 vp(coff.data_ptr() if coff is not None else 0),
                 vp(B.data.data_ptr()), ldb, sB, opB,
