@@ -171,8 +171,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # nvidia-smi takes ~0.1-0.5 s to start: block until it samples, so a
+            # timed region of a few tens of ms is still covered (20 ms period)
+            self.first = self.proc.stdout.readline()
         except OSError:
             self.proc = None
         return self
@@ -186,7 +189,7 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            self.lines = [l for l in [getattr(self, "first", "")] + out.splitlines() if l.strip()]
         return False
 
     def summary(self) -> dict:

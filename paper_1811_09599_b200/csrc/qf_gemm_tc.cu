@@ -2095,7 +2095,22 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[pb]))
                          : "memory");
         }
-        if (g.c_nblk) {
+        if (g.c_nblk && !use_beta && g.c_nblk % 2 == 0 && g.ldc % 2 == 0 && g.c_bstride % 2 == 0) {
+          // column blocks, 16-byte stores: a column pair never straddles a block
+          const int64_t m = m0 + lane;
+          float2 *cb = Cb + (int64_t)ec.bidx * g.sC + m * g.ldc;
+#pragma unroll
+          for (int c = 0; c < CH; c += 2) {
+            const int64_t n = (int64_t)ec.nt * BN + ch * CH + c;
+            if (ch * CH + c < ntile && m < g.M) {
+              const int64_t q = n / g.c_nblk;
+              const float xr = __uint_as_float(vr[c]), xi = __uint_as_float(vi[c]);
+              const float yr = __uint_as_float(vr[c + 1]), yi = __uint_as_float(vi[c + 1]);
+              *reinterpret_cast<float4 *>(cb + q * g.c_bstride + (n - q * g.c_nblk)) =
+                  make_float4(ar * xr - ai * xi, ar * xi + ai * xr, ar * yr - ai * yi, ar * yi + ai * yr);
+            }
+          }
+        } else if (g.c_nblk) {
           // column blocks: this lane's row, c_nblk consecutive columns per block
           const int64_t m = m0 + lane;
           float2 *cb = Cb + (int64_t)ec.bidx * g.sC + m * g.ldc;

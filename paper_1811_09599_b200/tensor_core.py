@@ -1057,13 +1057,26 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
     bo, bo2 = late.outs(op), late.outs(op2)
     if not bo or not bo2 or lb in op.labels or lb in op2.labels:
         return None
+    sliced = False
     if acc.labels and lb not in acc.labels and late.outs(acc):
-        return _expand_plan_open(acc, op, op2, late, tail2, bo, bo2)
-    if not acc.labels or acc.labels[0] != lb or late.outs(acc) or acc._data is None:
+        r = _expand_plan_open(acc, op, op2, late, tail2, bo, bo2)
+        if r is not None:
+            return r
+        # an open operand the reference slices per bit-string: its slices
+        # are the entries (TMA slice coordinates), like a batched operand
+        ao = late.outs(acc)
+        if (2 ** len(ao) <= late.limit or set(acc.labels[:len(ao)]) != set(ao)
+                or acc._data is None):
+            return None
+        sliced = True
+    elif not acc.labels or acc.labels[0] != lb or late.outs(acc) or acc._data is None:
         return None
-    if any(_is_batch(l) for l in acc.labels[1:] + op.labels + op2.labels):
+    if any(_is_batch(l) for l in op.labels + op2.labels):
         return None
-    core, cdims = list(acc.labels[1:]), list(acc.dims[1:])
+    lead = len(late.outs(acc)) if sliced else 1
+    if any(_is_batch(l) for l in acc.labels[lead:]):
+        return None
+    core, cdims = list(acc.labels[lead:]), list(acc.dims[lead:])
     cset, oset, o2set = set(core), set(op.labels), set(op2.labels)
     j = [l for l in core if l in oset]
     ko = [l for l in core if l in o2set]
@@ -1090,7 +1103,8 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
     dim.update(zip(op.labels, op.dims))
     dim.update(zip(op2.labels, op2.dims))
     P = lambda ls: math.prod(dim[l] for l in ls)
-    M, K, N, nb = P(rb), P(ko) * P(j), P(ra) * P(w_free), acc.dims[0]
+    M, K, N = P(rb), P(ko) * P(j), P(ra) * P(w_free)
+    nb = late.nb if sliced else acc.dims[0]
     # the re-associated product must not cost more than the reference's two
     # contractions, and the per-combination blocks must stay small
     fused = M * K * N
@@ -1101,7 +1115,7 @@ def expand_plan(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", tail2=()
     u = ShapeOnly((lb,) + tuple(u_lab), (nb,) + tuple(dim[l] for l in u_lab))
     return {"j": j, "rb": rb, "ko": ko, "ra": ra, "ki": ki, "w_free": w_free, "bo": bo,
             "bo2": bo2, "M": M, "K": K, "N": N, "nb": nb, "u": u, "k_order": k_order,
-            "view": view,
+            "view": view, "sliced": sliced,
             "labels": (lb,) + tuple(rb + ra + w_free),
             "dims": (nb,) + tuple(dim[l] for l in rb + ra + w_free)}
 
@@ -1155,6 +1169,18 @@ def _expand_plan_open(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits", ta
         return None
     u_lab = ao + rows + ko + bo + ra + ki
     u = ShapeOnly(tuple(u_lab), tuple(dim[l] for l in u_lab))
+    # every (acc slice, op/op2 output) combination at most as many as the
+    # bit-strings: compute them all with the result's outputs kept open --
+    # each acc slice read once (the op . op2 blocks side by side as column
+    # blocks of one B) instead of once per bit-string
+    keep = (2 ** (len(ao) + len(bo) + len(bo2)) <= nb and K <= 128
+            and 2 ** (len(bo) + len(bo2)) * N <= 256)
+    if keep:
+        lab = ao + bo + bo2 + rows + ra + w_free
+        return {"open": True, "keep_open": True, "view": view, "ao": ao, "k_order": k_order,
+                "j": j, "rb": rows, "ko": ko, "ra": ra, "ki": ki, "w_free": w_free, "bo": bo,
+                "bo2": bo2, "M": M, "K": K, "N": N, "nb": nb, "u": u, "labels": tuple(lab),
+                "dims": tuple(dim[l] for l in lab)}
     return {"open": True, "view": view, "ao": ao, "k_order": k_order, "j": j, "rb": rows,
             "ko": ko, "ra": ra, "ki": ki, "w_free": w_free, "bo": bo, "bo2": bo2, "M": M,
             "K": K, "N": N, "nb": nb, "u": u, "labels": (lb,) + tuple(rows + ra + w_free),
@@ -1171,6 +1197,30 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
     V = V.transpose_to(tuple(plan["bo"] + plan["bo2"] + k_order + plan["ra"] + plan["w_free"]))
     off = late.offsets(V, plan["bo"] + plan["bo2"])
     M, N, K, nb = plan["M"], plan["N"], plan["K"], plan["nb"]
+    if plan.get("keep_open"):
+        # all combinations: batch = acc's slices, B = every op . op2 block side
+        # by side ([K][blocks x N]), C stored as [slice][block][M][N]
+        nsl = 2 ** len(plan["ao"])
+        nblk = 2 ** (len(plan["bo"]) + len(plan["bo2"]))
+        V = V.transpose_to(tuple(k_order + plan["bo"] + plan["bo2"] + plan["ra"] +
+                                 plan["w_free"]))
+        entry = acc.size // nsl
+        kin, ra, sra, ko, sko, rb, srb = plan["view"]
+        out = device_buffer(nsl * nblk * M * N, acc.buf.dtype, acc.buf.device)
+        zeros = _zero_offsets(nsl, acc.buf.device)
+        NT = nblk * N
+        with _timed("gemm", 8 * nsl * M * NT * K, 8 * nsl * (M * K + K * NT + M * NT),
+                    f"b{nsl} m{M} n{NT} k{K} XK" if _timer else ""):
+            st = _lib.load().qf_cgemm_c64_view2(
+                _gemm_mode, nsl, M, NT, K, ctypes.c_void_p(acc.data.data_ptr()), entry,
+                ctypes.c_void_p(0), 0, kin, ra, sra, ko, sko, rb, srb,
+                ctypes.c_void_p(V.data.data_ptr()), NT, 0, _lib.OP_N,
+                ctypes.c_void_p(zeros.data_ptr()), 1, ctypes.c_void_p(out.data_ptr()), N,
+                nblk * M * N, N, M * N, 1.0, 0.0, 0.0, 0.0, stream_handle())
+        if st == _lib.QF_ERR_UNSUPPORTED:
+            return None
+        _lib.check(st, "gemm_expand_keep")
+        return Tensor(plan["labels"], out, plan["dims"])
     if plan.get("open"):
         # each bit-string's slice of acc read in place as a TMA view
         aoff = late.offsets(acc, plan["ao"])
@@ -1190,7 +1240,15 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
             return None
         _lib.check(st, "gemm_expand_open")
         return Tensor(plan["labels"], out, plan["dims"])
-    a_buf, a_off, entry = acc.raw()
+    if plan.get("sliced"):
+        # acc's per-bit-string slices (open outputs leading) as entries
+        a_buf, a_off = acc.data, 0
+        entry = acc.size // (2 ** len(late.outs(acc)))
+        a_boff, a_nsl = late.offsets(acc, late.outs(acc)), 2 ** len(late.outs(acc))
+    else:
+        a_buf, a_off, entry = acc.raw()
+        a_boff, a_nsl = None, 0
+    vp = ctypes.c_void_p
     out = device_buffer(nb * M * N, acc.buf.dtype, acc.buf.device)
     if plan.get("view") is not None:
         # batched entries read as a TMA view (k split around a free run)
@@ -1199,8 +1257,8 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
                     f"b{nb} m{M} n{N} k{K} XV" if _timer else ""):
             st = _lib.load().qf_cgemm_c64_view2(
                 _gemm_mode, nb, M, N, K, ctypes.c_void_p(a_buf.data_ptr() + 8 * a_off), entry,
-                ctypes.c_void_p(0), 0, kin, ra, sra, ko, sko, rb, srb,
-                ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
+                vp(a_boff.data_ptr() if a_boff is not None else 0), a_nsl, kin, ra, sra, ko,
+                sko, rb, srb, ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
                 ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
                 ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 0, 0, 1.0, 0.0, 0.0, 0.0,
                 stream_handle())
@@ -1213,7 +1271,8 @@ def contract_late_expand(acc: Tensor, op: Tensor, op2: Tensor, late: "LateBits",
                 f"b{nb} m{M} n{N} k{K} X" if _timer else ""):
         st = _lib.load().qf_cgemm_c64_ex2(
             _gemm_mode | flags, nb, M, N, K, ctypes.c_void_p(a_buf.data_ptr() + 8 * a_off),
-            max(K, 1), entry, _lib.OP_N, ctypes.c_void_p(0), 0, ctypes.c_void_p(0),
+            max(K, 1), entry, _lib.OP_N, vp(a_boff.data_ptr() if a_boff is not None else 0),
+            a_nsl, ctypes.c_void_p(0),
             ctypes.c_void_p(0), ctypes.c_void_p(V.data.data_ptr()), max(N, 1), 0, _lib.OP_N,
             ctypes.c_void_p(off.data_ptr()), V.size // max(K * N, 1),
             ctypes.c_void_p(out.data_ptr()), max(N, 1), M * N, 1.0, 0.0, 0.0, 0.0,

@@ -661,7 +661,9 @@ def test_reassociated_expansion_open_operand(nb, ra):
     assert plan is not None and plan.get("open")
     with tc.KernelTimer() as kt:
         got = tc.contract_late_expand(ta, ts, tw, late, plan)
-    assert got is not None and any(" XO" in k for k in kt.summary(detail=True))
+    assert got is not None and any(" XO" in k or " XK" in k for k in kt.summary(detail=True))
+    if plan.get("keep_open"):           # outputs kept open: slice the bit-strings out
+        got = late.batch(got)
     u = tc.contract_late(ta, ts, late, tail=("ko", "u", "w", "out3"))
     want = tc.contract_late(u, tw, late)
     w = want.transpose_to(got.labels).array
@@ -706,5 +708,41 @@ def test_reassociated_expansion_view_operand(nb, wide):
     assert got is not None and any(" XV" in k for k in kt.summary(detail=True))
     u = tc.contract_late(ta, ts, late, tail=("r", "u", "v", "out1"))
     want = tc.contract_late(u, tw, late)
+    w = want.transpose_to(got.labels).array
+    assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+
+
+@pytest.mark.parametrize("nb", [64, 300])
+def test_reassociated_expansion_keeps_outputs_open(nb):
+    """expand_plan on an open operand when every (slice, output) combination
+    is at most the bit-string count: all combinations in one pass with the
+    outputs kept open (column-blocked C through qf_cgemm_c64_view2), then the
+    next re-associated pair reads its per-bit-string slices by TMA slice
+    coordinate (qf_cgemm_c64_ex2 a_nslice) -- equal to the plain late walk."""
+    rng = np.random.default_rng(1600 + nb)
+    A = _rand(rng, (2, 2, 8, 16, 8, 8, 8), np.complex64)        # o0 o1 p q j r ko
+    S = _rand(rng, (8, 8, 2), np.complex64)                     # j u out2
+    W = _rand(rng, (8, 8, 8, 2), np.complex64)                  # ko u w out3
+    S2 = _rand(rng, (8, 4, 8, 2), np.complex64)                 # w x y out4
+    W2 = _rand(rng, (8, 8, 8, 2), np.complex64)                 # r y z out5
+    bits = rng.integers(0, 2, size=(6, nb)).astype(np.int32)
+    late = tc.LateBits(torch.from_numpy(bits).cuda(),
+                       {"o0": 0, "o1": 1, "out2": 2, "out3": 3, "out4": 4, "out5": 5}, limit=8)
+    ta = tc.Tensor(["o0", "o1", "p", "q", "j", "r", "ko"], A)
+    ts, tw = tc.Tensor(["j", "u", "out2"], S), tc.Tensor(["ko", "u", "w", "out3"], W)
+    ts2, tw2 = tc.Tensor(["w", "x", "y", "out4"], S2), tc.Tensor(["r", "y", "z", "out5"], W2)
+    plan = tc.expand_plan(ta, ts, tw, late)
+    assert plan is not None and plan.get("keep_open")
+    with tc.KernelTimer() as kt:
+        t_open = tc.contract_late_expand(ta, ts, tw, late, plan)
+        plan2 = tc.expand_plan(t_open, ts2, tw2, late)
+        assert plan2 is not None and plan2.get("sliced")
+        got = tc.contract_late_expand(t_open, ts2, tw2, late, plan2)
+    kinds = kt.summary(detail=True)
+    assert any(" XK" in k for k in kinds) and got is not None, kinds
+    u = tc.contract_late(ta, ts, late, tail=("ko", "u", "w", "out3"))
+    t = tc.contract_late(u, tw, late)
+    u2 = tc.contract_late(t, ts2, late, tail=("r", "y", "z", "out5"))
+    want = tc.contract_late(u2, tw2, late)
     w = want.transpose_to(got.labels).array
     assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
