@@ -1561,8 +1561,10 @@ __device__ __forceinline__ void stage_store_chunk(uint8_t *stg, const uint32_t (
 #pragma unroll
     for (int i = 0; i < 32 / RPI; ++i) {
       const int r = RPI * i + rs;
-      *reinterpret_cast<float4 *>(c + r * ldc + 2 * cc) =
-          *reinterpret_cast<const float4 *>(stg + r * PITCH + cc * 16);
+      // streaming (evict-first) stores: big results do not push the operands
+      // that later tiles re-read (A tiles across N tiles) out of L2
+      __stcs(reinterpret_cast<float4 *>(c + r * ldc + 2 * cc),
+             *reinterpret_cast<const float4 *>(stg + r * PITCH + cc * 16));
     }
     __syncwarp();
     return;
