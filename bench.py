@@ -490,6 +490,7 @@ def run_permute(args):
     pk = peaks()
     sizes = [int(s) for s in args.perm_sizes.split(",")]
     per_size = {}
+    eager = {s: [] for s in sizes}
     launches = 0
     for log2n in sizes:
         n = 1 << log2n
@@ -509,6 +510,27 @@ def run_permute(args):
             torch.cuda.synchronize()
             launches += _lib.launch_count(reset=True)
             ms = a.elapsed_time(b) / args.steps
+            eager[log2n].append(16 * n / ms / 1e6)
+            if args.perm_graph:
+                # the K launches replayed from one CUDA graph: no host gaps
+                # between back-to-back 40-60 us launches at 2^24
+                g = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream()
+                cs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cs), torch.cuda.graph(g, stream=cs):
+                    for _ in range(args.steps):
+                        tc.permute_buffer(src, dims, perm, out=dst)
+                torch.cuda.current_stream().wait_stream(cs)
+                _lib.launch_count(reset=True)
+                g.replay()
+                torch.cuda.synchronize()
+                a.record()
+                g.replay()
+                b.record()
+                torch.cuda.synchronize()
+                launches += args.steps
+                ms = a.elapsed_time(b) / args.steps
+                del g
             rates["binary" if i < args.perms // 2 else "mixed"].append(16 * n / ms / 1e6)
             if i in (0, args.perms // 2):  # spot-check bytes against index arithmetic
                 idx = torch.randint(0, n, (4096,), device="cuda")
@@ -526,9 +548,10 @@ def run_permute(args):
                                       "max_gbs": round(float(np.max(v)), 1),
                                       "frac_mean": round(float(np.mean(v)) / pk["hbm_gbs"], 4)}
                                   for k, v in rates.items() if v}
+        per_size[f"2^{log2n}"]["eager_mean_gbs"] = round(float(np.mean(eager[log2n])), 1)
         del src, dst
         torch.cuda.empty_cache()
-    allv = [d["mean_gbs"] for s in per_size.values() for d in s.values()]
+    allv = [d["mean_gbs"] for s in per_size.values() for d in s.values() if isinstance(d, dict)]
     value = float(np.mean(allv))
     return {"metric": "permutation GB/s (config 3)", "value": round(value, 1), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -536,7 +559,9 @@ def run_permute(args):
             "data": "synthetic i.i.d. complex normal", "config": {
                 "workload": f"config3: {args.perms} seeded perms per size "
                             f"(half binary dims, half mixed 2/4/8/16), sizes 2^{sizes}",
-                "l2": "inputs larger than L2 (>= 256 MiB)"},
+                "l2": "inputs larger than L2 (>= 256 MiB)",
+                "timing": "K launches replayed from one CUDA graph" if args.perm_graph
+                          else "K eager launches"},
             "roofline": {"bound": "hbm", "unit": "GB/s", "kernel": "permute_tiled",
                          "achieved": round(value, 1), "peak": pk["hbm_gbs"],
                          "frac": round(value / pk["hbm_gbs"], 4), "traffic": None,
@@ -679,6 +704,8 @@ def main(argv=None):
     ap.add_argument("--paths", type=int, default=4, help="paths timed for config4/config5")
     ap.add_argument("--perm-sizes", default="24,28,30")
     ap.add_argument("--perms", type=int, default=64)
+    ap.add_argument("--perm-graph", type=int, default=1,
+                    help="time the K permutes of a case as one CUDA-graph replay (1) or eagerly (0)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
