@@ -8,7 +8,7 @@
 // Design (B200-first, HBM-bound): one pass, every element crosses HBM once
 // in each direction.
 //   1. Normalise: drop unit axes, fuse axes adjacent in both layouts.
-//   2. Pick the tile: A = innermost INPUT axes with >= TA elements (reads
+//   2. Pick the tile: A = innermost INPUT axes with >= TA elements (256 B; reads
 //      become contiguous runs), B = innermost OUTPUT axes with >= TB
 //      elements (writes become contiguous runs).  An axis straddling the
 //      threshold is split (d -> d/f x f) so tiles stay small; power-of-two
@@ -443,8 +443,18 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
     return QF_OK;
   }
 
-  const int64_t TA = 512 / elem_bytes, TB = 512 / elem_bytes;
-  const int64_t Tmin = 32768 / elem_bytes, Tmax = 32768 / elem_bytes;  // 32 KB tiles (measured: 16 KB tiles ran ~20% slower)
+  // run lengths and tile size in bytes; QF_PERM_TA / QF_PERM_TB / QF_PERM_TILE
+  // override them (tuning experiments only)
+  auto knob = [](const char *name, int64_t dflt) {
+    const char *v = getenv(name);
+    return v ? (int64_t)atoll(v) : dflt;
+  };
+  // 256-byte runs: a 64 x 64 element tile with disjoint A/B (512-byte runs)
+  // ran at 4.85 TB/s; 32-element runs let A grow to 128 inputs while B keeps
+  // whole 256-byte output sectors (6.1-6.2 TB/s, profiles/r1n_permute_knobs.txt)
+  const int64_t TA = knob("QF_PERM_TA", 256) / elem_bytes, TB = knob("QF_PERM_TB", 256) / elem_bytes;
+  const int64_t Tmin = knob("QF_PERM_TILE", 32768) / elem_bytes,
+                Tmax = Tmin;  // 32 KB tiles (measured: 16 KB tiles ran ~20% slower)
 
   // 3. A = innermost input axes [a_start, r)
   int r = L.rank();
