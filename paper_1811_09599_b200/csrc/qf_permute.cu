@@ -445,9 +445,10 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
 
   // run lengths and tile size in bytes; QF_PERM_TA / QF_PERM_TB / QF_PERM_TILE
   // override them (tuning experiments only)
-  auto knob = [](const char *name, int64_t dflt) {
+  auto knob = [](const char *name, int64_t dflt) {  // clamped to sane byte counts
     const char *v = getenv(name);
-    return v ? (int64_t)atoll(v) : dflt;
+    const int64_t x = v ? (int64_t)atoll(v) : dflt;
+    return std::min<int64_t>(std::max<int64_t>(x, 64), 65536);
   };
   // 256-byte runs: a 64 x 64 element tile with disjoint A/B (512-byte runs)
   // ran at 4.85 TB/s; 32-element runs let A grow to 128 inputs while B keeps
