@@ -335,6 +335,38 @@ int qf_cgemm_c64_rowblocks(int mode, int64_t batch, int64_t M, int64_t N, int64_
  * the previous one.  QF_GEMM_FFMA calls never use the tensor-core twin. */
 int qf_rowmma(int enabled);
 
+/*
+ * Path sums and the multi-GPU slice collective.  The
+ * reference sums paths sequentially in one process
+ * (rq/amplitude_engine.py:123 single amplitudes, :153-157 open-qubit
+ * batches); a multi-GPU run gives every rank a contiguous share of the path
+ * list and combines the partial amplitudes with ONE all-reduce.
+ *
+ * NCCL is resolved at run time (the copy already loaded in the process, else
+ * $QF_NCCL_LIB, else libnccl.so.2); the library has no link-time NCCL
+ * dependency.  One communicator per (process group, device):
+ *   rank 0: qf_nccl_unique_id(uid, 128) -> broadcast uid by the host ->
+ *   every rank: qf_nccl_init(uid, nranks, rank, dev, &handle).
+ * qf_allreduce_c64 sums `count` complex64 values (as 2*count float32) in
+ * place across the communicator's ranks, enqueued on `stream`.
+ */
+int qf_nccl_available(void);  /* 1 if an NCCL library can be bound, else 0 */
+int qf_nccl_unique_id(void *uid, int64_t nbytes);
+int qf_nccl_init(const void *uid, int nranks, int rank, int dev, int *handle);
+int qf_nccl_destroy(int handle);
+int qf_allreduce_c64(int handle, void *buf, int64_t count, void *stream);
+
+/* y[i] += alpha * x[i], complex64, i in [0, n) -- one path's partial
+ * amplitudes added into the running sum (rq/amplitude_engine.py:123,157). */
+int qf_axpy_c64(int64_t n, float alpha_re, float alpha_im, const void *x, void *y, void *stream);
+
+/* out[b] = sum_i x[b*stride_x + i] * y[b*stride_y + i] (no conjugation),
+ * complex64, b in [0, batch): the final `result` step of a plan, the dot of
+ * two open region tensors (rq/contraction_plan.py:477-523 folding the last
+ * pair, rq/tensor_core.py:391-419 with every label shared). */
+int qf_dot_c64(int64_t batch, int64_t n, const void *x, int64_t stride_x, const void *y,
+               int64_t stride_y, void *out, void *stream);
+
 /* Name of the last kernel this library launched on the calling thread
  * (static string; "" if none) -- lets profilers attribute timings. */
 const char *qf_last_kernel(void);

@@ -41,6 +41,8 @@ EXPORTS = (
     "qf_fill_zero", "qf_tc3_set_variant", "qf_last_kernel",
     "qf_small_engine", "qf_rowmma", "qf_cgemm_c64_rowblocks",
     "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
+    "qf_nccl_available", "qf_nccl_unique_id", "qf_nccl_init", "qf_nccl_destroy",
+    "qf_allreduce_c64", "qf_axpy_c64", "qf_dot_c64",
 )
 
 
@@ -151,6 +153,15 @@ def _declare(lib):
     lib.qf_last_kernel.argtypes = []
     lib.qf_workspace_reserve.argtypes = [_i64, _c_void_p]
     lib.qf_workspace_release.argtypes = []
+    lib.qf_nccl_available.argtypes = []
+    lib.qf_nccl_unique_id.argtypes = [_c_void_p, _i64]
+    lib.qf_nccl_init.argtypes = [_c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.POINTER(ctypes.c_int)]
+    lib.qf_nccl_destroy.argtypes = [ctypes.c_int]
+    lib.qf_allreduce_c64.argtypes = [ctypes.c_int, _c_void_p, _i64, _c_void_p]
+    lib.qf_axpy_c64.argtypes = [_i64, ctypes.c_float, ctypes.c_float, _c_void_p, _c_void_p,
+                                _c_void_p]
+    lib.qf_dot_c64.argtypes = [_i64, _i64, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]
     lib.qf_launch_count.argtypes = [ctypes.c_int]
     lib.qf_launch_count.restype = _i64
     for name in EXPORTS:
@@ -201,3 +212,62 @@ def perm_array(perm: Sequence[int]):
 
 def launch_count(reset: bool = False) -> int:
     return int(load().qf_launch_count(1 if reset else 0))
+
+
+# -- multi-GPU slice collective (qf_nccl_* / qf_allreduce_c64) ----------------
+
+NCCL_UID_BYTES = 128
+
+
+def _current_stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 of a group draws it; the host
+    broadcasts the bytes to the other ranks)."""
+    buf = ctypes.create_string_buffer(NCCL_UID_BYTES)
+    check(load().qf_nccl_unique_id(buf, NCCL_UID_BYTES), "nccl_unique_id")
+    return buf.raw
+
+
+def nccl_init(uid: bytes, nranks: int, rank: int, device: int) -> int:
+    """Join the communicator named by `uid` as `rank` of `nranks` on
+    `device`; returns the library handle (collective over all ranks)."""
+    if len(uid) != NCCL_UID_BYTES:
+        raise ValueError(f"NCCL unique id must be {NCCL_UID_BYTES} bytes, got {len(uid)}")
+    h = ctypes.c_int(-1)
+    buf = ctypes.create_string_buffer(uid, NCCL_UID_BYTES)
+    check(load().qf_nccl_init(buf, int(nranks), int(rank), int(device), ctypes.byref(h)),
+          "nccl_init")
+    return int(h.value)
+
+
+def nccl_destroy(handle: int):
+    check(load().qf_nccl_destroy(int(handle)), "nccl_destroy")
+
+
+def allreduce_c64(handle: int, buf, count: int):
+    """In-place sum of `count` complex64 values of a device buffer over the
+    communicator, on the current CUDA stream."""
+    check(load().qf_allreduce_c64(int(handle), ctypes.c_void_p(buf.data_ptr()), int(count),
+                                  _current_stream()), "allreduce_c64")
+
+
+def axpy_c64(x, y, alpha: complex = 1.0, n: Optional[int] = None):
+    """y[:n] += alpha * x[:n] on the device (complex64)."""
+    n = int(x.numel()) if n is None else int(n)
+    a = complex(alpha)
+    check(load().qf_axpy_c64(n, a.real, a.imag, ctypes.c_void_p(x.data_ptr()),
+                             ctypes.c_void_p(y.data_ptr()), _current_stream()), "axpy_c64")
+
+
+def dot_c64(x, y, out, batch: int, n: int, stride_x: Optional[int] = None,
+            stride_y: Optional[int] = None):
+    """out[b] = sum_i x[b, i] * y[b, i] on the device (complex64)."""
+    sx = n if stride_x is None else int(stride_x)
+    sy = n if stride_y is None else int(stride_y)
+    check(load().qf_dot_c64(int(batch), int(n), ctypes.c_void_p(x.data_ptr()), sx,
+                            ctypes.c_void_p(y.data_ptr()), sy, ctypes.c_void_p(out.data_ptr()),
+                            _current_stream()), "dot_c64")

@@ -10,9 +10,10 @@ device-side:
     tensor, so each pairwise contraction is one batched GEMM.
   * `amplitude_batches(...)` -- the same for the open-qubit batch mode
     (many s_AB at once).
-  * multi-GPU: with torch.distributed initialised (one process per GPU),
-    each rank sums a contiguous chunk of the path list and one NCCL
-    all-reduce combines the partial amplitudes (`slices.py`).
+  * multi-GPU: `AmplitudeEngine(..., group=<process group>)` (one process
+    per GPU) gives each rank a contiguous chunk of the path list and one
+    all-reduce combines the partial amplitudes (`slices.py`); the default
+    group=None walks every path in this process.
 
 Results return to the host once per call (complex / numpy arrays), exactly
 the types the reference returns.
@@ -212,6 +213,8 @@ class AmplitudeEngine:
                             else torch.complex128)
         zero_buffer(acc)
         gi = ex.group_cut() if _path_batching else None
+        lo, _ = shard.range(len(paths))
+        first = True
         for grp in _path_groups(shard.take(paths), gi):
             if gi is not None and [p[gi] for p in grp] == list(range(ex.cut_dims[gi])):
                 try:
@@ -222,9 +225,17 @@ class AmplitudeEngine:
                     PATH_GROUPS_RUN[0] += 1
                     t = sum_path_axis(t, rep, keep_batch=t.dims[0] // rep > 1)
                     accumulate_buffer(finish(t), acc, size)
+                    if first and lo > 0:
+                        ex.flops -= ex.reuse_credit(paths[lo - 1], paths[lo])
+                    first = False
                     continue
             for p in grp:
                 accumulate_buffer(finish(ex.run(p)), acc, size)
+                if first and lo > 0:
+                    # a sequential walk would have reused these steps from the
+                    # previous rank's last path: book the flops only once
+                    ex.flops -= ex.reuse_credit(paths[lo - 1], paths[lo])
+                first = False
         return acc
 
     def _sum_paths(self, ex: PlanExecutor, paths, finish, size: int):

@@ -2163,8 +2163,11 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     uint32_t boff;
     constexpr int BE = (BN * KB) / NT;  // B elements per thread per k-block (BN = 64)
     if constexpr (BE == 2) {
-      const int b_kp = tid & 1, b_chunk = tid >> 7;
-      b_n = (tid >> 1) & (BN - 1);
+      // half-warps split by k pair: each half reads one contiguous 128-byte
+      // run of a k row of the raw B box (conflict-free), the B' stores of the
+      // two halves interleave 8-byte words of the same core-matrix rows
+      const int b_kp = (tid >> 4) & 1, b_chunk = tid >> 7;
+      b_n = (tid & 15) | (((tid >> 5) & 3) << 4);
       b_k = b_chunk * 4 + b_kp * 2;
       boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
     } else {
@@ -3638,6 +3641,8 @@ int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
   // long K: a TMA producer warp, 8 converter warps, 4 promotion warps with a
   // TMEM master accumulator (cp.async fetch by the converters when TMA
   // cannot describe the operands)
+  if (g_tc3_variant == 26 && tc::tma_ok(g)) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true>(g, s);
+  if (g_tc3_variant == 27 && tc::tma_ok(g)) return tc::launch_short<4, 8, 8, 4, 64, 32, 1, true>(g, s);
   if (g_tc3_variant != 13 && tc::tma_ok(g)) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
   return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
 }

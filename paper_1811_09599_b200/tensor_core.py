@@ -74,6 +74,14 @@ def set_gemm_mode(mode: str) -> str:
     return prev
 
 
+def tc3_real_macs_per_complex_mac() -> int:
+    """Real TF32 MMA multiply-adds the tensor-core engine issues per complex
+    multiply-add: 4 real products x 3 (hi*hi + hi*lo + lo*hi) = 12 in the
+    real-block form (the 3xTF32 ceiling is then TF32_peak / 3 in algorithmic
+    8-flop complex MACs)."""
+    return 12
+
+
 def get_gemm_mode() -> str:
     return next(k for k, v in _GEMM_MODES.items() if v == _gemm_mode)
 

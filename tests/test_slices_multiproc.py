@@ -30,7 +30,14 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        shard = slices.current_shard()
+        # group=None never shards or reduces, even with the process group up
+        assert slices.current_shard() == slices.SliceShard(0, 1)
+        solo = torch.tensor([complex(rank + 1, 0)], dtype=torch.complex64)
+        slices.reduce_partials(solo)
+        assert solo.item() == complex(rank + 1, 0)
+        assert slices.reduce_int(rank + 1) == rank + 1
+        group = dist.group.WORLD
+        shard = slices.current_shard(group)
         paths = enumerate_paths((8, 4), f=0.5, seed=3)
         mine = shard.take(paths)
         # partial "amplitudes": a deterministic function of the path
@@ -38,8 +45,8 @@ def _worker(rank, world, port, q):
         for p in mine:
             part += torch.tensor([complex(p[0], p[1]), complex(1, 0), complex(p[0] * p[1], -1)],
                                  dtype=torch.complex64)
-        slices.reduce_partials(part)
-        flops = slices.reduce_int(len(mine) * 10)
+        slices.reduce_partials(part, group)
+        flops = slices.reduce_int(len(mine) * 10, group)
         q.put((rank, mine, part.numpy(), flops))
     finally:
         dist.destroy_process_group()
