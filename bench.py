@@ -595,14 +595,14 @@ def run_permute(args):
 
 PATH_WORKLOADS = {
     "config4": {
-        "lattice": "grid:7x7", "depth": "1+40+1", "plan": "grid:7x7", "f": 1 / 64, "open": 0,
+        "lattice": "grid:7x7", "depth": "1+40+1", "plan": "grid:7x7:slice-first", "f": 1 / 64, "open": 0,
         "units": 256, "amps_per_unit": 1, "cpu_depth": "1+28+1",
         "desc": "config4: grid:7x7 RQC 1+40+1 (bond 32), slice-first plan with the reference's "
                 "cuts (right 19:26, bottom 37:38; 1024 slices), f=1/64 (16 seeded paths per "
                 "amplitude), 256 seeded bit-strings walked in order",
     },
     "config5": {
-        "lattice": "bristlecone-70", "depth": "1+32+1", "plan": "bristlecone-70", "f": 0.005,
+        "lattice": "bristlecone-70", "depth": "1+32+1", "plan": "bristlecone-70:slice-first", "f": 0.005,
         "open": 6, "units": 1000, "amps_per_unit": 64, "cpu_depth": "1+24+1",
         "desc": "config5: bristlecone-70 RQC 1+32+1 (bond 16), slice-first plan with the "
                 "reference's cuts w0..w3 (65536 slices), f=0.005 (328 seeded paths per batch), "
@@ -768,7 +768,12 @@ def run_paths(args):
                 raise AssertionError(f"N>1 self-check failed: {selfcheck}")
         barrier(world)
 
-    # ---- end to end through the public API (host in, host out)
+    # ---- end to end through the public API (host in, host out); the timed
+    # walk's cached intermediates (up to ~70 GiB at config 4) are released
+    # first so the API call has the device to itself
+    state.update(ex=None, acc=None, results=[], contrib={})
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     h2d = d2h = 0
     e2e_s = []
     for u in range(max(1, args.e2e_units)):

@@ -19,7 +19,7 @@ from .circuits import (Circuit, CircuitFormatError, DepthSpec, Gate, Lattice, cr
 from .contraction_plan import (ContractionPlan, CostEstimate, CutSpec, ContractStep, PlanError,
                                PlanExecutor, builtin_plan, enumerate_paths, estimate_cost,
                                execute_plan, format_plan, grid_plan, load_plan, parse_plan,
-                               two_region_plan)
+                               shipped_plans, slice_first_plan, two_region_plan)
 from .network_builder import Net2D, Net3D, build_3d, contract_grid, contract_time, gate_tensor
 from .sampler import (SampleRun, SamplerConfig, SamplingErrorReport, accept_probability,
                       circuit_batches, estimate_sampling_error, frugal_sample, required_batches,
@@ -41,7 +41,7 @@ __all__ = [
     "Net2D", "Net3D", "build_3d", "contract_time", "contract_grid", "gate_tensor",
     "ContractionPlan", "CutSpec", "ContractStep", "PlanError", "MemoryBudgetError",
     "PlanExecutor", "CostEstimate", "parse_plan", "format_plan", "builtin_plan", "grid_plan",
-    "two_region_plan", "load_plan", "enumerate_paths", "execute_plan", "estimate_cost",
+    "two_region_plan", "load_plan", "shipped_plans", "slice_first_plan", "enumerate_paths", "execute_plan", "estimate_cost",
     "AmplitudeEngine", "AmplitudeBatch", "FidelitySpec", "PathStats", "mixed_state_samples",
     "amplitude_record", "batch_records", "read_amplitudes", "write_amplitudes",
     "SliceShard", "current_shard", "reduce_partials", "shard_range",

@@ -25,7 +25,7 @@ def timed(fn):
 
 if which == "config4":
     lat = qf.Lattice.named("grid:7x7"); circ = qf.generate_rqc(lat, "1+40+1", 0)
-    plan = qf.load_plan("grid:7x7")
+    plan = qf.load_plan("grid:7x7:slice-first")
     eng = qf.AmplitudeEngine(circ, plan)
     rng = np.random.Generator(np.random.PCG64(0))
     out = format(int(rng.integers(0, 2 ** 49)), "049b")
@@ -36,7 +36,7 @@ if which == "config4":
     open_c = ()
 else:
     lat = qf.Lattice.named("bristlecone-70"); circ = qf.generate_rqc(lat, "1+32+1", 0)
-    plan = qf.load_plan("bristlecone-70")
+    plan = qf.load_plan("bristlecone-70:slice-first")
     eng = qf.AmplitudeEngine(circ, plan)
     c_sites = tuple(sorted(plan.batch_sites[:6]))
     rng = np.random.Generator(np.random.PCG64(0))

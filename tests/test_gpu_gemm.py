@@ -102,11 +102,10 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (9, 300, 5, 24), (4, 640, 32, 64), (3, 512, 24, 130)]
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 17, 18, 19, 20],
-                ids=["ws", "SS", "TS", "promoted-v2", "stream", "reg", "pair", "ws-ks2", "ws-ks4",
-                     "ws-shortk", "short-8warps", "short-16warps", "short-epilogue-warps",
-                     "long-tmem-master-ck4", "long-tmem-master-ck8", "long-ws-registers",
-                     "short-producer-warps", "long-producer-warps", "long-tma", "short-tma"])
+@pytest.fixture(params=[0, 10, 11, 12, 13, 20, 21, 26, 27],
+                ids=["auto", "short-8warps", "short-16warps", "short-epilogue-warps",
+                     "long-converter-fetch", "short-tma", "short-tma-ring4", "long-tma-ck16",
+                     "long-tma-ck32"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -117,19 +116,15 @@ def tc_variant(request):
 @pytest.mark.parametrize("shape", TC_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
 def test_tcgen05_3xtf32_c64(shape, ops, tc_variant):
-    """3xTF32 keeps ~fp32 accuracy: same 1e-5 bar as the FFMA kernel.  The
-    unpromoted v1 variants accumulate all of K in TMEM (error ~1.4e-8 K),
-    so they are only held to the bar for K <= 256."""
-    if tc_variant in (1, 2) and shape[3] > 256:
-        pytest.skip("v1 variants are exercised at short K only")
+    """3xTF32 keeps ~fp32 accuracy: same 1e-5 bar as the FFMA kernel."""
     err = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3)
     assert err < 1e-5, err
 
 
 @pytest.mark.parametrize("shape", SHORTK_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-@pytest.mark.parametrize("variant", [0, 10, 11, 12, 17, 20],
-                         ids=["auto", "8warps", "16warps", "epilogue-warps", "producer-warps", "tma"])
+@pytest.mark.parametrize("variant", [0, 10, 11, 12, 20],
+                         ids=["auto", "8warps", "16warps", "epilogue-warps", "tma"])
 def test_tcgen05_short_k_runs(shape, ops, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
@@ -141,8 +136,8 @@ def test_tcgen05_short_k_runs(shape, ops, variant):
 
 @pytest.mark.parametrize("a_labels", [["@b", "p", "s", "q", "t"], ["@b", "s", "q", "t", "p"]],
                          ids=["k-innermost", "row-innermost"])
-@pytest.mark.parametrize("variant", [10, 11, 12, 17],
-                         ids=["8warps", "16warps", "epilogue-warps", "producer-warps"])
+@pytest.mark.parametrize("variant", [10, 11, 12],
+                         ids=["8warps", "16warps", "epilogue-warps"])
 def test_gathered_short_k_many_tiles(a_labels, variant):
     """Gathered A through the short-K kernel with several M tiles per batch
     (row offsets prefetched a tile ahead, B reused across the run), for both
@@ -168,9 +163,8 @@ def test_gathered_short_k_many_tiles(a_labels, variant):
 
 
 @pytest.mark.parametrize("K", [1024, 4096, 32768])
-@pytest.mark.parametrize("variant", [0, 13, 14, 15, 18, 19],
-                         ids=["default", "tmem-master-ck4", "tmem-master-ck8", "ws-registers",
-                              "producer-warps", "tma"])
+@pytest.mark.parametrize("variant", [0, 13, 26, 27],
+                         ids=["default", "converter-fetch", "tma-ck16", "tma-ck32"])
 def test_tcgen05_promoted_accuracy_at_long_k(K, variant):
     """Promotion keeps the long-K error near the FFMA kernel's (config-4
     GEMMs have K = 2^15)."""

@@ -68,10 +68,13 @@ def test_grid_plans_match_reference_text(golden, key):
 
 
 def test_shipped_slice_plans_match_golden(golden):
-    assert qf.format_plan(qf.load_plan("grid:7x7")) == golden["plans"]["grid7x7_slice"]
-    assert qf.format_plan(qf.load_plan("bristlecone-70")) == golden["plans"]["b70_slice"]
+    assert qf.format_plan(qf.load_plan("grid:7x7:slice-first")) == golden["plans"]["grid7x7_slice"]
+    assert qf.format_plan(qf.load_plan("bristlecone-70:slice-first")) == golden["plans"]["b70_slice"]
     for kind in ("grid:7x7", "bristlecone-70"):
-        qf.builtin_plan(qf.Lattice.named(kind)).analyze(qf.Lattice.named(kind))
+        lat = qf.Lattice.named(kind)
+        qf.slice_first_plan(lat).analyze(lat)
+        assert qf.format_plan(qf.slice_first_plan(lat)) == \
+            qf.format_plan(qf.load_plan(kind + ":slice-first"))
 
 
 def test_estimate_cost_matches_reference(golden):
@@ -185,8 +188,9 @@ def test_lattice_shapes():
     lat = qf.Lattice.rectangle(3, 4)
     assert lat.edges()[:3] == ((0, 1), (0, 4), (1, 2))
     assert qf.edge_activations(lat, 8) == {e: 1 for e in lat.edges()}
+    assert qf.Lattice.named("bristlecone-24").n == 24
     with pytest.raises(ValueError):
-        qf.Lattice.named("bristlecone-24")
+        qf.Lattice.named("bristlecone-23")
 
 
 def test_circuit_format_errors():
@@ -305,7 +309,7 @@ def test_batch_order_is_plan_order_lexsort(name, n):
     import paper_1811_09599_b200 as qf
     lat = qf.Lattice.named(name)
     circ = qf.generate_rqc(lat, "1+8+1", 0)
-    eng = qf.AmplitudeEngine(circ, qf.builtin_plan(lat) if n == 70 else qf.grid_plan(lat, n_cuts=1))
+    eng = qf.AmplitudeEngine(circ, qf.slice_first_plan(lat) if n == 70 else qf.grid_plan(lat, n_cuts=1))
     bits = np.random.default_rng(1).integers(0, 2, size=(777, n)).astype(np.int32)
     bits[5] = bits[9]                       # a duplicate: stable order
     order = eng.batch_order(bits)
