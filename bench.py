@@ -252,12 +252,6 @@ def peaks() -> dict:
     else:
         d = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
              "source": "B200_PROFILING.md fallback"}
-    tf32 = os.path.join(ROOT, "profiles", "measured_tf32.json")
-    if os.path.exists(tf32):
-        with open(tf32) as fh:
-            d["tf32_tflops"] = json.load(fh)["tf32_tflops"]
-        return d
-    d.setdefault("tf32_tflops", d["bf16_tflops"] / 2)
     return d
 
 
@@ -393,7 +387,9 @@ def run_gpu(args):
                           "share": round(d["ms"] / total, 4),
                           "tflops": round(d["flops"] / d["ms"] / 1e9, 2) if d["ms"] else None,
                           "gbs": round(d["bytes"] / d["ms"] / 1e6, 1) if d["ms"] else None}
-        tensor_peak = pk["tf32_tflops"] / 3                # 3xTF32 complex ceiling
+        # 3xTF32 complex ceiling of the real-block kernel (TF32 = burst bf16 / 2:
+        # a config-2 step is milliseconds long); the ridge classifies launches
+        tensor_peak, _, peak_basis = tensor_peak_of(pk, sustained=False)
         ridge = tensor_peak * 1e12 / (pk["hbm_gbs"] * 1e9)
         # launches grouped by (CUDA kernel, the roofline that bounds the
         # launch's shape: tensor if its algorithmic flop/byte >= the ridge);
@@ -412,9 +408,9 @@ def run_gpu(args):
             name, bnd = key
             g = groups[key]
             if bnd == "tensor":
-                achieved, peak = g["flops"] / g["ms"] / 1e9, tensor_peak
-                r = {"bound": "tensor", "unit": "TFLOP/s", "kernel": name,
-                     "peak_basis": "cuBLAS TF32 measured (profiles/measured_tf32.json) / 3 (3xTF32)"}
+                peak, _, basis = tensor_peak_of(pk, sustained=False, kernel=name)
+                achieved = g["flops"] / g["ms"] / 1e9
+                r = {"bound": "tensor", "unit": "TFLOP/s", "kernel": name, "peak_basis": basis}
             else:
                 achieved, peak = g["bytes"] / g["ms"] / 1e6, pk["hbm_gbs"]
                 r = {"bound": "hbm", "unit": "GB/s", "kernel": name,
@@ -626,7 +622,7 @@ def path_units(wl: dict, circ, plan, count: int) -> list:
     return units, c_sites
 
 
-def tensor_peak(pk: dict, sustained: bool) -> tuple:
+def tensor_peak_of(pk: dict, sustained: bool, kernel: str = "cgemm_tc3k") -> tuple:
     """(3xTF32 complex ceiling in algorithmic TFLOP/s, TF32 peak, basis) from
     the driver-measured bf16 peak: TF32 dense runs at half the bf16 rate, and
     the kernel issues `mma_per_cmac` real TF32 MMAs of k-width 1 per complex
@@ -634,7 +630,7 @@ def tensor_peak(pk: dict, sustained: bool) -> tuple:
     from paper_1811_09599_b200 import tensor_core as tc
     bf16 = pk["bf16_tflops_sustained"] if sustained else pk["bf16_tflops"]
     tf32 = bf16 / 2
-    per = tc.tc3_real_macs_per_complex_mac()
+    per = tc.tc3_real_macs_per_complex_mac(kernel)
     return (tf32 * 8 / (2 * per), tf32,
             f"{'bf16_tflops_sustained' if sustained else 'bf16_tflops'} {bf16} ({pk['source']}) "
             f"/ 2 = TF32 {tf32:.1f}; x 8 / (2 x {per} real TF32 MACs per complex MAC)")
@@ -734,14 +730,15 @@ def run_paths(args):
     step_kernel_ms = sum(x["ms"] for x in kerns.values())
     exec_flops = sum(x["flops"] for x in kerns.values())
     pk = peaks()
-    ceil, tf32, basis = tensor_peak(pk, sustained=True)
+    ceil, tf32, basis = tensor_peak_of(pk, sustained=True, kernel=dom)
     achieved = d["flops"] / d["ms"] / 1e9
     roof = {"bound": "tensor", "unit": "TFLOP/s", "kernel": dom,
             "achieved": round(achieved, 2), "peak": round(ceil, 1),
             "frac": round(achieved / ceil, 4), "peak_basis": basis,
             "launches": d["launches"], "ms_per_step": round(d["ms"] / args.steps, 2),
             "share_of_step": round(d["ms"] / args.steps / ms, 4),
-            "tensor_pipe_util": round(achieved * 2 * tc.tc3_real_macs_per_complex_mac() / 8 / tf32, 4),
+            "tensor_pipe_util": round(achieved * 2 * tc.tc3_real_macs_per_complex_mac(dom) / 8 / tf32, 4),
+            "frac_of_real_block_3xtf32_ceiling": round(achieved / (tf32 / 3), 4),
             "algorithmic": f"8*m*k*n flops per {dom} launch summed over the {d['launches']} launches "
                            f"of the {args.steps} timed steps / their CUDA-event time (eager launches, "
                            f"events on the launching stream)",
@@ -995,6 +992,8 @@ def main(argv=None):
                     help="config1/config2 only: bit-strings per rank (no collective) or the "
                          "slices of one batch split over the ranks (one all-reduce)")
     ap.add_argument("--gemm", choices=["auto", "ffma", "tc3"], default=None)
+    ap.add_argument("--tc3-variant", type=int, default=0,
+                    help="pin a tensor-core kernel flavour (qf_tc3_set_variant) for A/B runs")
     ap.add_argument("--cpu-sample", type=int, default=1024,
                     help="config1/2: bit-strings timed on the host cores")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -1028,6 +1027,9 @@ def main(argv=None):
         rank, world, local = dist_env()
         torch.cuda.set_device(local)
         init_dist(world, "nccl")
+        if args.tc3_variant:
+            from paper_1811_09599_b200 import _lib
+            _lib.load().qf_tc3_set_variant(args.tc3_variant)
         try:
             if args.workload == "permute":
                 out = run_permute(args)

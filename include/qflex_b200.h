@@ -266,13 +266,31 @@ int qf_zgemm_c128(int64_t batch, int64_t M, int64_t N, int64_t K,
  */
 int qf_accumulate(const void *x, void *y, int64_t n, int elem_bytes, void *stream);
 
+/* Index tables of the batched walks (entry bases of per-entry operand
+ * fetches), computed on the device:
+ *   out[e] = (base ? base[e / rep] : (e / rep) * entry) + (e % rep) * stride,
+ * e in [0, n).  base (DEVICE int64[n / rep]) may be NULL.  Serves the
+ * broadcast of a path-free operand over a path-batched one and the
+ * (bit-string, cut value) slices of a path-batched walk -- the reference
+ * walks those paths one by one (rq/amplitude_engine.py:123). */
+int qf_affine_offsets(int64_t *out, int64_t n, int64_t rep, int64_t entry, const int64_t *base,
+                      int64_t stride, void *stream);
+
+/* y[i] = re + i*im for i in [0, n) (complex64: elem_bytes 8, complex128: 16);
+ * e.g. the ones row that sums a path axis. */
+int qf_fill_value(void *y, int64_t n, double re, double im, int elem_bytes, void *stream);
+
 /* y[0:bytes) = 0, stream-ordered (accumulator reset before a path sum). */
 int qf_fill_zero(void *y, int64_t bytes, void *stream);
 
 /*
- * Stream-ordered workspace the GEMM split-K path uses (the only memory
- * the library owns).  Reserve up front to keep allocation out of timed
- * regions; released by qf_workspace_release.
+ * Workspace the GEMM split-K path uses (the only memory the library owns),
+ * grow-only per device: growing keeps the previous buffer alive (a CUDA graph
+ * that captured a GEMM holds its pointer) and is refused while the stream is
+ * capturing -- reserve before capturing to keep allocation out of timed
+ * regions and graphs.  qf_workspace_release frees every buffer of the
+ * current device (synchronizing it); call it only when no captured graph
+ * that used the library is replayed afterwards.
  */
 int qf_workspace_reserve(int64_t bytes, void *stream);
 int qf_workspace_release(void);

@@ -42,7 +42,7 @@ EXPORTS = (
     "qf_small_engine", "qf_rowmma", "qf_cgemm_c64_rowblocks",
     "qf_workspace_reserve", "qf_workspace_release", "qf_launch_count",
     "qf_nccl_available", "qf_nccl_unique_id", "qf_nccl_init", "qf_nccl_destroy",
-    "qf_allreduce_c64", "qf_axpy_c64", "qf_dot_c64",
+    "qf_allreduce_c64", "qf_axpy_c64", "qf_dot_c64", "qf_affine_offsets", "qf_fill_value",
 )
 
 
@@ -162,6 +162,9 @@ def _declare(lib):
     lib.qf_axpy_c64.argtypes = [_i64, ctypes.c_float, ctypes.c_float, _c_void_p, _c_void_p,
                                 _c_void_p]
     lib.qf_dot_c64.argtypes = [_i64, _i64, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]
+    lib.qf_affine_offsets.argtypes = [_c_void_p, _i64, _i64, _i64, _c_void_p, _i64, _c_void_p]
+    lib.qf_fill_value.argtypes = [_c_void_p, _i64, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                  _c_void_p]
     lib.qf_launch_count.argtypes = [ctypes.c_int]
     lib.qf_launch_count.restype = _i64
     for name in EXPORTS:

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "qf_common.cuh"
 
@@ -35,9 +36,16 @@ int check_launch(const char *what) {
   return QF_OK;
 }
 
+// Grow-only workspace per device.  A CUDA graph that captured a GEMM keeps
+// the workspace pointer it saw, so a buffer is never freed while the library
+// may still hand it out: growing retires the old buffer (kept until
+// qf_workspace_release, which the caller may only invoke once no captured
+// graph uses library workspaces), and growing during stream capture is
+// refused (reserve before capturing; the engine's graph runner warms up).
 struct Workspace {
   void *ptr = nullptr;
   int64_t bytes = 0;
+  std::vector<void *> retired;
 };
 static std::mutex g_ws_mu;
 static std::unordered_map<int, Workspace> g_ws;
@@ -49,9 +57,18 @@ void *workspace(int64_t bytes, cudaStream_t stream, int *status) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   Workspace &w = g_ws[dev];
   if (w.bytes >= bytes) return w.ptr;
-  if (w.ptr) cudaFreeAsync(w.ptr, stream);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  if (cap != cudaStreamCaptureStatusNone) {
+    set_error("workspace: %lld bytes needed during stream capture (have %lld); reserve first "
+              "(qf_workspace_reserve) or run the call once before capturing",
+              (long long)bytes, (long long)w.bytes);
+    *status = QF_ERR_INVALID;
+    return nullptr;
+  }
+  if (w.ptr) w.retired.push_back(w.ptr);
   int64_t want = bytes < (1 << 20) ? (1 << 20) : bytes;
-  cudaError_t e = cudaMallocAsync(&w.ptr, (size_t)want, stream);
+  cudaError_t e = cudaMalloc(&w.ptr, (size_t)want);
   if (e != cudaSuccess) {
     w.ptr = nullptr;
     w.bytes = 0;
@@ -141,6 +158,24 @@ __global__ void accumulate_kernel(const E *__restrict__ x, E *__restrict__ y, in
     b.y += a.y;
     y[t] = b;
   }
+}
+
+// out[e] = (base ? base[e / rep] : (e / rep) * entry) + (e % rep) * stride
+__global__ void affine_offsets_kernel(int64_t *__restrict__ out, int64_t n, int64_t rep,
+                                      int64_t entry, const int64_t *__restrict__ base,
+                                      int64_t stride) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / rep, r = e - q * rep;
+    out[e] = (base ? __ldg(base + q) : q * entry) + r * stride;
+  }
+}
+
+template <typename E>
+__global__ void fill_value_kernel(E *__restrict__ y, int64_t n, E v) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = v;
 }
 
 static int grid_for(int64_t n, int threads) {
@@ -274,6 +309,32 @@ int qf_fill_zero(void *y, int64_t bytes, void *stream) {
   return QF_OK;
 }
 
+int qf_affine_offsets(int64_t *out, int64_t n, int64_t rep, int64_t entry, const int64_t *base,
+                      int64_t stride, void *stream) {
+  QF_REQUIRE(n >= 0 && rep >= 1, "affine_offsets: bad extents n=%lld rep=%lld", (long long)n,
+             (long long)rep);
+  if (n == 0) return QF_OK;
+  QF_REQUIRE(out != nullptr, "affine_offsets: out is NULL");
+  qf::affine_offsets_kernel<<<qf::grid_for(n, 256), 256, 0, qf::as_stream(stream)>>>(
+      out, n, rep, entry, base, stride);
+  return qf::check_launch("affine_offsets");
+}
+
+int qf_fill_value(void *y, int64_t n, double re, double im, int elem_bytes, void *stream) {
+  QF_REQUIRE(n >= 0, "fill_value: negative length");
+  QF_REQUIRE(elem_bytes == 8 || elem_bytes == 16, "fill_value: elem_bytes must be 8 or 16");
+  if (n == 0) return QF_OK;
+  QF_REQUIRE(y != nullptr, "fill_value: y is NULL");
+  cudaStream_t s = qf::as_stream(stream);
+  if (elem_bytes == 8)
+    qf::fill_value_kernel<float2><<<qf::grid_for(n, 256), 256, 0, s>>>(
+        (float2 *)y, n, make_float2((float)re, (float)im));
+  else
+    qf::fill_value_kernel<double2><<<qf::grid_for(n, 256), 256, 0, s>>>(
+        (double2 *)y, n, make_double2(re, im));
+  return qf::check_launch("fill_value");
+}
+
 int qf_workspace_reserve(int64_t bytes, void *stream) {
   int st = QF_OK;
   qf::workspace(bytes, qf::as_stream(stream), &st);
@@ -285,8 +346,10 @@ int qf_workspace_release(void) {
   int dev = 0;
   cudaGetDevice(&dev);
   auto it = qf::g_ws.find(dev);
-  if (it != qf::g_ws.end() && it->second.ptr) {
-    cudaFree(it->second.ptr);
+  if (it != qf::g_ws.end()) {
+    cudaDeviceSynchronize();
+    for (void *p : it->second.retired) cudaFree(p);
+    if (it->second.ptr) cudaFree(it->second.ptr);
     it->second = qf::Workspace();
   }
   return QF_OK;

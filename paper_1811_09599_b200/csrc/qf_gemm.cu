@@ -1498,7 +1498,22 @@ int gemm_simt(const GemmArgs &g, cudaStream_t s) {
     const bool rows = sizeof(R) == 4 && g.opA == QF_OP_N && !g.a_roff && P >= 8 && g.N <= 4;
     if (rows) kchunk = (kchunk + 63) / 64 * 64;   // 16-byte aligned chunks
     nsplit = (g.K + kchunk - 1) / kchunk;
-    QF_REQUIRE(g.batch <= 65535, "gemm: skinny batch %lld exceeds 65535", (long long)g.batch);
+    if (g.batch > 65535) {
+      // gridDim.y carries the batch: split into launches of <= 65535 entries
+      // (entry bases advance by the strides or through the offset tables)
+      for (int64_t lo = 0; lo < g.batch; lo += 65535) {
+        GemmArgs h = g;
+        h.batch = std::min<int64_t>(65535, g.batch - lo);
+        if (g.a_boff) h.a_boff = g.a_boff + lo;
+        else h.A = static_cast<const typename C2<R>::T *>(g.A) + lo * g.sA;
+        if (g.b_boff) h.b_boff = g.b_boff + lo;
+        else h.B = static_cast<const typename C2<R>::T *>(g.B) + lo * g.sB;
+        h.C = static_cast<typename C2<R>::T *>(g.C) + lo * g.sC;
+        const int rc = gemm_simt<R>(h, s);
+        if (rc != QF_OK) return rc;
+      }
+      return QF_OK;
+    }
     int st = QF_OK;
     void *ws = workspace(g.batch * nsplit * P * (int64_t)sizeof(typename C2<R>::T), s, &st);
     if (st != QF_OK) return st;

@@ -1300,17 +1300,18 @@ int launch_short(const GemmArgs &g, cudaStream_t s) {
   const int64_t grid = CK > 0 ? grid0 : (total + chunk - 1) / chunk;  // long K: strided tiles
   kern<<<(unsigned)grid, (NW + NE + NPW) * 32 + 32, L::SMEM, s>>>(
       g, (uint32_t)tiles_m, (uint32_t)tiles_n, (uint32_t)total, (uint32_t)chunk, tmA, tmB);
-  return check_launch("cgemm_tc3k");
+  // the Gauss flavour is reported under its own name (9 real TF32 MACs per
+  // complex MAC instead of 12: its tensor roofline differs)
+  return check_launch(G3 ? "cgemm_tc3g" : "cgemm_tc3k");
 }
 
 }  // namespace tc
 
 // Tuning knob (qf_tc3_set_variant): 0 = auto.  Pins for A/B measurements of
 // the kernel flavours auto chooses between: 10/11/12/20 = short-K flavours
-// (launch_short_auto), 13 = long-K converter-fetch (no TMA), 21 = TMA
-// short-K with a 4-deep A ring,
-// 23 = 64-column tiles for narrow TMA views, 26/27 = long-K TMA-fed with the
-// TMEM partial promoted every 16/32 k-blocks instead of 4.
+// (launch_short_auto), 21 = TMA short-K with a 4-deep A ring, 23 = 64-column
+// tiles for narrow TMA views, 13/19/26/27/30/31 = long-K flavours
+// (launch_long).
 static int g_tc3_variant = 0;
 
 bool tc3_gather_ok(const GemmArgs &g) { return g.K <= 4096; }
@@ -1328,16 +1329,24 @@ static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
 }
 
 // long K: a TMA producer warp, 8 converter warps, 4 promotion warps with a
-// TMEM master accumulator (cp.async fetch by the converters when TMA
-// cannot describe the operands)
+// TMEM master accumulator.  Default: the Gauss form (9 instead of 12 TF32
+// MMAs per complex MAC) with the partial promoted every 64 k-blocks (512 k:
+// truncation error of the tensor pipe's fp32 accumulation ~3.7e-6 per chunk,
+// rounded sums across chunks).  Under the 1 kW cap the big GEMMs are power
+// bound, and 3/4 of the tensor work runs them ~17% faster at higher clocks
+// (32768^3: 158.6 -> 185.5 TFLOP/s sustained; 4096 x 65536 x 4096: 171.5
+// -> 198.3; profiles/r2_gemm_g3.jsonl).  Pins: 19 = the real-block form
+// (CK 4), 26/27 = real-block CK 16/32, 30/31 = Gauss CK 16/32, 13 =
+// converter fetch (no TMA; also the fallback when TMA cannot describe the
+// operands).
 static int launch_long(const GemmArgs &g, cudaStream_t s) {
   if (g_tc3_variant != 13 && tc::tma_ok(g)) {
+    if (g_tc3_variant == 19) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
     if (g_tc3_variant == 26) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true>(g, s);
     if (g_tc3_variant == 27) return tc::launch_short<4, 8, 8, 4, 64, 32, 1, true>(g, s);
     if (g_tc3_variant == 30) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true, true>(g, s);
     if (g_tc3_variant == 31) return tc::launch_short<4, 8, 8, 4, 64, 32, 1, true, true>(g, s);
-    if (g_tc3_variant == 32) return tc::launch_short<4, 8, 8, 4, 64, 64, 1, true, true>(g, s);
-    return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
+    return tc::launch_short<4, 8, 8, 4, 64, 64, 1, true, true>(g, s);
   }
   return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
 }

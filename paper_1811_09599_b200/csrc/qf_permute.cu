@@ -313,6 +313,16 @@ struct PermPlan {
   // device copies (per plan per device)
   int64_t *d64 = nullptr;
   int32_t *d32 = nullptr;
+  // set when the plan was requested while a stream was capturing: a CUDA
+  // graph holds its table pointers, so the cache never evicts it
+  bool pinned = false;
+  PermPlan() = default;
+  PermPlan(const PermPlan &) = delete;
+  PermPlan &operator=(const PermPlan &) = delete;
+  ~PermPlan() {  // cudaFree waits for work still using the tables
+    if (d64) cudaFree(d64);
+    if (d32) cudaFree(d32);
+  }
 };
 
 static int ilog2_exact(int64_t v) {
@@ -445,16 +455,19 @@ static int build_plan(int rank, const int64_t *dims_in, const int32_t *perm_in, 
 
   // run lengths and tile size in bytes; QF_PERM_TA / QF_PERM_TB / QF_PERM_TILE
   // override them (tuning experiments only)
+  // (read once per process: cached plans stay consistent with them)
   auto knob = [](const char *name, int64_t dflt) {  // clamped to sane byte counts
     const char *v = getenv(name);
     const int64_t x = v ? (int64_t)atoll(v) : dflt;
     return std::min<int64_t>(std::max<int64_t>(x, 64), 65536);
   };
+  static const int64_t kTA = knob("QF_PERM_TA", 256), kTB = knob("QF_PERM_TB", 256),
+                       kTile = knob("QF_PERM_TILE", 32768);
   // 256-byte runs: a 64 x 64 element tile with disjoint A/B (512-byte runs)
   // ran at 4.85 TB/s; 32-element runs let A grow to 128 inputs while B keeps
   // whole 256-byte output sectors (6.1-6.2 TB/s, profiles/r1n_permute_knobs.txt)
-  const int64_t TA = knob("QF_PERM_TA", 256) / elem_bytes, TB = knob("QF_PERM_TB", 256) / elem_bytes;
-  const int64_t Tmin = knob("QF_PERM_TILE", 32768) / elem_bytes,
+  const int64_t TA = kTA / elem_bytes, TB = kTB / elem_bytes;
+  const int64_t Tmin = kTile / elem_bytes,
                 Tmax = Tmin;  // 32 KB tiles (measured: 16 KB tiles ran ~20% slower)
 
   // 3. A = innermost input axes [a_start, r)
@@ -754,9 +767,12 @@ static std::mutex g_plan_mu;
 static std::map<std::string, std::shared_ptr<PermPlan>> g_plans;
 
 static int get_plan(int rank, const int64_t *dims, const int32_t *perm, int elem_bytes,
-                    std::shared_ptr<PermPlan> &out) {
+                    std::shared_ptr<PermPlan> &out, cudaStream_t stream) {
   int dev = 0;
   cudaGetDevice(&dev);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(stream, &cap);
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
   std::string key;
   key.reserve(16 + rank * 12);
   key.append((const char *)&dev, sizeof(dev));
@@ -768,9 +784,16 @@ static int get_plan(int rank, const int64_t *dims, const int32_t *perm, int elem
     std::lock_guard<std::mutex> lk(g_plan_mu);
     auto it = g_plans.find(key);
     if (it != g_plans.end()) {
+      if (capturing) it->second->pinned = true;
       out = it->second;
       return QF_OK;
     }
+  }
+  if (capturing) {
+    // building a plan allocates and uploads its tables: not capturable
+    qf::set_error("permute: plan for this (dims, perm) first requested during stream capture; "
+                  "run the call once before capturing");
+    return QF_ERR_INVALID;
   }
   auto plan = std::make_shared<PermPlan>();
   int st = build_plan(rank, dims, perm, elem_bytes, *plan);
@@ -784,7 +807,10 @@ static int get_plan(int rank, const int64_t *dims, const int32_t *perm, int elem
                        cudaMemcpyHostToDevice));
   }
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  if (g_plans.size() > 8192) g_plans.clear();  // plans are cheap to rebuild
+  if (g_plans.size() > 8192) {  // plans are cheap to rebuild; graph-held ones stay
+    for (auto it = g_plans.begin(); it != g_plans.end();)
+      it = it->second->pinned ? std::next(it) : g_plans.erase(it);
+  }
   g_plans[key] = plan;
   out = plan;
   return QF_OK;
@@ -830,7 +856,7 @@ extern "C" {
 int qf_permute(const void *src, void *dst, int rank, const int64_t *dims, const int32_t *perm,
                int elem_bytes, void *stream) {
   std::shared_ptr<qf::PermPlan> plan;
-  int st = qf::get_plan(rank, dims, perm, elem_bytes, plan);
+  int st = qf::get_plan(rank, dims, perm, elem_bytes, plan, qf::as_stream(stream));
   if (st != QF_OK) return st;
   if (plan->n == 0) return QF_OK;
   QF_REQUIRE(src != dst, "permute: src and dst must not alias");

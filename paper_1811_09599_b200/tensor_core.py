@@ -74,12 +74,13 @@ def set_gemm_mode(mode: str) -> str:
     return prev
 
 
-def tc3_real_macs_per_complex_mac() -> int:
-    """Real TF32 MMA multiply-adds the tensor-core engine issues per complex
-    multiply-add: 4 real products x 3 (hi*hi + hi*lo + lo*hi) = 12 in the
-    real-block form (the 3xTF32 ceiling is then TF32_peak / 3 in algorithmic
-    8-flop complex MACs)."""
-    return 12
+def tc3_real_macs_per_complex_mac(kernel: str = "cgemm_tc3k") -> int:
+    """Real TF32 MMA multiply-adds a tensor-core kernel issues per complex
+    multiply-add: the real-block form (`cgemm_tc3k`) 4 real products x 3
+    (hi*hi + hi*lo + lo*hi) = 12, the Gauss form (`cgemm_tc3g`) 3 x 3 = 9.
+    The 3xTF32 ceiling in algorithmic 8-flop complex MACs is then
+    TF32_peak * 8 / (2 * that)."""
+    return 9 if kernel == "cgemm_tc3g" else 12
 
 
 def get_gemm_mode() -> str:
@@ -208,6 +209,16 @@ def gather_buffer(src, dims: Sequence[int], axis: int, idx):
                                     stream_handle())
     _lib.check(st, "gather")
     return out
+
+
+def affine_offsets(out, n: int, rep: int, entry: int, base=None, stride: int = 0):
+    """out[e] = (base[e // rep] if base is given else (e // rep) * entry)
+    + (e % rep) * stride on the device (int64 entry-base tables)."""
+    st = _lib.load().qf_affine_offsets(ctypes.c_void_p(out.data_ptr()), int(n), int(rep),
+                                       int(entry),
+                                       ctypes.c_void_p(base.data_ptr()) if base is not None else None,
+                                       int(stride), stream_handle())
+    _lib.check(st, "affine_offsets")
 
 
 def zero_buffer(y):
@@ -884,7 +895,8 @@ def _zero_offsets(n: int, device):
     key = (n, str(device))
     z = _ZEROS.get(key)
     if z is None:
-        z = _ZEROS[key] = torch.zeros(n, dtype=torch.int64, device=device)
+        z = _ZEROS[key] = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+        affine_offsets(z, n, 1, 0)
     return z
 
 
@@ -1012,16 +1024,14 @@ def _contract_open(a: Tensor, b: Tensor, late: LateBits, tail=()) -> Optional[Te
 
 
 PATH_LABEL = "@p"
-_ARANGE: dict = {}
 
 
 def _path_offsets(off, rep: int, stride: int):
     """Per-(bit-string, path value) entry bases: off[b] + j*stride, j fastest."""
-    key = (rep, str(off.device))
-    ar = _ARANGE.get(key)
-    if ar is None:
-        ar = _ARANGE[key] = torch.arange(rep, dtype=torch.int64, device=off.device)
-    return (off[:, None] + ar[None, :] * stride).reshape(-1)
+    n = int(off.numel()) * rep
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=off.device)
+    affine_offsets(out, n, rep, 0, base=off, stride=stride)
+    return out[:n]
 
 
 class ShapeOnly:
@@ -1478,8 +1488,9 @@ def _bcast_offsets(n: int, rep: int, entry: int, device):
     key = (n, rep, entry, str(device))
     hit = _BCAST.get(key)
     if hit is None:
-        hit = torch.div(torch.arange(n, dtype=torch.int64, device=device), rep,
-                        rounding_mode="floor") * entry
+        hit = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+        affine_offsets(hit, n, rep, entry)
+        hit = hit[:n]
         if len(_BCAST) > 64:
             _BCAST.clear()
         _BCAST[key] = hit
@@ -1576,7 +1587,10 @@ def sum_path_axis(t: Tensor, rep: int, keep_batch: bool, label: str = "@b") -> T
     key = (rep, str(t.buf.dtype), str(t.buf.device))
     ones = _ONES.get(key)
     if ones is None:
-        ones = _ONES[key] = torch.ones(rep, dtype=t.buf.dtype, device=t.buf.device)
+        ones = _ONES[key] = torch.empty(rep, dtype=t.buf.dtype, device=t.buf.device)
+        st = _lib.load().qf_fill_value(ctypes.c_void_p(ones.data_ptr()), rep, 1.0, 0.0,
+                                       _elem_bytes(ones), stream_handle())
+        _lib.check(st, "fill_value")
     out = device_buffer(nb * R, t.buf.dtype, t.buf.device)
     lib = _lib.load()
     with _timed("gemm", 8 * nb * R * rep, _elem_bytes(out) * (NB * R + nb * R),

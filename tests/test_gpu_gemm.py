@@ -740,3 +740,66 @@ def test_reassociated_expansion_keeps_outputs_open(nb):
     want = tc.contract_late(u2, tw2, late)
     w = want.transpose_to(got.labels).array
     assert np.linalg.norm(got.array - w) / np.linalg.norm(w) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# library-owned state vs CUDA graphs
+
+
+def test_skinny_batch_beyond_grid_limit_c128():
+    """The split-K skinny path (M*N <= 256, K >= 256) carries the batch in
+    gridDim.y; more than 65535 entries are split into several launches."""
+    assert _gemm(70000, 1, 1, 256, 0, 1, np.complex128) < 1e-12
+
+
+def test_graph_replay_survives_workspace_growth():
+    """A captured split-K GEMM keeps the workspace pointer it saw: a later,
+    larger eager GEMM must not free it under the graph."""
+    rng = np.random.default_rng(11)
+    b, K = 64, 4096
+    A = torch.from_numpy(_rand(rng, (b, 1, K), np.complex64).reshape(-1)).cuda()
+    B = torch.from_numpy(_rand(rng, (b, K, 1), np.complex64).reshape(-1)).cuda()
+    C = torch.zeros(b, dtype=torch.complex64, device="cuda")
+    run = lambda: tc.gemm_buffer(b, 1, 1, K, A, 0, B, 0, C, mode=_lib.GEMM_FFMA)  # noqa: E731
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        run()                                  # warm-up reserves the workspace
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run()
+    want = C.clone()
+    # a larger split-K call (16 x 16 outputs per entry: > 1 MiB of partials)
+    # grows the workspace eagerly
+    b2, M2, K2 = 500, 16, 8192
+    A2 = torch.randn(b2 * M2 * K2, dtype=torch.complex64, device="cuda")
+    B2 = torch.randn(b2 * K2 * M2, dtype=torch.complex64, device="cuda")
+    C2 = torch.empty(b2 * M2 * M2, dtype=torch.complex64, device="cuda")
+    tc.gemm_buffer(b2, M2, M2, K2, A2, 0, B2, 0, C2, mode=_lib.GEMM_FFMA)
+    del A2, B2
+    C.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C, want)
+
+
+def test_permute_plan_first_built_in_capture_is_refused():
+    x = torch.randn(2 ** 12, dtype=torch.complex64, device="cuda")
+    y = torch.empty_like(x)
+    dims, perm = [2] * 12, [11, 3, 7, 0, 10, 1, 9, 2, 8, 4, 6, 5]
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(Exception):
+        with torch.cuda.graph(g):
+            tc.permute_buffer(x, dims, perm, out=y)
+    torch.cuda.synchronize()
+    tc.permute_buffer(x, dims, perm, out=y)          # eager: plan built
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):                        # now capturable (and pinned)
+        tc.permute_buffer(x, dims, perm, out=y)
+    y.zero_()
+    g2.replay()
+    torch.cuda.synchronize()
+    want = x.cpu().numpy().reshape(dims).transpose(perm).reshape(-1)
+    assert np.array_equal(y.cpu().numpy(), want)
