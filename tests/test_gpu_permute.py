@@ -4,6 +4,7 @@ transpose, itself pinned to the reference's permute_fast bytes)."""
 from __future__ import annotations
 
 import hashlib
+import os
 import math
 
 import numpy as np
@@ -126,3 +127,69 @@ def test_benchmark_permute_schema_and_perms():
     csv = tc.benchmark_csv(rows)
     assert csv.splitlines()[0] == "op,rank,gamma,threads,median_ns,p10_ns,p90_ns"
     assert len(csv.splitlines()) == 7
+
+
+# ---------------------------------------------------------------------------
+# config 3 exactly as benchmarked: bench.config3_cases (64 seeded perms per
+# size), every permutation byte-compared against the C oracle
+# (oracle/permute_ref.c, the reference's permute_naive restated), with the
+# bench's input values
+
+
+def _host_ram_bytes() -> int:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):  # pragma: no cover
+        return 0
+
+
+def _byte_compare_config3(log2n: int, count: int, which=None):
+    from bench import config3_cases
+    from oracle import permute_oracle as P
+    n = 1 << log2n
+    g = torch.Generator(device="cuda").manual_seed(log2n)
+    src = torch.randn(n, dtype=torch.complex64, device="cuda", generator=g)
+    dst = torch.empty_like(src)
+    src_h = src.cpu().numpy()
+    got_h = torch.empty(n, dtype=torch.complex64).pin_memory()
+    want = np.empty(n, dtype=np.complex64)
+    cases = config3_cases(log2n, 64, seed=log2n)
+    picks = range(len(cases)) if which is None else which
+    done = 0
+    for i in list(picks)[:count]:
+        dims, perm = cases[i]
+        tc.permute_buffer(src, dims, perm, out=dst)
+        got_h.copy_(dst)
+        P.permute(src_h, dims, perm, out=want)
+        assert got_h.numpy().tobytes() == want.tobytes(), (log2n, i, dims, perm)
+        done += 1
+    return done
+
+
+def test_c_oracle_matches_numpy_oracle():
+    from oracle import permute_oracle as P
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        rank = int(rng.integers(1, 10))
+        dims = [int(rng.integers(1, 5)) for _ in range(rank)]
+        perm = [int(p) for p in rng.permutation(rank)]
+        x = (rng.standard_normal(dims) + 1j * rng.standard_normal(dims)).astype(np.complex64)
+        assert P.permute(x, dims, perm).tobytes() == O.permute_naive(x, perm).tobytes()
+
+
+def test_config3_2pow24_all_64_byte_exact():
+    assert _byte_compare_config3(24, 64) == 64
+
+
+def test_config3_2pow28_all_64_byte_exact():
+    if _host_ram_bytes() < 16 * 2 ** 30:
+        pytest.skip("needs ~8 GiB of host RAM for the oracle buffers")
+    assert _byte_compare_config3(28, 64) == 64
+
+
+def test_config3_2pow30_byte_exact_sample():
+    """8 of the 64 benchmarked 2^30 permutations (4 binary, 4 mixed), whole
+    16 GiB tensors (8 GiB in + 8 GiB out) byte-compared."""
+    if _host_ram_bytes() < 48 * 2 ** 30:
+        pytest.skip("needs ~24 GiB of host RAM for the oracle buffers")
+    assert _byte_compare_config3(30, 8, which=[0, 11, 22, 31, 32, 43, 54, 63]) == 8

@@ -74,3 +74,15 @@ def test_statevector_oracle_agrees_with_golden(golden):
     psi = O.statevector(golden["circuits"][case["circuit"]], 0)
     got = [psi[int(b, 2)] for b in case["out_bits"]]
     assert rel_l2(got, golden_amps(case)) < 1e-10
+
+
+def test_c_permutation_oracle_matches_reference_bytes(golden_perm):
+    """oracle/permute_ref.c reproduces the reference's permute_fast bytes."""
+    import hashlib
+    from oracle import permute_oracle as P
+    for case in golden_perm["cases"]:
+        g = np.random.default_rng(case["input_seed"])
+        dims = case["dims"]
+        x = (g.standard_normal(dims) + 1j * g.standard_normal(dims)).astype(np.complex64)
+        out = P.permute(x, dims, case["perm"])
+        assert hashlib.sha256(out.tobytes()).hexdigest() == case["sha256"], case

@@ -106,3 +106,84 @@ def test_slice_for_budget_impossible_raises():
     lat = qf.Lattice.named("grid:3x3")
     with pytest.raises(qf.PlanError):
         pt.slice_for_budget(lat, "1+8+1", {0, 1, 3, 4}, {2, 5}, {6, 7, 8}, 1, max_cuts=1)
+
+
+# ---------------------------------------------------------------------------
+# exact subset-DP trees (plan_tools.tree_order / tree_plan)
+
+_D_REGION = [24, 25, 26, 27, 31, 32, 33, 34, 38, 39, 40, 41, 45, 46, 47, 48]
+
+
+def _max_lg_of_chain(lat, order, bonds, sliced):
+    acc, worst, flops = None, 0, 0
+    for s in order:
+        op = pt._site_shape(lat, s, bonds, sliced, set())
+        if acc is None:
+            acc = op
+            continue
+        f, acc = pt._fold_cost(acc, op)
+        flops += f
+        worst = max(worst, sum(pt._lg(d) for d in acc.values()))
+    return flops, worst
+
+
+def test_tree_order_rediscovers_7x7_region_d_tree():
+    """Region D of the 7x7 (1+40+1) plan: the exact DP finds a tree with every
+    intermediate <= 2^30 at 4.48e13 flops, where the
+    reference's greedy region order (rq/contraction_plan.py:651-673) peaks
+    above 2^30 and costs more."""
+    from paper_1811_09599_b200.contraction_plan import _region_order
+    from paper_1811_09599_b200.network_builder import edge_label
+    lat = qf.Lattice.named("grid:7x7")
+    bonds = pt.bond_dims(lat, "1+40+1")
+    sliced = {edge_label(19, 26), edge_label(37, 38)}
+    flops, tree = pt.tree_order(lat, _D_REGION, bonds, sliced=sliced, cap_log2=30)
+    assert sorted(pt._tree_sites(tree)) == _D_REGION
+    assert flops <= 4.49e13
+    g_flops, g_worst = _max_lg_of_chain(lat, _region_order(lat, _D_REGION), bonds, sliced)
+    assert g_worst > 30 and g_flops > flops
+
+
+def test_tree_plan_7x7_matches_or_beats_the_hand_slice_first_plan():
+    lat = qf.Lattice.named("grid:7x7")
+    plan = pt.tree_plan(qf.load_plan("grid:7x7"), lat, "1+40+1")
+    plan.analyze(lat)
+    est = qf.estimate_cost(plan, lat, "1+40+1")
+    hand = qf.estimate_cost(qf.slice_first_plan(lat), lat, "1+40+1")
+    shipped = qf.estimate_cost(qf.load_plan("grid:7x7"), lat, "1+40+1")
+    assert est.total_flops <= hand.total_flops
+    assert est.peak_bytes < 80 * 2 ** 30 < shipped.peak_bytes
+    assert [c.name for c in plan.cuts] == ["right", "bottom"]
+    assert plan.batch_sites == qf.load_plan("grid:7x7").batch_sites
+
+
+@pytest.mark.parametrize("name,cap,peak_gib", [("bristlecone-48", 30, 32), ("bristlecone-60", 32, 80),
+                                               ("bristlecone-64", 32, 64), ("bristlecone-70", 30, 32)])
+def test_tree_plans_for_bristlecone_are_feasible_at_full_depth(name, cap, peak_gib):
+    """Bris-48/60/64/70 at 1+32+1 with their shipped cuts: the shipped plans
+    need 10^4..10^11 GiB; the tree plans fit a B200."""
+    lat = qf.Lattice.named(name)
+    ship = qf.load_plan(name)
+    c_sites = tuple(sorted(ship.batch_sites[:6]))
+    plan = pt.tree_plan(ship, lat, "1+32+1", open_sites=c_sites, cap_log2=cap)
+    est = qf.estimate_cost(plan, lat, "1+32+1", open_sites=c_sites)
+    est0 = qf.estimate_cost(ship, lat, "1+32+1", open_sites=c_sites)
+    assert est.peak_bytes < peak_gib * 2 ** 30 < est0.peak_bytes
+    assert est.total_flops < est0.total_flops
+
+
+@pytest.mark.parametrize("name,depth", [("grid:7x7", "1+16+1"), ("bristlecone-48", "1+8+1"),
+                                        ("bristlecone-24", "1+8+1")])
+def test_tree_plan_amplitudes_equal_shipped_plan(name, depth):
+    """Same amplitudes as the shipped plan (numpy oracle, test infrastructure)."""
+    lat = qf.Lattice.named(name)
+    circ = qf.generate_rqc(lat, depth, 3)
+    ship = qf.load_plan(name)
+    tree = pt.tree_plan(ship, lat, depth)
+    text = qf.write_circuit(circ)
+    a = O.OracleEngine(text, qf.format_plan(ship), np.complex128)
+    b = O.OracleEngine(text, qf.format_plan(tree), np.complex128)
+    rng = np.random.default_rng(4)
+    for _ in range(2):
+        out = "".join(str(int(x)) for x in rng.integers(0, 2, size=lat.n))
+        assert abs(a.amplitude(0, out)[0] - b.amplitude(0, out)[0]) <= 1e-10 * abs(a.amplitude(0, out)[0])
