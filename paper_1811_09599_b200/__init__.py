@@ -12,7 +12,8 @@ fallback: without a CUDA device the numeric calls raise.
 from ._lib import LibraryMissingError, MemoryBudgetError
 from .amplitude_engine import (AmplitudeBatch, AmplitudeEngine, FidelitySpec, PathStats,
                                amplitude_record, batch_records, mixed_state_samples,
-                               read_amplitudes, set_path_batching, write_amplitudes)
+                               read_amplitudes, set_path_batching, set_single_call_graphs,
+                               write_amplitudes)
 from .circuits import (Circuit, CircuitFormatError, DepthSpec, Gate, Lattice, cross_gate_count,
                        cz_cut_count, edge_activations, generate_rqc, parse_circuit, pattern_bonds,
                        write_circuit)
@@ -37,7 +38,7 @@ __all__ = [
     "cz_cut_count", "edge_activations", "generate_rqc", "parse_circuit", "pattern_bonds",
     "write_circuit",
     "Tensor", "PermutePlan", "plan_permutation", "permute_fast", "permute_naive", "contract",
-    "set_gemm_mode", "set_path_batching", "get_gemm_mode", "benchmark_permute", "benchmark_csv",
+    "set_gemm_mode", "set_path_batching", "set_single_call_graphs", "get_gemm_mode", "benchmark_permute", "benchmark_csv",
     "Net2D", "Net3D", "build_3d", "contract_time", "contract_grid", "gate_tensor",
     "ContractionPlan", "CutSpec", "ContractStep", "PlanError", "MemoryBudgetError",
     "PlanExecutor", "CostEstimate", "parse_plan", "format_plan", "builtin_plan", "grid_plan",

@@ -42,8 +42,16 @@ namespace tc {
 // epilogue staging tile (32 rows x CPW complex, rows padded by 16 B so both
 // the row-per-lane writes and the row-contiguous reads are conflict-free)
 template <int STAGES, int RAW, int NW, int NE, int BN_ = V2_BN, int CK_ = 0, int NPW_ = 0,
-          bool TMA_ = false, bool G3_ = false>
+          bool TMA_ = false, bool G3_ = false, int ALT_ = 1>
 struct LayoutK {
+  // ALT_ = 2: the NW converter warps form two groups that take alternate
+  // k-blocks (group g converts k-blocks q with q % 2 == g), so each warp has
+  // two k-blocks of tensor time to cover its per-k-block latency chain
+  // (mbarrier waits, shared-memory round trips, the async-proxy fence,
+  // tcgen05.st + wait) -- with one group the converters, not the tensor
+  // pipe, paced the long-K kernel (tensor pipe ~46% active).
+  static_assert(ALT_ == 1 || (ALT_ == 2 && G3_ && NW == 16), "alternating groups: Gauss form");
+  static constexpr int ALT = ALT_;
   // G3_: the Gauss (3-multiplication) form of the complex product on the
   // tensor pipe -- T1 = Ar.Br, T2 = Ai.Bi, T3 = (Ar+Ai).(Br+Bi), Re = T1 - T2,
   // Im = T3 - T1 - T2 -- i.e. 9 TF32 MMAs of N = BN per 8 complex k instead
@@ -51,7 +59,7 @@ struct LayoutK {
   // (hi and lo), A in TMEM holds Ar, Ai, Ar+Ai (hi and lo: 48 columns per
   // stage).  Long-K TMA-fed only: one TMEM partial [T1 | T2 | T3] drained by
   // the promotion warps into the fp32 master [Re | Im] every CK_ k-blocks.
-  static_assert(!G3_ || (CK_ > 0 && TMA_ && NPW_ == 1 && BN_ == 64 && NW == 8),
+  static_assert(!G3_ || (CK_ > 0 && TMA_ && NPW_ == 1 && BN_ == 64 && NW == 8 * ALT_),
                 "the Gauss form is a long-K TMA-fed flavour with 64-column tiles");
   static constexpr bool G3 = G3_;
   static_assert(NPW_ == 0 || (NPW_ == (TMA_ ? 1 : 4) && NE == 4 && (BN_ == 64 || (TMA_ && BN_ == 32))),
@@ -68,7 +76,7 @@ struct LayoutK {
   static_assert(BN_ == 64 || (NE >= 4 && (BN_ == 8 || BN_ == 16 || BN_ == 32)),
                 "narrow N tiles need the epilogue warps");
   static constexpr int NT = NW * 32;                 // converter threads
-  static constexpr int NWG = NW / 4;                 // warps per TMEM lane quadrant
+  static constexpr int NWG = NW / ALT_ / 4;          // warps per TMEM lane quadrant (per group)
   static constexpr int KPW = KB / NWG;               // k of a k-block per warp
   static constexpr int BN = BN_;                     // complex output columns per tile
   static constexpr int CPW = BN / NWG;               // epilogue columns per warp
@@ -99,12 +107,13 @@ struct LayoutK {
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-template <int STAGES, int RAW, int NW, int NE, int BN_, int CK_, int NPW, bool TMA, bool G3 = false>
+template <int STAGES, int RAW, int NW, int NE, int BN_, int CK_, int NPW, bool TMA, bool G3 = false,
+          int ALT = 1>
 __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     cgemm_tc3k_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, uint32_t chunk, const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB) {
-  using L = LayoutK<STAGES, RAW, NW, NE, BN_, CK_, NPW, TMA, G3>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN_, CK_, NPW, TMA, G3, ALT>;
   // NPW > 0: 4 producer warps own the global fetch (cp.async into padded raw
   // rows, completion signalled on per-slot mbarriers); the converter warps
   // only read, split and store into TMEM / the B' planes.
@@ -131,11 +140,11 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
 
   if (tid == 0) {
     for (int i = 0; i < STAGES + 2; ++i) mbar_init(&bars[i], 1);
-    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], NW);
+    for (int i = 0; i < STAGES; ++i) mbar_init(&full[i], NW / ALT);
     for (int i = 0; i < 2; ++i) mbar_init(&accfree[i], NE ? NE : 1);
     for (int i = 0; i < RAW; ++i) {
       mbar_init(&rawfull[i], (NPW && !TMA) ? NPW * 32 : 1);
-      mbar_init(&rawfree[i], NW);
+      mbar_init(&rawfree[i], NW / ALT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -213,73 +222,79 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
 
 
   if (warp == NW + NE + NPW) {
-    // ===== MMA issuer (whole warp walks the sequence, one elected lane issues)
-    uint32_t q = 0, t = 0, chunkc = 0;
-    for (uint32_t w = w0; w < w1; w += wstep, ++t) {
-      for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
-        const uint32_t s = q & (STAGES - 1);
-        mbar_wait(&full[s], (q / STAGES) & 1u);
-        tc_fence_after();
-        uint32_t pbuf = t & 1u;
-        uint32_t pos = kb;
-        if constexpr (G3) {
-          // one partial buffer: the promotion warps read chunk c-1 out of it
-          // before chunk c's first MMA overwrites it
-          pos = kb & (CK_ - 1);
-          pbuf = 0;
-          if (pos == 0 && chunkc >= 1) {
-            mbar_wait(&accfree[0], (chunkc - 1) & 1u);
-            tc_fence_after();
-          }
-        } else if constexpr (PROMO) {
-          pos = kb & (CK_ - 1);
-          pbuf = chunkc & 1u;
-          if (pos == 0 && chunkc >= 2) {  // promotion warps drained this partial
-            mbar_wait(&accfree[pbuf], ((chunkc >> 1) + 1) & 1u);
-            tc_fence_after();
-          }
-        }
-        const uint32_t d = tmem + pbuf * (uint32_t)L::P_COLS;
-        uint8_t *stage = smem + s * L::STAGE;
-        const uint32_t bhi = smem_u32(stage), blo = smem_u32(stage + L::B_PLANE);
-        const uint64_t b1h = smem_desc(bhi + L::B_BLOCK), b1l = smem_desc(blo + L::B_BLOCK);
-        const uint64_t b2h = smem_desc(bhi), b2l = smem_desc(blo);
-        const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * (uint32_t)L::A_STAGE_COLS;
-        const uint32_t acc0 = pos > 0 ? 1u : 0u;
-        const bool chunk_end = PROMO ? (pos == CK_ - 1 || kb == nk - 1) : (kb == nk - 1);
-        if (!PROMO && NE > 0 && kb == 0 && t >= 2) {  // epilogue warps drained this buffer (tile t-2)
-          mbar_wait(&accfree[t & 1u], ((t >> 1) + 1) & 1u);
+    // ===== MMA issuer: lane 0 alone walks the sequence (tcgen05.mma is issued
+    // by one thread; a lone lane needs no elect/convergence code).  Per stage
+    // only the waits, the MMAs and the commits run: the B' descriptors are
+    // the stage-0 descriptor plus a constant byte offset >> 4 (the address
+    // field is the descriptor's low 14 bits and shared memory < 256 KB), the
+    // A planes a constant TMEM column offset.  With 9 N = 64 MMAs per stage
+    // (Gauss form) the issue loop itself used to pace the tensor pipe.
+    if (lane == 0) {
+      const uint64_t desc0 = smem_desc(smem_u32(smem));
+      constexpr uint32_t ST16 = (uint32_t)L::STAGE >> 4, BP16 = (uint32_t)L::B_PLANE >> 4,
+                         BB16 = (uint32_t)L::B_BLOCK >> 4;
+      uint32_t q = 0, t = 0, chunkc = 0;
+      for (uint32_t w = w0; w < w1; w += wstep, ++t) {
+        for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+          const uint32_t s = q & (STAGES - 1);
+          mbar_wait(&full[s], (q / STAGES) & 1u);
           tc_fence_after();
-        }
-        if constexpr (G3) {
-          if (elect_one()) {
+          uint32_t pbuf = t & 1u;
+          uint32_t pos = kb;
+          if constexpr (G3) {
+            // one partial buffer: the promotion warps read chunk c-1 out of it
+            // before chunk c's first MMA overwrites it
+            pos = kb & (CK_ - 1);
+            pbuf = 0;
+            if (pos == 0 && chunkc >= 1) {
+              mbar_wait(&accfree[0], (chunkc - 1) & 1u);
+              tc_fence_after();
+            }
+          } else if constexpr (PROMO) {
+            pos = kb & (CK_ - 1);
+            pbuf = chunkc & 1u;
+            if (pos == 0 && chunkc >= 2) {  // promotion warps drained this partial
+              mbar_wait(&accfree[pbuf], ((chunkc >> 1) + 1) & 1u);
+              tc_fence_after();
+            }
+          }
+          if (!PROMO && NE > 0 && kb == 0 && t >= 2) {  // epilogue warps drained this buffer (tile t-2)
+            mbar_wait(&accfree[t & 1u], ((t >> 1) + 1) & 1u);
+            tc_fence_after();
+          }
+          const uint32_t d = tmem + pbuf * (uint32_t)L::P_COLS;
+          const uint64_t bh = desc0 + (uint64_t)(s * ST16), bl = bh + BP16;
+          const uint32_t a = tmem + (uint32_t)L::A_COL0 + s * (uint32_t)L::A_STAGE_COLS;
+          const uint32_t acc0 = pos > 0 ? 1u : 0u;
+          const bool chunk_end = PROMO ? (pos == CK_ - 1 || kb == nk - 1) : (kb == nk - 1);
+          if constexpr (G3) {
             // A planes: Ar hi/lo (+0, +8), Ai hi/lo (+16, +24), Ar+Ai hi/lo
             // (+32, +40); B' blocks 0/1/2 = Br, Bi, Br+Bi (hi plane, lo plane)
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-              const uint64_t bh = smem_desc(bhi + j * L::B_BLOCK), bl = smem_desc(blo + j * L::B_BLOCK);
               const uint32_t dj = d + (uint32_t)(j * BN_);
-              mma_ts(dj, a + 16 * j, bh, IDESC, acc0);
-              mma_ts(dj, a + 16 * j, bl, IDESC, 1u);
-              mma_ts(dj, a + 16 * j + 8, bh, IDESC, 1u);
+              mma_ts(dj, a + 16 * j, bh + j * BB16, IDESC, acc0);
+              mma_ts(dj, a + 16 * j, bl + j * BB16, IDESC, 1u);
+              mma_ts(dj, a + 16 * j + 8, bh + j * BB16, IDESC, 1u);
             }
             mma_commit(&bars[s]);
             if (chunk_end) mma_commit(&pbar[0]);
+          } else {
+            // [Dre|Dim] += Ar.[Br|Bi] + Ai.[-Bi|Br]: windows at B' blocks 1 and 0
+            mma_ts(d, a + 0, bh + BB16, IDESC, acc0);
+            mma_ts(d, a + 0, bl + BB16, IDESC, 1u);
+            mma_ts(d, a + 8, bh + BB16, IDESC, 1u);
+            mma_ts(d, a + 16, bh, IDESC, 1u);
+            mma_ts(d, a + 16, bl, IDESC, 1u);
+            mma_ts(d, a + 24, bh, IDESC, 1u);
+            mma_commit(&bars[s]);
+            if (chunk_end) mma_commit(&pbar[pbuf]);
           }
-        } else if (elect_one()) {
-          mma_ts(d, a + 0, b1h, IDESC, acc0);
-          mma_ts(d, a + 0, b1l, IDESC, 1u);
-          mma_ts(d, a + 8, b1h, IDESC, 1u);
-          mma_ts(d, a + 16, b2h, IDESC, 1u);
-          mma_ts(d, a + 16, b2l, IDESC, 1u);
-          mma_ts(d, a + 24, b2h, IDESC, 1u);
-          mma_commit(&bars[s]);
-          if (chunk_end) mma_commit(&pbar[pbuf]);
+          if (PROMO && chunk_end) ++chunkc;
         }
-        if (PROMO && chunk_end) ++chunkc;
-        __syncwarp();
       }
     }
+    __syncwarp();
   } else if (TMA && warp >= NW + NE) {
     // ===== TMA producer (one elected lane): per k-block one box of A and,
     // unless resident, one box of B into the raw ring; the mbarrier's
@@ -497,18 +512,19 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         mbar_wait(&pbar[0], chunkc & 1u);
         tc_fence_after();
         const uint32_t pbase = tmem + lane_base;
+        constexpr int PC = L::ALT > 1 ? 8 : 16;   // columns per piece (register budget)
 #pragma unroll 1
-        for (int piece = 0; piece < BN / 16; ++piece) {
-          uint32_t t1[16], t2[16], t3[16], mr[16], mi[16];
-          tmem_ld16(pbase + piece * 16, t1);
-          tmem_ld16(pbase + BN + piece * 16, t2);
-          tmem_ld16(pbase + 2 * BN + piece * 16, t3);
+        for (int piece = 0; piece < BN / PC; ++piece) {
+          uint32_t t1[PC], t2[PC], t3[PC], mr[PC], mi[PC];
+          tmem_ld_cols<PC>(pbase + piece * PC, t1);
+          tmem_ld_cols<PC>(pbase + BN + piece * PC, t2);
+          tmem_ld_cols<PC>(pbase + 2 * BN + piece * PC, t3);
           if (c > 0) {
-            tmem_ld16(mbase + piece * 16, mr);
-            tmem_ld16(mbase + BN + piece * 16, mi);
+            tmem_ld_cols<PC>(mbase + piece * PC, mr);
+            tmem_ld_cols<PC>(mbase + BN + piece * PC, mi);
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (piece == BN / 16 - 1) {
+          if (piece == BN / PC - 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0)
@@ -516,14 +532,14 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
                            : "memory");
           }
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < PC; ++j) {
             const float x1 = __uint_as_float(t1[j]), x2 = __uint_as_float(t2[j]);
             const float re = x1 - x2, im = __uint_as_float(t3[j]) - x1 - x2;
             t1[j] = __float_as_uint(c > 0 ? __uint_as_float(mr[j]) + re : re);
             t2[j] = __float_as_uint(c > 0 ? __uint_as_float(mi[j]) + im : im);
           }
-          tmem_st16(mbase + piece * 16, t1);
-          tmem_st16(mbase + BN + piece * 16, t2);
+          tmem_st_cols<PC>(mbase + piece * PC, t1);
+          tmem_st_cols<PC>(mbase + BN + piece * PC, t2);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
@@ -667,21 +683,26 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     // (slot released at once), split, B' planes + tcgen05.st of A
     int b_n, b_k;
     uint32_t boff;
-    constexpr int BE = (BN * KB) / NT;  // B elements per thread per k-block (BN = 64)
+    constexpr int NTG = NT / ALT;         // converter threads per group
+    const int gtid = tid % NTG, grp = tid / NTG;
+    constexpr int BE = (BN * KB) / NTG;   // B elements per thread per k-block (BN = 64)
     if constexpr (BE == 2) {
-      // half-warps split by k pair: each half reads one contiguous 128-byte
-      // run of a k row of the raw B box (conflict-free), the B' stores of the
-      // two halves interleave 8-byte words of the same core-matrix rows
-      const int b_kp = (tid >> 4) & 1, b_chunk = tid >> 7;
-      b_n = (tid & 15) | (((tid >> 5) & 3) << 4);
+      // a half-warp covers 16 columns n0..n0+15: lanes 0-7 take n0..n0+7 at
+      // one k pair, lanes 8-15 n0+8..n0+15 at the other (the next half-warp
+      // the swapped pairs).  The raw-B reads (two k rows, 1 KB apart) then
+      // touch disjoint bank halves, and the 8-byte B' stores of the 16 lanes
+      // fill all 32 banks of one core-matrix row block: one wavefront each.
+      const int t = gtid & 127, hw = t >> 4, l = t & 15;
+      const int b_kp = ((l >> 3) & 1) ^ (hw & 1), b_chunk = gtid >> 7;
+      b_n = 16 * (hw >> 1) + (l & 7) + 8 * ((l >> 3) & 1);
       b_k = b_chunk * 4 + b_kp * 2;
       boff = core_off(b_n, b_chunk) + (uint32_t)(b_kp * 8);
     } else {
-      b_k = tid & 7;
-      b_n = tid >> 3;
+      b_k = gtid & 7;
+      b_n = gtid >> 3;
       boff = core_off(b_n, b_k >> 2) + (uint32_t)((b_k & 3) * 4);
     }
-    const uint32_t kw0 = (uint32_t)(wg * KPW);
+    const uint32_t kw0 = (uint32_t)((wg % L::NWG) * KPW);
     constexpr int CPR = KPW / 2;
     Cur cc;
     cur_init(cc, w0);
@@ -689,6 +710,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
     for (; cc.w < w1; cur_next(cc)) {
       const bool breuse = rd != 0u && cc.run >= rd;
       for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
+        if (ALT > 1 && (int)(q % ALT) != grp) continue;   // the other group's k-block
         const uint32_t slot = q & (RAW - 1), s = q & (STAGES - 1);
         mbar_wait(&rawfull[slot], (q / RAW) & 1u);
         const uint8_t *rA = smem + L::RAWA_OFF + slot * L::RAWA_SLOT;
@@ -806,7 +828,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             split_fast(av[p].z + av[p].w, sh[2 * p + 1], sl[2 * p + 1]);
           }
           const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * L::A_STAGE_COLS) + kw0;
-          static_assert(KPW == 4, "Gauss form: 8 converter warps");
+          static_assert(KPW == 4, "Gauss form: 8 converter warps per group");
           tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
           tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
           tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
@@ -1230,10 +1252,10 @@ bool tma_ok(const GemmArgs &g) {
 }
 
 template <int STAGES, int RAW, int NW, int NE, int BN = V2_BN, int CK = 0, int NPW = 0, bool TMA = false,
-          bool G3 = false>
+          bool G3 = false, int ALT = 1>
 int launch_short(const GemmArgs &g, cudaStream_t s) {
-  using L = LayoutK<STAGES, RAW, NW, NE, BN, CK, NPW, TMA, G3>;
-  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN, CK, NPW, TMA, G3>;
+  using L = LayoutK<STAGES, RAW, NW, NE, BN, CK, NPW, TMA, G3, ALT>;
+  auto kern = cgemm_tc3k_kernel<STAGES, RAW, NW, NE, BN, CK, NPW, TMA, G3, ALT>;
   CUtensorMap tmA{}, tmB{};
   if constexpr (TMA) {
     const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
@@ -1346,6 +1368,8 @@ static int launch_long(const GemmArgs &g, cudaStream_t s) {
     if (g_tc3_variant == 27) return tc::launch_short<4, 8, 8, 4, 64, 32, 1, true>(g, s);
     if (g_tc3_variant == 30) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true, true>(g, s);
     if (g_tc3_variant == 31) return tc::launch_short<4, 8, 8, 4, 64, 32, 1, true, true>(g, s);
+    if (g_tc3_variant == 32) return tc::launch_short<4, 8, 8, 4, 64, 64, 1, true, true>(g, s);
+    if (g_tc3_variant == 33) return tc::launch_short<4, 8, 16, 4, 64, 64, 1, true, true, 2>(g, s);
     return tc::launch_short<4, 8, 8, 4, 64, 64, 1, true, true>(g, s);
   }
   return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);

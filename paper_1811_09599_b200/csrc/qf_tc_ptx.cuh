@@ -219,6 +219,14 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&v)[CPW])
 // fp32 bit patterns) -> C through the warp's staging tile: alpha applied in
 // registers, then each store instruction covers whole row segments; beta and
 // ragged edges are handled per 16-byte pair.  `c` = C at (row m0, column c0).
+template <int CPW>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t (&v)[CPW]) {
+  if constexpr (CPW == 32) tmem_st32(taddr, v);
+  else if constexpr (CPW == 16) tmem_st16(taddr, v);
+  else if constexpr (CPW == 8) tmem_st8(taddr, v);
+  else __trap();
+}
+
 template <int CH, int PITCH>
 __device__ __forceinline__ void stage_store_chunk(uint8_t *stg, const uint32_t (&vr)[CH],
                                                   const uint32_t (&vi)[CH], float2 *c, int64_t ldc,
