@@ -222,14 +222,16 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
 
 
   if (warp == NW + NE + NPW) {
-    // ===== MMA issuer: lane 0 alone walks the sequence (tcgen05.mma is issued
-    // by one thread; a lone lane needs no elect/convergence code).  Per stage
-    // only the waits, the MMAs and the commits run: the B' descriptors are
-    // the stage-0 descriptor plus a constant byte offset >> 4 (the address
-    // field is the descriptor's low 14 bits and shared memory < 256 KB), the
-    // A planes a constant TMEM column offset.  With 9 N = 64 MMAs per stage
-    // (Gauss form) the issue loop itself used to pace the tensor pipe.
-    if (lane == 0) {
+    // ===== MMA issuer: the whole warp walks the sequence (its values stay in
+    // uniform registers), one elected lane issues.  Per stage only the
+    // waits, the MMAs and the commits run: the B' descriptors are the
+    // stage-0 descriptor plus a constant byte offset >> 4 (the address field
+    // is the descriptor's low 14 bits and shared memory < 256 KB), the A
+    // planes a constant TMEM column offset.  With 9 N = 64 MMAs per stage
+    // (Gauss form) per-stage descriptor arithmetic used to pace the tensor
+    // pipe.  (A lone-lane loop is worse: every MMA then needs an
+    // elect/broadcast waterfall to move its operands to uniform registers.)
+    {
       const uint64_t desc0 = smem_desc(smem_u32(smem));
       constexpr uint32_t ST16 = (uint32_t)L::STAGE >> 4, BP16 = (uint32_t)L::B_PLANE >> 4,
                          BB16 = (uint32_t)L::B_BLOCK >> 4;
@@ -268,18 +270,20 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           const uint32_t acc0 = pos > 0 ? 1u : 0u;
           const bool chunk_end = PROMO ? (pos == CK_ - 1 || kb == nk - 1) : (kb == nk - 1);
           if constexpr (G3) {
-            // A planes: Ar hi/lo (+0, +8), Ai hi/lo (+16, +24), Ar+Ai hi/lo
-            // (+32, +40); B' blocks 0/1/2 = Br, Bi, Br+Bi (hi plane, lo plane)
+            if (elect_one()) {
+              // A planes: Ar hi/lo (+0, +8), Ai hi/lo (+16, +24), Ar+Ai hi/lo
+              // (+32, +40); B' blocks 0/1/2 = Br, Bi, Br+Bi (hi plane, lo plane)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              const uint32_t dj = d + (uint32_t)(j * BN_);
-              mma_ts(dj, a + 16 * j, bh + j * BB16, IDESC, acc0);
-              mma_ts(dj, a + 16 * j, bl + j * BB16, IDESC, 1u);
-              mma_ts(dj, a + 16 * j + 8, bh + j * BB16, IDESC, 1u);
+              for (int j = 0; j < 3; ++j) {
+                const uint32_t dj = d + (uint32_t)(j * BN_);
+                mma_ts(dj, a + 16 * j, bh + j * BB16, IDESC, acc0);
+                mma_ts(dj, a + 16 * j, bl + j * BB16, IDESC, 1u);
+                mma_ts(dj, a + 16 * j + 8, bh + j * BB16, IDESC, 1u);
+              }
+              mma_commit(&bars[s]);
+              if (chunk_end) mma_commit(&pbar[0]);
             }
-            mma_commit(&bars[s]);
-            if (chunk_end) mma_commit(&pbar[0]);
-          } else {
+          } else if (elect_one()) {
             // [Dre|Dim] += Ar.[Br|Bi] + Ai.[-Bi|Br]: windows at B' blocks 1 and 0
             mma_ts(d, a + 0, bh + BB16, IDESC, acc0);
             mma_ts(d, a + 0, bl + BB16, IDESC, 1u);
@@ -291,10 +295,10 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             if (chunk_end) mma_commit(&pbar[pbuf]);
           }
           if (PROMO && chunk_end) ++chunkc;
+          __syncwarp();
         }
       }
     }
-    __syncwarp();
   } else if (TMA && warp >= NW + NE) {
     // ===== TMA producer (one elected lane): per k-block one box of A and,
     // unless resident, one box of B into the raw ring; the mbarrier's
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         // Gauss form: master [Re | Im] (+)= [T1 - T2 | T3 - T1 - T2] from the
         // single partial [T1 | T2 | T3]; the partial is released to the MMA
         // warp as soon as its last piece has been read
-        mbar_wait(&pbar[0], chunkc & 1u);
+        mbar_wait_sleep(&pbar[0], chunkc & 1u, 2000u);   // a chunk is ~20 us of MMAs
         tc_fence_after();
         const uint32_t pbase = tmem + lane_base;
         constexpr int PC = L::ALT > 1 ? 8 : 16;   // columns per piece (register budget)
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
       }
       for (uint32_t c = 0; c < nchunks && !L::G3; ++c, ++chunkc) {
         const uint32_t pbuf = chunkc & 1u;
-        mbar_wait(&pbar[pbuf], (chunkc >> 1) & 1u);
+        mbar_wait_sleep(&pbar[pbuf], (chunkc >> 1) & 1u, 500u);
         tc_fence_after();
         const uint32_t pbase = tmem + lane_base + pbuf * (uint32_t)L::P_COLS;
 #pragma unroll 1
@@ -764,28 +768,58 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         if (lane == 0)  // release semantics order the reads above before the refill
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&rawfree[slot]))
                        : "memory");
-        if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
-        if (!breuse && L::G3) {
-          // Gauss form: B' blocks [Br | Bi | Br + Bi], hi and lo planes
-          uint8_t *stage = smem + s * L::STAGE;
-          uint8_t *ph = stage, *pl = stage + L::B_PLANE;
+        if constexpr (L::G3) {
+          // Gauss form.  Everything is split into registers BEFORE the wait
+          // for the stage to be free, so only the stores sit between the
+          // tensor pipe releasing stage s and this warp's arrival on full[s]
+          // (that latency, not bandwidth, paced the pipe).  B' blocks [Br | Bi
+          // | Br + Bi] (hi and lo planes); A planes Ar, Ai, Ar + Ai in TMEM
+          // (hi at +0/+16/+32, lo 8 columns after).
+          uint32_t bp[12];
           if constexpr (BE == 2) {
-            uint32_t hr0, lr0, hi0, li0, hs0, ls0, hr1, lr1, hi1, li1, hs1, ls1;
-            split_fast(bb4.x, hr0, lr0);
-            split_fast(bb4.y, hi0, li0);
-            split_fast(bb4.x + bb4.y, hs0, ls0);
-            split_fast(bb4.z, hr1, lr1);
-            split_fast(bb4.w, hi1, li1);
-            split_fast(bb4.z + bb4.w, hs1, ls1);
-            *reinterpret_cast<uint2 *>(ph + 0 * L::B_BLOCK + boff) = make_uint2(hr0, hr1);
-            *reinterpret_cast<uint2 *>(ph + 1 * L::B_BLOCK + boff) = make_uint2(hi0, hi1);
-            *reinterpret_cast<uint2 *>(ph + 2 * L::B_BLOCK + boff) = make_uint2(hs0, hs1);
-            *reinterpret_cast<uint2 *>(pl + 0 * L::B_BLOCK + boff) = make_uint2(lr0, lr1);
-            *reinterpret_cast<uint2 *>(pl + 1 * L::B_BLOCK + boff) = make_uint2(li0, li1);
-            *reinterpret_cast<uint2 *>(pl + 2 * L::B_BLOCK + boff) = make_uint2(ls0, ls1);
+            split_fast(bb4.x, bp[0], bp[6]);
+            split_fast(bb4.y, bp[2], bp[8]);
+            split_fast(bb4.x + bb4.y, bp[4], bp[10]);
+            split_fast(bb4.z, bp[1], bp[7]);
+            split_fast(bb4.w, bp[3], bp[9]);
+            split_fast(bb4.z + bb4.w, bp[5], bp[11]);
           }
-          fence_async_smem();
-        } else if (!breuse) {
+          uint32_t rh[KPW], rl[KPW], ih[KPW], il[KPW], sh[KPW], sl[KPW];
+#pragma unroll
+          for (int p = 0; p < CPR; ++p) {
+            split_fast(av[p].x, rh[2 * p], rl[2 * p]);
+            split_fast(av[p].y, ih[2 * p], il[2 * p]);
+            split_fast(av[p].x + av[p].y, sh[2 * p], sl[2 * p]);
+            split_fast(av[p].z, rh[2 * p + 1], rl[2 * p + 1]);
+            split_fast(av[p].w, ih[2 * p + 1], il[2 * p + 1]);
+            split_fast(av[p].z + av[p].w, sh[2 * p + 1], sl[2 * p + 1]);
+          }
+          if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
+          if (!breuse) {
+            uint8_t *stage = smem + s * L::STAGE;
+            uint8_t *ph = stage, *pl = stage + L::B_PLANE;
+            if constexpr (BE == 2) {
+#pragma unroll
+              for (int j = 0; j < 3; ++j) {
+                *reinterpret_cast<uint2 *>(ph + j * L::B_BLOCK + boff) = make_uint2(bp[2 * j], bp[2 * j + 1]);
+                *reinterpret_cast<uint2 *>(pl + j * L::B_BLOCK + boff) =
+                    make_uint2(bp[6 + 2 * j], bp[6 + 2 * j + 1]);
+              }
+            }
+            fence_async_smem();
+          }
+          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * L::A_STAGE_COLS) + kw0;
+          static_assert(KPW == 4, "Gauss form: 8 converter warps per group");
+          tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+          tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+          tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+          tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+          tmem_st4(acol + 32, sh[0], sh[1], sh[2], sh[3]);
+          tmem_st4(acol + 40, sl[0], sl[1], sl[2], sl[3]);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        } else {
+        if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
+        if (!breuse) {
           uint8_t *stage = smem + s * L::STAGE;
           uint8_t *ph = stage, *pl = stage + L::B_PLANE;
           if constexpr (BE == 2) {
@@ -815,28 +849,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           }
           fence_async_smem();
         }
-        if constexpr (L::G3) {
-          // A planes Ar, Ai, Ar + Ai (hi at +0/+16/+32, lo 8 columns after)
-          uint32_t rh[KPW], rl[KPW], ih[KPW], il[KPW], sh[KPW], sl[KPW];
-#pragma unroll
-          for (int p = 0; p < CPR; ++p) {
-            split_fast(av[p].x, rh[2 * p], rl[2 * p]);
-            split_fast(av[p].y, ih[2 * p], il[2 * p]);
-            split_fast(av[p].x + av[p].y, sh[2 * p], sl[2 * p]);
-            split_fast(av[p].z, rh[2 * p + 1], rl[2 * p + 1]);
-            split_fast(av[p].w, ih[2 * p + 1], il[2 * p + 1]);
-            split_fast(av[p].z + av[p].w, sh[2 * p + 1], sl[2 * p + 1]);
-          }
-          const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * L::A_STAGE_COLS) + kw0;
-          static_assert(KPW == 4, "Gauss form: 8 converter warps per group");
-          tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
-          tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
-          tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
-          tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
-          tmem_st4(acol + 32, sh[0], sh[1], sh[2], sh[3]);
-          tmem_st4(acol + 40, sl[0], sl[1], sl[2], sl[3]);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        } else {
+        {
           uint32_t rh[KPW], rl[KPW], ih[KPW], il[KPW];
 #pragma unroll
           for (int p = 0; p < CPR; ++p) {
@@ -859,6 +872,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
+        }  // real-block form
         tc_fence_before();
         __syncwarp();
         if (lane == 0)
