@@ -80,6 +80,11 @@ struct GemmArgs {
   // outputs of several open-output values computed side by side land as
   // separate [M][c_nblk] blocks (ldc = c_nblk)
   int64_t c_nblk = 0, c_bstride = 0;
+  // profiling knob of the long-K Gauss kernel (env QF_TC3_DEBUG, results are
+  // garbage when set): 1 = skip the B' stores, 2 = skip the A tcgen05.st,
+  // 4 = promotion warps release the partial without reading it, 8 = the
+  // TMA producer loads nothing (the converters re-read stale raw slots)
+  int dbg = 0;
 };
 
 __device__ __forceinline__ int64_t a_row_base(const GemmArgs &g, int64_t r) {

@@ -235,6 +235,10 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
       const uint64_t desc0 = smem_desc(smem_u32(smem));
       constexpr uint32_t ST16 = (uint32_t)L::STAGE >> 4, BP16 = (uint32_t)L::B_PLANE >> 4,
                          BB16 = (uint32_t)L::B_BLOCK >> 4;
+      // (Measured alternatives for the Gauss form, all slower on the full
+      // kernel: one lane issuing alone (operand waterfalls), waiting on every
+      // other stage, and issuing k-block pairs per elect block -- the latter
+      // two only win when the converters are idle; profiles/r2_gemm_notes.md.)
       uint32_t q = 0, t = 0, chunkc = 0;
       for (uint32_t w = w0; w < w1; w += wstep, ++t) {
         for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             // before chunk c's first MMA overwrites it
             pos = kb & (CK_ - 1);
             pbuf = 0;
-            if (pos == 0 && chunkc >= 1) {
+            if (pos == 0 && chunkc >= 1 && !(g.dbg & 64)) {
               mbar_wait(&accfree[0], (chunkc - 1) & 1u);
               tc_fence_after();
             }
@@ -325,9 +329,18 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           if (g.v_t) v_ra *= 2;  // float coordinate of the contiguous row run
         }
         for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+          if (g.dbg & 32) continue;   // profiling: converters only hand stages over
           const uint32_t slot = f & (RAW - 1);
           if (f >= RAW) mbar_wait(&rawfree[slot], ((f / RAW) + 1) & 1u);
           const uint32_t bar = smem_u32(&rawfull[slot]);
+          if (g.dbg & 8) {   // profiling: no operand traffic at all
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+            if (++v_ki == (g.v_kin ? (int32_t)(g.v_kin / KB) : 1)) {
+              v_ki = 0;
+              ++v_ko;
+            }
+            continue;
+          }
           const uint32_t bytes = L::RAWA_SLOT + (breuse ? 0u : (uint32_t)L::RAWB_SLOT);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                        : "memory");
@@ -513,8 +526,14 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
         // Gauss form: master [Re | Im] (+)= [T1 - T2 | T3 - T1 - T2] from the
         // single partial [T1 | T2 | T3]; the partial is released to the MMA
         // warp as soon as its last piece has been read
-        mbar_wait_sleep(&pbar[0], chunkc & 1u, 2000u);   // a chunk is ~20 us of MMAs
+        mbar_wait_sleep(&pbar[0], chunkc & 1u, 200u);   // a chunk is ~10 us of MMAs
         tc_fence_after();
+        if (g.dbg & 4) {
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[0])) : "memory");
+          continue;
+        }
         const uint32_t pbase = tmem + lane_base;
         constexpr int PC = L::ALT > 1 ? 8 : 16;   // columns per piece (register budget)
 #pragma unroll 1
@@ -716,6 +735,14 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
       for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
         if (ALT > 1 && (int)(q % ALT) != grp) continue;   // the other group's k-block
         const uint32_t slot = q & (RAW - 1), s = q & (STAGES - 1);
+        if (g.dbg & 32) {   // profiling: only the stage handshake (use with 8: no producer traffic)
+          if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+          continue;
+        }
         mbar_wait(&rawfull[slot], (q / RAW) & 1u);
         const uint8_t *rA = smem + L::RAWA_OFF + slot * L::RAWA_SLOT;
         const uint8_t *rB = smem + L::RAWB_OFF + slot * L::RAWB_SLOT;
@@ -795,7 +822,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
             split_fast(av[p].z + av[p].w, sh[2 * p + 1], sl[2 * p + 1]);
           }
           if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
-          if (!breuse) {
+          if (!breuse && !(g.dbg & 1)) {
             uint8_t *stage = smem + s * L::STAGE;
             uint8_t *ph = stage, *pl = stage + L::B_PLANE;
             if constexpr (BE == 2) {
@@ -810,13 +837,15 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
           }
           const uint32_t acol = tmem + lane_base + (uint32_t)(L::A_COL0 + s * L::A_STAGE_COLS) + kw0;
           static_assert(KPW == 4, "Gauss form: 8 converter warps per group");
-          tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
-          tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
-          tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
-          tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
-          tmem_st4(acol + 32, sh[0], sh[1], sh[2], sh[3]);
-          tmem_st4(acol + 40, sl[0], sl[1], sl[2], sl[3]);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (!(g.dbg & 2)) {
+            tmem_st4(acol + 0, rh[0], rh[1], rh[2], rh[3]);
+            tmem_st4(acol + 8, rl[0], rl[1], rl[2], rl[3]);
+            tmem_st4(acol + 16, ih[0], ih[1], ih[2], ih[3]);
+            tmem_st4(acol + 24, il[0], il[1], il[2], il[3]);
+            tmem_st4(acol + 32, sh[0], sh[1], sh[2], sh[3]);
+            tmem_st4(acol + 40, sl[0], sl[1], sl[2], sl[3]);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          }
         } else {
         if (q >= STAGES) mbar_wait(&bars[s], ((q / STAGES) + 1) & 1u);
         if (!breuse) {
@@ -1383,7 +1412,7 @@ static int launch_long(const GemmArgs &g, cudaStream_t s) {
     if (g_tc3_variant == 30) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true, true>(g, s);
     if (g_tc3_variant == 31) return tc::launch_short<4, 8, 8, 4, 64, 32, 1, true, true>(g, s);
     if (g_tc3_variant == 32) return tc::launch_short<4, 8, 8, 4, 64, 64, 1, true, true>(g, s);
-    if (g_tc3_variant == 33) return tc::launch_short<4, 8, 16, 4, 64, 64, 1, true, true, 2>(g, s);
+    if (g_tc3_variant == 34) return tc::launch_short<2, 8, 8, 4, 64, 64, 1, true, true>(g, s);
     return tc::launch_short<4, 8, 8, 4, 64, 64, 1, true, true>(g, s);
   }
   return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
@@ -1429,7 +1458,17 @@ bool tc3_eligible(const GemmArgs &g) {
   return g.N >= 12 && g.K <= 256 && g.M * g.batch >= 128 * 148;
 }
 
-int gemm_tc3(const GemmArgs &g, cudaStream_t s) {
+static int tc3_debug() {
+  static const int v = [] {
+    const char *e = getenv("QF_TC3_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+int gemm_tc3(const GemmArgs &g_in, cudaStream_t s) {
+  GemmArgs g = g_in;
+  g.dbg = tc3_debug();
   if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
   QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
   if (g.c_nblk && (!g.v_kin || g.K > 128 || g.c_trans)) {

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_gemm.py -q -x -k "tcgen05" > gpurun_out/g32_tests.txt 2>&1
+QF_TC3_DEBUG=44 timeout 120 python scripts/gemm_probe.py --shape 8192,8192,8192 --seconds 2 --check 0 | sed "s/^/dbg=44 /" >> gpurun_out/g32_probe.txt 2>&1
+QF_TC3_DEBUG=3 timeout 120 python scripts/gemm_probe.py --shape 8192,8192,8192 --seconds 2 --check 0 | sed "s/^/dbg=3 /" >> gpurun_out/g32_probe.txt 2>&1
+for s in 8192,8192,8192 32768,32768,32768 4096,4096,65536; do
+  timeout 300 python scripts/gemm_probe.py --shape $s --seconds 5 >> gpurun_out/g32_probe.txt 2>>gpurun_out/g32_err.txt
+done
+echo done

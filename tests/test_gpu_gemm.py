@@ -102,10 +102,10 @@ SHORTK_SHAPES = [(2, 1024, 192, 32), (5, 1000, 64, 60), (64, 256, 64, 16), (256,
                  (9, 300, 5, 24), (4, 640, 32, 64), (3, 512, 24, 130)]
 
 
-@pytest.fixture(params=[0, 10, 11, 12, 13, 19, 20, 21, 26, 31, 33],
+@pytest.fixture(params=[0, 10, 11, 12, 13, 19, 20, 21, 26, 31, 34],
                 ids=["auto", "short-8warps", "short-16warps", "short-epilogue-warps",
                      "long-converter-fetch", "long-real-block", "short-tma", "short-tma-ring4",
-                     "long-real-block-ck16", "long-gauss-ck32", "long-gauss-alt2"])
+                     "long-real-block-ck16", "long-gauss-ck32", "long-gauss-2stages"])
 def tc_variant(request):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(request.param)
@@ -163,9 +163,9 @@ def test_gathered_short_k_many_tiles(a_labels, variant):
 
 
 @pytest.mark.parametrize("K", [1024, 4096, 32768])
-@pytest.mark.parametrize("variant", [0, 13, 19, 26, 27, 30, 31, 33],
+@pytest.mark.parametrize("variant", [0, 13, 19, 26, 27, 30, 31, 34],
                          ids=["default", "converter-fetch", "real-block-ck4", "real-block-ck16",
-                              "real-block-ck32", "gauss-ck16", "gauss-ck32", "gauss-alt2"])
+                              "real-block-ck32", "gauss-ck16", "gauss-ck32", "gauss-2stages"])
 def test_tcgen05_promoted_accuracy_at_long_k(K, variant):
     """Promotion keeps the long-K error near the FFMA kernel's (config-4
     GEMMs have K = 2^15)."""
