@@ -5,8 +5,8 @@ config of BASELINE.json and the tensor-core-bound one): seeded grid:7x7
 random circuit, depth 1+40+1 (bond dim 32), the reference's two cuts
 (1024 slices) in a slice-first plan, fidelity f = 1/64 (16 seeded paths per
 amplitude), 256 seeded bit-strings.  One *step* = one contraction path on
-every rank (`PlanExecutor.run`); value = amplitudes/s = paths/s / 16.  A
-short config-2 run is reported under `secondary`.
+every rank (`PlanExecutor.run`); value = amplitudes/s = paths/s / 16.  Short
+runs of the other configs (2, 1, 3 and 5) are reported under `secondary`.
 
 Config 2 (`--workload config2`, BASELINE configs[1]): seeded grid:5x5
 random circuit, depth 1+24+1 (bond dim 8), 1024 seed-drawn output
@@ -773,7 +773,7 @@ def run_paths(args):
     torch.cuda.empty_cache()
     h2d = d2h = 0
     e2e_s = []
-    for u in range(max(1, args.e2e_units)):
+    for u in range(max(0, args.e2e_units)):
         bits, fixed = units[u]
         e_eng = qf.AmplitudeEngine(circ, plan, device=local, group=group)
         barrier(world)
@@ -795,7 +795,7 @@ def run_paths(args):
         h2d = sum(arr.nbytes for stack in qf.build_3d(circ, 0, None).blocks.values()
                   for _, arr in stack)
         del e_eng
-    e2e_unit_s = max_over_ranks(float(np.mean(e2e_s)), world, dev)
+    e2e_unit_s = max_over_ranks(float(np.mean(e2e_s)) if e2e_s else float("nan"), world, dev)
     e2e = wl["amps_per_unit"] / e2e_unit_s
 
     result = None
@@ -821,8 +821,9 @@ def run_paths(args):
             "executed_tflops": round(exec_flops / args.steps / (ms / 1e3) / 1e12, 2),
             "reference_equivalent_tflops": round(paths_per_s / n_paths * flops_unit / 1e12, 2),
             "gemm_mode": qf.get_gemm_mode(),
-            "e2e": {"value": round(e2e, 6), "unit": "amplitudes/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "seconds_per_unit": round(e2e_unit_s, 2),
+            "e2e": {"value": round(e2e, 6) if e2e_s else None, "unit": "amplitudes/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "seconds_per_unit": round(e2e_unit_s, 2) if e2e_s else None,
                     "api": ("AmplitudeEngine(circuit, plan).amplitude_batch(0, s_ab, c_sites, 64)"
                             if c_sites else "AmplitudeEngine(circuit, plan).amplitude(0, bits, f)")
                            + " per unit, network built from the host circuit every call"},
@@ -965,21 +966,47 @@ def run_reference(args):
                     "d2h_bytes_per_step": 0}}
 
 
-def secondary_config2(args) -> dict:
-    """Config 2 (BASELINE configs[1]) measured in the same run, summarised
-    beside the headline: a short run of the batched bit-string workload."""
-    sub = argparse.Namespace(**vars(args))
-    sub.workload, sub.steps, sub.warmup, sub.no_cpu_baseline = "config2", 10, 3, True
-    try:
-        r = run_gpu(sub)
-    except Exception as exc:  # the headline stands on its own
-        return {"workload": "config2", "error": repr(exc)[:300]}
-    if r is None:
-        return None
-    return {"workload": r["config"]["workload"], "value": r["value"], "unit": r["unit"],
-            "ms_per_step": r["ms_per_step"], "e2e": r["e2e"]["value"],
-            "roofline": {k: r["roofline"].get(k) for k in ("bound", "kernel", "achieved", "peak", "frac")},
-            "gpu_launches": r["gpu_launches"], "self_check": r.get("self_check")}
+def _compact(r: dict) -> dict:
+    out = {"workload": r["config"]["workload"], "value": r["value"], "unit": r["unit"],
+           "ms_per_step": r.get("ms_per_step"), "steps": r.get("steps"),
+           "e2e": (r.get("e2e") or {}).get("value"),
+           "roofline": {k: r["roofline"].get(k) for k in ("bound", "kernel", "achieved", "peak",
+                                                            "unit", "frac")},
+           "gpu_launches": r.get("gpu_launches"), "self_check": r.get("self_check")}
+    for k in ("per_size", "executed_tflops", "units_completed_in_run"):
+        if k in r:
+            out[k] = r[k]
+    return out
+
+
+def secondary_workloads(args) -> list:
+    """The other BASELINE configs measured in the same run, summarised beside
+    the headline (short runs: config 2 = configs[1], the batched bit-string
+    workload; config 1; config 3 = 8 of the 64 seeded permutations per size;
+    config 5 = path steps of the first open-qubit batch)."""
+    import torch
+    runs = (("config2", run_gpu, {"steps": 10}),
+            ("config1", run_gpu, {"steps": 10}),
+            ("permute", run_permute, {"steps": 3, "perms": 8}),
+            ("config5", run_paths, {"steps": 10, "e2e_units": 0}))
+    want = [w.strip() for w in str(args.secondary_workloads).split(",") if w.strip()]
+    out = []
+    for name, fn, over in runs:
+        if name not in want or name == args.workload:
+            continue
+        sub = argparse.Namespace(**vars(args))
+        sub.workload, sub.warmup, sub.no_cpu_baseline = name, 3, True
+        for k, v in over.items():
+            setattr(sub, k, v)
+        try:
+            r = fn(sub)
+            if r is not None:
+                out.append(_compact(r))
+        except Exception as exc:  # the headline stands on its own
+            out.append({"workload": name, "error": repr(exc)[:300]})
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    return out
 
 
 def main(argv=None):
@@ -1004,8 +1031,9 @@ def main(argv=None):
                     help="config4 = headline (the largest single-GPU config, tensor-core bound); "
                          "config5; config2 (BASELINE configs[1]); config1; permute = config 3")
     ap.add_argument("--secondary", type=int, default=1,
-                    help="config4/5: also run a short config-2 measurement (reported under "
-                         "'secondary')")
+                    help="config4/5: also run short measurements of the other configs "
+                         "(reported under 'secondary')")
+    ap.add_argument("--secondary-workloads", default="config2,config1,permute,config5")
     ap.add_argument("--e2e-units", type=int, default=1,
                     help="config4/5: whole units (amplitudes / batches) timed through the API")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
@@ -1036,7 +1064,7 @@ def main(argv=None):
             elif args.workload in PATH_WORKLOADS:
                 out = run_paths(args)
                 if args.secondary:
-                    sec = secondary_config2(args)
+                    sec = secondary_workloads(args)
                     if out is not None:
                         out["secondary"] = sec
             else:
