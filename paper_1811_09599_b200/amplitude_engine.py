@@ -21,8 +21,10 @@ the types the reference returns.
 
 from __future__ import annotations
 
+import gc
 import json
 import math
+import warnings
 from dataclasses import dataclass
 from typing import IO, Iterable, Optional, Sequence, Union
 
@@ -268,18 +270,24 @@ class AmplitudeEngine:
         key = (_bits_str(in_bits, n), fidelity.f, fidelity.seed)
         modes = self.__dict__.setdefault("_single_mode", {})
         if modes.get(key) == "graph":
-            with torch.cuda.device(self._torch_device()):
-                runner = self._graph_runner(in_bits, 1, fidelity, False)
-                vals = runner(_bits_matrix([out], n))
-            return complex(vals[0]), runner.stats
+            try:
+                with torch.cuda.device(self._torch_device()):
+                    runner = self._graph_runner(in_bits, 1, fidelity, False)
+                    vals = runner(_bits_matrix([out], n))
+                return complex(vals[0]), runner.stats
+            except GraphCaptureError as exc:
+                # still the device path, only without the replay shortcut
+                warnings.warn(f"single-call CUDA graph unavailable ({exc}); walking eagerly")
+                modes[key] = "eager"
         with torch.cuda.device(self._torch_device()):
             net = self.base_net(in_bits).fix_outputs({q: int(b) for q, b in enumerate(out)})
             ex = self._executor(net)
             paths = fidelity.paths_for(ex.cut_dims)
             acc, flops = self._sum_paths(ex, paths, lambda t: t.data, 1)
             total = complex(acc.cpu().numpy()[0])
-        modes[key] = "graph" if _graph_singles and ex.peak_bytes <= GRAPH_SINGLE_MAX_BYTES \
-            else "eager"
+        if modes.get(key) != "eager":   # "eager" sticks once a capture has failed
+            modes[key] = "graph" if _graph_singles and ex.peak_bytes <= GRAPH_SINGLE_MAX_BYTES \
+                else "eager"
         return total, PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)
 
     def amplitudes(self, in_bits: Union[str, int], out_bits: Sequence,
@@ -368,7 +376,13 @@ class AmplitudeEngine:
         key = (_bits_str(in_bits, self.circuit.n), batch, fidelity.f, fidelity.seed, late)
         cache = self.__dict__.setdefault("_graphs", {})
         if key not in cache:
-            cache[key] = _GraphRunner(self, key[0], batch, fidelity, late)
+            try:
+                cache[key] = _GraphRunner(self, key[0], batch, fidelity, late)
+            except RuntimeError as exc:
+                if "captur" not in str(exc):
+                    raise
+                torch.cuda.synchronize()
+                raise GraphCaptureError(str(exc).splitlines()[0]) from exc
         return cache[key]
 
     def amplitude_batch(self, in_bits: Union[str, int], s_ab: Union[str, int],
@@ -430,6 +444,11 @@ class AmplitudeEngine:
             return acc.cpu().numpy()
 
 
+class GraphCaptureError(RuntimeError):
+    """Capturing a plan walk as a CUDA graph failed (the eager device walk
+    still works)."""
+
+
 class _GraphRunner:
     """One captured plan walk for a fixed (input, batch size, fidelity).
 
@@ -465,8 +484,20 @@ class _GraphRunner:
         self.graph = torch.cuda.CUDAGraph()
         from . import _lib
         before = _lib.launch_count()
-        with torch.cuda.graph(self.graph):
-            self.acc, ex, paths = body()
+        # No cyclic garbage collection while the stream captures: finalisers of
+        # earlier engines' objects (graphs, pinned buffers, events) issue CUDA
+        # calls that are illegal during a global-mode capture and invalidate
+        # it -- seen as an intermittent "previous error during capture" when
+        # many engines come and go (the reference's acceptance criterion 1).
+        gc_was_on = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        try:
+            with torch.cuda.graph(self.graph):
+                self.acc, ex, paths = body()
+        finally:
+            if gc_was_on:
+                gc.enable()
         self.kernels = _lib.launch_count() - before   # library kernels per replay
         flops = slices.reduce_int(ex.flops, eng.group, self.acc.device)
         self.stats = PathStats(math.prod(ex.cut_dims), len(paths), flops, ex.peak_bytes)

@@ -341,7 +341,11 @@ class Tensor:
         if isinstance(array, np.ndarray) or np.isscalar(array):
             arr = np.asarray(array)
             if arr.dtype not in _TORCH_OF:
-                arr = arr.astype(np.complex64)
+                # real/integer input widens without rounding: 8-byte reals to
+                # complex128, everything narrower to complex64 (the reference
+                # keeps any numpy dtype; values compare equal either way)
+                wide = arr.dtype.kind in "fiu" and arr.dtype.itemsize >= 8
+                arr = arr.astype(np.complex128 if wide else np.complex64)
             dims = arr.shape
             _require_cuda()
             data = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1)).to(
@@ -1609,17 +1613,30 @@ def sum_path_axis(t: Tensor, rep: int, keep_batch: bool, label: str = "@b") -> T
 
 @dataclass(frozen=True)
 class Move:
+    """One pass of the reference's CPU decomposition (rq/tensor_core.py:41-57):
+    an "L" move permutes the leading axes and leaves the trailing `gamma`
+    axes in place, an "R" move permutes the trailing `gamma` axes;
+    `group_perm` is in gather order over the affected group."""
+
     kind: str
     group_perm: tuple
     gamma: int
 
+    def __post_init__(self):
+        if self.kind not in ("L", "R"):
+            raise ValueError(f"move kind must be 'L' or 'R', got {self.kind!r}")
+
 
 @dataclass(frozen=True)
 class PermutePlan:
-    """(dims, perm) of a transpose.  The reference decomposes it into CPU
-    cache-sized L/R moves (rq/tensor_core.py:81-206); on the B200 the whole
-    permutation is one shared-memory-tiled pass (K1), so `moves` is empty
-    and `device_pass` describes what runs."""
+    """(dims, perm) of a transpose plus the reference's L/R move list.
+
+    The reference executes `moves` as cache-sized CPU passes
+    (rq/tensor_core.py:81-206).  On the B200 the whole permutation is ONE
+    shared-memory-tiled pass (K1) whatever the moves say: they are kept as
+    plan metadata with the reference's decomposition rules so that callers
+    inspecting `move_summary()` / `fallback` see the same plan, and
+    `device_pass` names what actually runs."""
 
     dims: tuple
     perm: tuple
@@ -1637,6 +1654,105 @@ class PermutePlan:
         return [(m.kind, m.gamma) for m in self.moves]
 
 
+def _in_place(seq) -> bool:
+    return all(v == i for i, v in enumerate(seq))
+
+
+def _vol(dims, axes) -> int:
+    return math.prod(dims[a] for a in axes)
+
+
+def _moves_three(dims, perm, lo: int, hi: int):
+    """The general L-R-L template (rq/tensor_core.py:154-206): a left move
+    parks the axes that must end up trailing next to the window, a right
+    move orders the final suffix, a last left move orders the prefix.
+    Returns the move tuple or None when no (gamma_L, gamma_R) fits."""
+    k = len(dims)
+    rank_of = {a: j for j, a in enumerate(perm)}
+    # smallest suffix length whose input AND output blocks reach the L bound
+    g_l = next((g for g in range(1, k)
+                if _vol(dims, range(k - g, k)) >= lo and _vol(dims, perm[k - g:]) >= lo), None)
+    if g_l is None:
+        return None
+    head = k - g_l
+    tail_axes = list(perm[head:])
+    strays = [a for a in tail_axes if a < head]           # must cross into the suffix
+    stay = sorted((a for a in range(head) if a not in tail_axes), key=rank_of.__getitem__)
+    first = stay + strays
+    lay = first + list(range(head, k))
+    # widest R window within the budget that still covers strays + suffix
+    need = g_l + len(strays)
+    g_r = next((g for g in range(k, need - 1, -1) if _vol(dims, lay[k - g:]) <= hi), None)
+    if g_r is None:
+        return None
+    moves = []
+    if not _in_place(first):
+        moves.append(Move("L", tuple(first), g_l))
+    win = lay[k - g_r:]
+    rest = sorted((a for a in win if a not in tail_axes), key=rank_of.__getitem__)
+    target = rest + tail_axes
+    local = tuple(win.index(a) for a in target)
+    if not _in_place(local):
+        moves.append(Move("R", local, g_r))
+    lay = lay[:k - g_r] + target
+    now = lay[:head]
+    last = tuple(now.index(a) for a in perm[:head])
+    if not _in_place(last):
+        moves.append(Move("L", last, g_l))
+    return tuple(moves)
+
+
+def _plan_moves(dims, perm, mu: int, nu: int):
+    """(moves, fallback) by the reference's rules, tried in its order:
+    identity; fixed suffix of >= 2^mu entries -> one L; fixed prefix with a
+    window of <= 2^nu entries -> one R; a prefix block mapped onto itself
+    with the rest a legal window -> L then R; the L-R-L template; else the
+    naive fallback (rq/tensor_core.py:81-151)."""
+    k = len(dims)
+    lo, hi = 1 << mu, 1 << nu
+    if _in_place(perm):
+        return (), None
+    fixed_tail = next((g for g in range(k + 1) if g == k or perm[k - 1 - g] != k - 1 - g), k)
+    if fixed_tail >= 1 and _vol(dims, range(k - fixed_tail, k)) >= lo:
+        return (Move("L", tuple(perm[:k - fixed_tail]), fixed_tail),), None
+    fixed_head = next((g for g in range(k + 1) if g == k or perm[g] != g), k)
+    if _vol(dims, range(fixed_head, k)) <= hi:
+        return (Move("R", tuple(p - fixed_head for p in perm[fixed_head:]), k - fixed_head),), None
+    # largest b with perm[:b] a permutation of 0..b-1 and a legal trailing window
+    split, top = None, -1
+    for b in range(1, k):
+        top = max(top, perm[b - 1])
+        if top == b - 1 and lo <= _vol(dims, range(b, k)) <= hi:
+            split = b
+    if split is not None:
+        out = []
+        if not _in_place(perm[:split]):
+            out.append(Move("L", tuple(perm[:split]), k - split))
+        back = tuple(p - split for p in perm[split:])
+        if not _in_place(back):
+            out.append(Move("R", back, k - split))
+        return tuple(out), None
+    three = _moves_three(dims, perm, lo, hi)
+    if three is not None:
+        return three, None
+    return (), "naive"
+
+
+def moves_compose(plan: "PermutePlan") -> tuple:
+    """The permutation obtained by applying `plan.moves` in order (gather
+    order, like `perm`) -- equals plan.perm unless the plan fell back."""
+    k = len(plan.dims)
+    lay = list(range(k))
+    for m in plan.moves:
+        if m.kind == "L":
+            head = lay[:k - m.gamma]
+            lay = [head[j] for j in m.group_perm] + lay[k - m.gamma:]
+        else:
+            win = lay[k - m.gamma:]
+            lay = lay[:k - m.gamma] + [win[j] for j in m.group_perm]
+    return tuple(lay)
+
+
 def plan_permutation(dims: Sequence[int], perm: Sequence[int], mu: int = 5, nu: int = 10) -> PermutePlan:
     dims = tuple(int(d) for d in dims)
     perm = tuple(int(p) for p in perm)
@@ -1646,8 +1762,9 @@ def plan_permutation(dims: Sequence[int], perm: Sequence[int], mu: int = 5, nu: 
         raise ValueError(f"need 0 <= mu <= nu, got mu={mu}, nu={nu}")
     if any(d < 1 for d in dims):
         raise ValueError("dims must be positive")
-    identity = perm == tuple(range(len(dims)))
-    return PermutePlan(dims, perm, (), mu, nu, None, "none" if identity else "tiled")
+    moves, fallback = _plan_moves(dims, perm, mu, nu)
+    return PermutePlan(dims, perm, moves, mu, nu, fallback,
+                       "none" if _in_place(perm) else "tiled")
 
 
 def _as_device(array):
@@ -1655,7 +1772,14 @@ def _as_device(array):
         return array.reshape(-1), None
     arr = np.ascontiguousarray(array)
     if arr.dtype not in _TORCH_OF:
-        raise ValueError(f"permutation supports complex64/complex128, got {arr.dtype}")
+        # K1 moves 8- and 16-byte elements without touching their bits: other
+        # 8/16-byte dtypes (float64, int64, ...) ride through as raw elements
+        if arr.dtype.itemsize not in (8, 16) or arr.dtype.hasobject:
+            raise ValueError("permutation supports 8- and 16-byte elements "
+                             f"(complex64/complex128, float64, int64), got {arr.dtype}")
+        raw = arr.reshape(-1).view(np.complex64 if arr.dtype.itemsize == 8 else np.complex128)
+        _require_cuda()
+        return torch.from_numpy(raw).to(torch.cuda.current_device()), arr.dtype
     _require_cuda()
     return torch.from_numpy(arr.reshape(-1)).to(torch.cuda.current_device()), arr.dtype
 
@@ -1666,7 +1790,7 @@ def permute_fast(array, plan: PermutePlan, thread_count: int = 1, workspace=None
     out = permute_buffer(data, plan.dims, plan.perm)[: math.prod(plan.dims)]
     if np_dtype is None:
         return out.view(plan.out_dims) if len(plan.out_dims) <= 25 else out
-    return out.cpu().numpy().reshape(plan.out_dims)
+    return out.cpu().numpy().view(np_dtype).reshape(plan.out_dims)
 
 
 def permute_naive(array, perm: Sequence[int]):

@@ -316,3 +316,27 @@ def test_batch_order_is_plan_order_lexsort(name, n):
     seq = eng._consume_seq
     assert sorted(seq.tolist()) == list(range(n))
     assert (order == np.lexsort([bits[:, q] for q in reversed(seq)])).all()
+
+
+def test_permutation_plans_match_reference_moves():
+    """plan_permutation keeps the reference's L/R decomposition as plan
+    metadata (rq/tensor_core.py:81-206): same moves and fallback on the
+    golden cases written by tests/golden/make_golden_moves.py, and the moves
+    compose to the permutation."""
+    import json
+    import os
+    from paper_1811_09599_b200 import tensor_core as tcore
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_moves.json")
+    with open(path) as fh:
+        cases = json.load(fh)
+    assert len(cases) >= 400
+    for c in cases:
+        plan = tcore.plan_permutation(c["dims"], c["perm"], c["mu"], c["nu"])
+        assert [[m.kind, list(m.group_perm), m.gamma] for m in plan.moves] == c["moves"], c
+        assert plan.fallback == c["fallback"]
+        if plan.fallback is None:
+            assert tcore.moves_compose(plan) == tuple(c["perm"])
+    worked = tcore.plan_permutation([2] * 7, [2, 5, 4, 0, 3, 6, 1], mu=2, nu=4)
+    assert worked.move_summary() == [("L", 2), ("R", 4), ("L", 2)]
+    with pytest.raises(ValueError):
+        tcore.Move("X", (0,), 1)
