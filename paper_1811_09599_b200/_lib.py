@@ -274,3 +274,8 @@ def dot_c64(x, y, out, batch: int, n: int, stride_x: Optional[int] = None,
     check(load().qf_dot_c64(int(batch), int(n), ctypes.c_void_p(x.data_ptr()), sx,
                             ctypes.c_void_p(y.data_ptr()), sy, ctypes.c_void_p(out.data_ptr()),
                             _current_stream()), "dot_c64")
+
+
+def last_kernel() -> str:
+    """Name of the kernel family the library launched last on this thread."""
+    return load().qf_last_kernel().decode()

@@ -1226,7 +1226,7 @@ __global__ void __launch_bounds__((NW + NE + NPW) * 32 + 32, 1)
 }
 
 // 3-D float tensor map (dims innermost first, strides in bytes) for TMA boxes
-static bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2,
+bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2,
                       uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1, bool swz64) {
   const cuuint64_t dims[3] = {d0, d1, d2};
   const cuuint64_t strides[2] = {s1, s2};
@@ -1250,8 +1250,8 @@ static bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1,
 }
 
 // 5-D float tensor map of an A view (dims innermost first, byte strides)
-static bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5],
-                       const uint64_t (&strides)[4], const uint32_t (&box)[5], bool swz64 = true) {
+bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5],
+                const uint64_t (&strides)[4], const uint32_t (&box)[5], bool swz64) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1405,6 +1405,11 @@ static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
 // converter fetch (no TMA; also the fallback when TMA cannot describe the
 // operands).
 static int launch_long(const GemmArgs &g, cudaStream_t s) {
+  // N >= 128 and K >= 512: the wide (128 x 128) Gauss kernel with its master in
+  // registers (qf_gemm_tcw.cu).  Pins: 40/41/42 = wide with CK 64/128/32,
+  // 32 = the 64-column Gauss kernel (CK 64).
+  if ((g_tc3_variant == 0 || (g_tc3_variant >= 40 && g_tc3_variant <= 42)) && tc3w_ok(g))
+    return gemm_tc3w(g, s, g_tc3_variant == 41 ? 128 : g_tc3_variant == 42 ? 32 : 64);
   if (g_tc3_variant != 13 && tc::tma_ok(g)) {
     if (g_tc3_variant == 19) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
     if (g_tc3_variant == 26) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true>(g, s);

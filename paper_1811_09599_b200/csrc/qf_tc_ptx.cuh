@@ -2,7 +2,7 @@
 // mbarriers, UMMA shared-memory descriptors, tensor-memory loads/stores,
 // tcgen05.mma issue/commit, the TF32 hi/lo split and the staged epilogue
 // store.  Shared by qf_gemm_tc.cu (3xTF32 real-block form) and
-// qf_gemm_g3.cu (3xTF32 Gauss form).
+// qf_gemm_tcw.cu (the 128 x 128 Gauss-form long-K kernel).
 #pragma once
 
 #include <cuda.h>
@@ -308,5 +308,18 @@ __device__ __forceinline__ void stage_store_chunk(uint8_t *stg, const uint32_t (
   __syncwarp();
 }
 
+// host side (qf_gemm_tc.cu): TMA tensor maps over float data (dims innermost
+// first, byte strides) and the operand test for them
+bool make_tmap(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+               uint64_t s2, uint32_t b0, uint32_t b1, bool swz64);
+bool make_tmap5(CUtensorMap *m, const void *ptr, const uint64_t (&dims)[5],
+                const uint64_t (&strides)[4], const uint32_t (&box)[5], bool swz64 = true);
+bool tma_ok(const GemmArgs &g);
+
 }  // namespace tc
+
+// qf_gemm_tcw.cu: the wide (128 x 128) Gauss-form long-K kernel
+bool tc3w_ok(const GemmArgs &g);
+int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck);
+
 }  // namespace qf

@@ -806,3 +806,47 @@ def test_permute_plan_first_built_in_capture_is_refused():
     torch.cuda.synchronize()
     want = x.cpu().numpy().reshape(dims).transpose(perm).reshape(-1)
     assert np.array_equal(y.cpu().numpy(), want)
+
+
+# wide (128 x 128 tile) Gauss long-K kernel, qf_gemm_tcw.cu: full and ragged
+# tiles in M, N and K, several tiles per CTA, entries (batch), all operand
+# layouts, 1/2/many promotion chunks per tile
+WIDE_SHAPES = [(1, 256, 256, 1024), (1, 128, 128, 512), (2, 384, 640, 520), (1, 1000, 1152, 778),
+               (3, 2048, 1024, 1024), (1, 19000, 128, 512), (1, 128, 2048, 4100)]
+
+
+@pytest.mark.parametrize("shape", WIDE_SHAPES)
+@pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
+@pytest.mark.parametrize("variant", [40, 41, 42], ids=["ck64", "ck128", "ck32"])
+def test_tcgen05_wide_gauss_long_k(shape, ops, variant):
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(variant)
+    try:
+        err = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3)
+        assert _lib.last_kernel() == "cgemm_tc3w"
+    finally:
+        lib.qf_tc3_set_variant(prev)
+    assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("K", [4096, 32768])
+@pytest.mark.parametrize("variant", [40, 41], ids=["ck64", "ck128"])
+def test_tcgen05_wide_accuracy_at_long_k(K, variant):
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(variant)
+    try:
+        err = _gemm(1, 256, 256, K, 0, 0, np.complex64, mode=_lib.GEMM_TC3)
+    finally:
+        lib.qf_tc3_set_variant(prev)
+    assert err < (5e-6 if variant == 40 else 1e-5), err
+
+
+@pytest.mark.parametrize("ab", [(0.5 - 1j, 0.0), (1.0, 0.5 + 0.25j)])
+def test_tcgen05_wide_alpha_beta(ab):
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(40)
+    try:
+        err = _gemm(2, 300, 384, 1024, 0, 1, np.complex64, _lib.GEMM_TC3, ab[0], ab[1])
+    finally:
+        lib.qf_tc3_set_variant(prev)
+    assert err < 1e-5, err
