@@ -1406,10 +1406,14 @@ static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
 // operands).
 static int launch_long(const GemmArgs &g, cudaStream_t s) {
   // N >= 128 and K >= 512: the wide (128 x 128) Gauss kernel with its master in
-  // registers (qf_gemm_tcw.cu).  Pins: 40/41/42 = wide with CK 64/128/32,
-  // 32 = the 64-column Gauss kernel (CK 64).
-  if ((g_tc3_variant == 0 || (g_tc3_variant >= 40 && g_tc3_variant <= 42)) && tc3w_ok(g))
-    return gemm_tc3w(g, s, g_tc3_variant == 41 ? 128 : g_tc3_variant == 42 ? 32 : 64);
+  // registers (qf_gemm_tcw.cu).  Pins: 40/41/42 = wide single-CTA with CK
+  // 64/128/32, 43/44/45 = CTA pairs (cta_group::2) with CK 64/128/32, 32 = the
+  // 64-column Gauss kernel (CK 64).
+  if ((g_tc3_variant == 0 || (g_tc3_variant >= 40 && g_tc3_variant <= 45)) && tc3w_ok(g)) {
+    const int v = g_tc3_variant;
+    const int ck = (v == 41 || v == 44) ? 128 : (v == 42 || v == 45) ? 32 : 64;
+    return gemm_tc3w(g, s, ck, v == 0 ? -1 : v >= 43 ? 1 : 0);   // auto: pairs when M fills them
+  }
   if (g_tc3_variant != 13 && tc::tma_ok(g)) {
     if (g_tc3_variant == 19) return tc::launch_short<4, 8, 8, 4, 64, 4, 1, true>(g, s);
     if (g_tc3_variant == 26) return tc::launch_short<4, 8, 8, 4, 64, 16, 1, true>(g, s);
@@ -1505,8 +1509,10 @@ int gemm_tc3(const GemmArgs &g_in, cudaStream_t s) {
     return tc::launch_short<4, 8, 8, 4, 64, 4>(g, s);
   }
   // short K (<= 256): no promotion needed (error <= 3.6e-6); tile-level
-  // double-buffered TMEM accumulators with a deferred epilogue
-  if (g.K <= 256) return launch_short_auto(g, s);
+  // double-buffered TMEM accumulators with a deferred epilogue (unless the
+  // wide kernel's K threshold, QF_TC3W_MINK, has been lowered to take them)
+  if (g.K <= 256 && !((g_tc3_variant == 0 || g_tc3_variant >= 40) && tc3w_ok(g)))
+    return launch_short_auto(g, s);
   return launch_long(g, s);
 }
 

@@ -3,7 +3,7 @@
 // in registers.
 //
 // Replaces the OpenBLAS cgemm behind `@` at rq/tensor_core.py:417 for the
-// big compute-bound contractions (configs 4 and 5: K >= 512, N >= 128).
+// big compute-bound contractions (configs 4 and 5: K >= 256, N >= 128).
 //
 // Why a second long-K flavour.  The 128 x 64 Gauss kernel (qf_gemm_tc.cu,
 // "cgemm_tc3g") is bound by the 1 kW power cap and by a per-stage handshake
@@ -37,6 +37,7 @@
 // B_j(lo) + A_j(lo) B_j(hi), j = 1..3.  Re = T1 - T2, Im = T3 - T1 - T2 at
 // promotion.
 #include <algorithm>
+#include <cstdlib>
 
 #include "qf_tc_ptx.cuh"
 
@@ -48,7 +49,8 @@ using namespace tc;
 constexpr int BN = 128;          // complex output columns per tile
 constexpr int STAGES = 2;        // converted stages (A planes in TMEM + B' planes in smem)
 constexpr int RAW = 8;           // raw TMA ring depth (k-blocks in flight)
-constexpr int NCONV = 6;         // converting warps: 4 (A rows + B columns 0-63) + 2 (B columns 64-127)
+// converting warps: 4 (A rows + B columns 0-63) + 2 (B columns 64-127); in a CTA
+// pair every CTA converts only its 64 columns of B, on the 4 A warps
 constexpr int NPROMO = 8;        // promotion / epilogue warps
 constexpr int THREADS_W = 512;   // warps 0-3 | 4 TMA, 5 MMA, 6-7 | 8-15
 constexpr int REGS_A = 112;      // setmaxnreg targets (multiples of 8; 128 at launch)
@@ -56,12 +58,15 @@ constexpr int REGS_MISC = 72;
 constexpr int REGS_PROMO = 160;
 static_assert(128 * REGS_A + 128 * REGS_MISC + 256 * REGS_PROMO <= 65536, "register file");
 
+template <bool PAIR>
 struct Lw {
-  static constexpr int B_BLOCK = BN * 32;            // one plane block: 128 n x 8 tf32, K-major
+  static constexpr int BNL = PAIR ? BN / 2 : BN;     // B columns converted / held by this CTA
+  static constexpr int NCONV = PAIR ? 4 : 6;         // converting warps per CTA
+  static constexpr int B_BLOCK = BNL * 32;           // one plane block: BNL n x 8 tf32, K-major
   static constexpr int B_PLANE = 3 * B_BLOCK;        // [Br | Bi | Br+Bi]
   static constexpr int STAGE = 2 * B_PLANE;          // hi plane, lo plane
   static constexpr int RAWA_SLOT = BM * 64;          // 128 rows x 8 complex
-  static constexpr int RAWB_SLOT = BN * 64;
+  static constexpr int RAWB_SLOT = BNL * 64;
   static constexpr int RAWA_OFF = STAGES * STAGE;
   static constexpr int RAWB_OFF = RAWA_OFF + RAW * RAWA_SLOT;
   static constexpr int EPI_PITCH = 16 * 8 + 16;      // 16 complex columns per staging pass
@@ -81,6 +86,46 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                : "r"(taddr));
+}
+
+// CTA pair (cta_group::2): a cluster of two CTAs computes a 256 x 128 tile with
+// M = 256 MMAs issued by the leader (rank 0).  Each CTA keeps its 128 A rows in
+// its own TMEM and its 64 columns of the B' planes in its own shared memory,
+// which halves every SM's B conversion and B bytes from L2.  Converters and
+// promotion warps of both CTAs arrive on the leader's barriers; MMA completions
+// are multicast to both CTAs.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+// arrive on a barrier of the pair's leader (a cluster address; rank 0 maps to itself)
+__device__ __forceinline__ void arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mma_ts2(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit2(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
 }
 
 template <int N>
@@ -123,12 +168,13 @@ __device__ __forceinline__ void cur_set(Cur &c, uint32_t w, uint32_t tiles_m, ui
 // half-warp), so raw reads hit disjoint bank halves and the 8-byte B' stores
 // of 16 lanes fill one core-matrix row block.  A converters run tv = tid,
 // tid + 128 of half 0; B converters tv = u, u + 64, u + 128, u + 192 of half 1.
-template <bool A_ROLE>
+template <bool A_ROLE, bool PAIR>
 __device__ __forceinline__ void convert_loop(const GemmArgs &g, uint8_t *smem, uint64_t *bars,
-                                             uint64_t *full, uint64_t *rawfull, uint64_t *rawfree,
-                                             uint32_t tmem, uint32_t w0, uint32_t wstep,
-                                             uint32_t total, uint32_t nk) {
-  using L = Lw;
+                                             uint32_t full_leader, uint64_t *rawfull,
+                                             uint64_t *rawfree, uint32_t tmem, uint32_t w0,
+                                             uint32_t wstep, uint32_t total, uint32_t nk) {
+  using L = Lw<PAIR>;
+  constexpr int BNL = L::BNL;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int u = A_ROLE ? tid : tid - 192;        // index among this role's threads
   constexpr int NB = A_ROLE ? 2 : 4;              // B k pairs per thread
@@ -148,7 +194,7 @@ __device__ __forceinline__ void convert_loop(const GemmArgs &g, uint8_t *smem, u
     boff[i] = core_off(n, b_chunk) + (uint32_t)(b_kp * 8);
     // opB N: [8 k][128 n] dense (two 8-byte reads, rows b_k and b_k + 1);
     // opB T: [128 n][64 B] with the 64-byte swizzle (one 16-byte read)
-    b_src[i] = g.opB == QF_OP_N ? b_k * (BN * 8) + n * 8
+    b_src[i] = g.opB == QF_OP_N ? b_k * (BNL * 8) + n * 8
                                 : n * 64 + (((b_k >> 1) ^ ((n >> 1) & 3)) << 4);
   }
   uint32_t q = 0;
@@ -178,7 +224,7 @@ __device__ __forceinline__ void convert_loop(const GemmArgs &g, uint8_t *smem, u
       for (int i = 0; i < NB; ++i) {
         if (g.opB == QF_OP_N) {
           const float2 y0 = *reinterpret_cast<const float2 *>(rB + b_src[i]);
-          const float2 y1 = *reinterpret_cast<const float2 *>(rB + b_src[i] + BN * 8);
+          const float2 y1 = *reinterpret_cast<const float2 *>(rB + b_src[i] + BNL * 8);
           bv[i] = make_float4(y0.x, y0.y, y1.x, y1.y);
         } else {
           bv[i] = *reinterpret_cast<const float4 *>(rB + b_src[i]);
@@ -236,18 +282,21 @@ __device__ __forceinline__ void convert_loop(const GemmArgs &g, uint8_t *smem, u
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+      // (pair: a plain remote arrive, as CUTLASS's 2-SM pipelines do -- what it
+      // publishes is read by the tensor core through the async proxy, fenced above)
+      if (lane == 0) arrive_cluster(full_leader + s * 8u);
     }
   }
 }
 
-template <int CK>
+template <int CK, bool PAIR>
 __global__ void __launch_bounds__(THREADS_W, 1)
     cgemm_tc3w_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB) {
-  using L = Lw;
+  using L = Lw<PAIR>;
+  constexpr int NCONV = L::NCONV;
+  constexpr uint32_t NCTA = PAIR ? 2 : 1;
   static_assert((CK & (CK - 1)) == 0 && CK >= 8, "promotion chunk: a power of two");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR_OFF);  // [STAGES] stage free
@@ -263,10 +312,10 @@ __global__ void __launch_bounds__(THREADS_W, 1)
   if (tid == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&bars[i], 1);
-      mbar_init(&full[i], NCONV);
+      mbar_init(&full[i], NCONV * NCTA);      // (leader's: both CTAs' converters)
     }
     mbar_init(pbar, 1);
-    mbar_init(accfree, NPROMO);
+    mbar_init(accfree, NPROMO * NCTA);        // (leader's: both CTAs' promotion warps)
     for (int i = 0; i < RAW; ++i) {
       mbar_init(&rawfull[i], 1);
       mbar_init(&rawfree[i], NCONV);
@@ -274,16 +323,29 @@ __global__ void __launch_bounds__(THREADS_W, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(L::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(L::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(L::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();   // barrier inits + TMEM allocation visible pair-wide
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t w0 = blockIdx.x, wstep = gridDim.x;
+  // pair: w counts 256 x 128 pair tiles, both CTAs of a cluster walk the same
+  // sequence and CTA `crank` owns rows [128 crank, 128 crank + 128) of each
+  const uint32_t crank = PAIR ? cluster_rank() : 0u;
+  const uint32_t w0 = PAIR ? blockIdx.x >> 1 : blockIdx.x, wstep = PAIR ? gridDim.x >> 1 : gridDim.x;
+  const uint32_t full_leader = PAIR ? map_to_rank(smem_u32(full), 0) : smem_u32(full);
+  const uint32_t accfree_leader = PAIR ? map_to_rank(smem_u32(accfree), 0) : smem_u32(accfree);
   const uint32_t nk = ((uint32_t)g.K + KB - 1) / KB;
   const uint32_t nchunks = (nk + CK - 1) / CK;
 
@@ -317,9 +379,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
           if (piece == 15) {   // the partial is in registers: hand it back to the tensor pipe
             tc_fence_before();
             __syncwarp();
-            if (lane == 0)
-              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(accfree))
-                           : "memory");
+            if (lane == 0) arrive_cluster(accfree_leader);
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -331,7 +391,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
         }
       }
       // ---- epilogue out of the master registers, 16 columns per pass
-      const int64_t m0 = (int64_t)ec.mt * BM + lg * 32;
+      const int64_t m0 = (int64_t)(ec.mt * NCTA + crank) * BM + lg * 32;
       const int64_t n0 = (int64_t)ec.nt * BN + half * 64;
       float2 *cw = Cb + (int64_t)ec.bidx * g.sC + m0 * g.ldc + n0;
       const int64_t ntile = g.N - n0;   // columns left from n0 (may be <= 0 on a ragged edge)
@@ -352,15 +412,18 @@ __global__ void __launch_bounds__(THREADS_W, 1)
   } else if (warp >= 4) {
     reg_dec<REGS_MISC>();   // warps 4-7 form one warpgroup: one setmaxnreg for all its roles
     if (warp >= 6) {
-      convert_loop<false>(g, smem, bars, full, rawfull, rawfree, tmem, w0, wstep, total, nk);
+      if constexpr (!PAIR)
+        convert_loop<false, false>(g, smem, bars, full_leader, rawfull, rawfree, tmem, w0, wstep,
+                                   total, nk);
     } else if (warp == 5) {
+      if (crank == 0) {
       // ===== MMA issuer: the whole warp walks the stage sequence, one elected
       // lane issues.  B' descriptors = stage-0 descriptor + constant (the
       // address field is the low 14 bits, in 16-byte units).
       const uint64_t desc0 = smem_desc(smem_u32(smem));
       constexpr uint32_t ST16 = (uint32_t)L::STAGE >> 4, BP16 = (uint32_t)L::B_PLANE >> 4,
                          BB16 = (uint32_t)L::B_BLOCK >> 4;
-      constexpr uint32_t IDESC = idesc_tf32(BM, BN);
+      constexpr uint32_t IDESC = idesc_tf32(PAIR ? 2 * BM : BM, BN);
       uint32_t q = 0, chunkc = 0;
       for (uint32_t w = w0; w < total; w += wstep) {
         for (uint32_t kb = 0; kb < nk; ++kb, ++q) {
@@ -379,20 +442,32 @@ __global__ void __launch_bounds__(THREADS_W, 1)
           if (elect_one()) {
             // A planes: Ar hi/lo (+0, +8), Ai hi/lo (+16, +24), Ar+Ai hi/lo (+32, +40);
             // B' blocks 0/1/2 = Br, Bi, Br+Bi
-  #pragma unroll
+#pragma unroll
             for (int j = 0; j < 3; ++j) {
               const uint32_t dj = tmem + (uint32_t)(j * BN);
-              mma_ts(dj, a + 16 * j, bh + j * BB16, IDESC, acc0);
-              mma_ts(dj, a + 16 * j, bl + j * BB16, IDESC, 1u);
-              mma_ts(dj, a + 16 * j + 8, bh + j * BB16, IDESC, 1u);
+              if constexpr (PAIR) {
+                mma_ts2(dj, a + 16 * j, bh + j * BB16, IDESC, acc0);
+                mma_ts2(dj, a + 16 * j, bl + j * BB16, IDESC, 1u);
+                mma_ts2(dj, a + 16 * j + 8, bh + j * BB16, IDESC, 1u);
+              } else {
+                mma_ts(dj, a + 16 * j, bh + j * BB16, IDESC, acc0);
+                mma_ts(dj, a + 16 * j, bl + j * BB16, IDESC, 1u);
+                mma_ts(dj, a + 16 * j + 8, bh + j * BB16, IDESC, 1u);
+              }
             }
-            mma_commit(&bars[s]);
-            if (chunk_end) mma_commit(pbar);
+            if constexpr (PAIR) {
+              mma_commit2(&bars[s]);
+              if (chunk_end) mma_commit2(pbar);
+            } else {
+              mma_commit(&bars[s]);
+              if (chunk_end) mma_commit(pbar);
+            }
           }
           if (chunk_end) ++chunkc;
           __syncwarp();
         }
       }
+      }   // leader
     } else {
       // ===== TMA producer (one elected lane): per k-block one box of A and one
       // of B into the raw ring; the slot's mbarrier completes on their bytes
@@ -404,7 +479,8 @@ __global__ void __launch_bounds__(THREADS_W, 1)
         uint32_t f = 0;
         for (uint32_t w = w0; w < total; w += wstep) {
           cur_set(pc, w, tiles_m, tiles_n);
-          const int32_t m0 = (int32_t)(pc.mt * BM), n0 = (int32_t)(pc.nt * BN), b = (int32_t)pc.bidx;
+          const int32_t m0 = (int32_t)((pc.mt * NCTA + crank) * BM), b = (int32_t)pc.bidx;
+          const int32_t n0 = (int32_t)(pc.nt * BN + crank * L::BNL);   // pair: this CTA's B columns
           const int32_t bslice = g.b_boff ? (int32_t)(__ldg(g.b_boff + pc.bidx) / (g.K * g.N)) : b;
           const int32_t aslice = g.a_boff ? (int32_t)(__ldg(g.a_boff + pc.bidx) / g.sA) : b;
           // A view: row coordinates of this tile, k-block -> (ki, ko) counters
@@ -456,19 +532,27 @@ __global__ void __launch_bounds__(THREADS_W, 1)
     }
   } else {
     reg_dec<REGS_A>();
-    convert_loop<true>(g, smem, bars, full, rawfull, rawfree, tmem, w0, wstep, total, nk);
+    convert_loop<true, PAIR>(g, smem, bars, full_leader, rawfull, rawfree, tmem, w0, wstep, total,
+                             nk);
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(L::TMEM_COLS));
+  if constexpr (PAIR) {
+    cluster_sync_all();   // the leader's MMAs read this CTA's smem / TMEM until here
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(L::TMEM_COLS));
+  } else {
+    __syncthreads();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(L::TMEM_COLS));
+  }
 }
 
-template <int CK>
+template <int CK, bool PAIR>
 static int launch_wide(const GemmArgs &g, cudaStream_t s) {
-  using L = Lw;
-  auto kern = cgemm_tc3w_kernel<CK>;
+  using L = Lw<PAIR>;
+  auto kern = cgemm_tc3w_kernel<CK, PAIR>;
   CUtensorMap tmA{}, tmB{};
   const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
   const uint64_t na = g.a_boff ? (uint64_t)g.a_nslice : nb;   // A entries addressable
@@ -490,8 +574,8 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
   const uint64_t nbs = g.b_boff ? (uint64_t)g.b_nslice : nb;
   const int64_t sbs = g.b_boff ? g.K * g.N : std::max<int64_t>(g.sB, 1);
   const bool okB = g.opB == QF_OP_N
-                       ? make_tmap(&tmB, g.B, 2 * g.N, g.K, nbs, g.ldb * 8, sbs * 8, 2 * BN, 8, false)
-                       : make_tmap(&tmB, g.B, 2 * g.K, g.N, nbs, g.ldb * 8, sbs * 8, 16, BN, true);
+                       ? make_tmap(&tmB, g.B, 2 * g.N, g.K, nbs, g.ldb * 8, sbs * 8, 2 * L::BNL, 8, false)
+                       : make_tmap(&tmB, g.B, 2 * g.K, g.N, nbs, g.ldb * 8, sbs * 8, 16, L::BNL, true);
   if (!okA || !okB) {
     set_error("tc3w: cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld)", (long long)g.M,
               (long long)g.N, (long long)g.K);
@@ -506,13 +590,37 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
     }
     attr = true;
   }
-  const int64_t tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + BM - 1) / BM;
+  // pair: tiles are 256 x 128, one per cluster of two CTAs
+  constexpr int64_t TM = PAIR ? 2 * BM : BM;
+  const int64_t tiles_n = (g.N + BN - 1) / BN, tiles_m = (g.M + TM - 1) / TM;
   const int64_t total = tiles_n * tiles_m * g.batch;
   if (total >= (int64_t)1 << 31) {
     set_error("tc3w: %lld tiles exceed the 32-bit tile index", (long long)total);
     return QF_ERR_INVALID;
   }
-  const int64_t grid = std::min<int64_t>(total, (int64_t)sm_count());
+  const int64_t units = PAIR ? sm_count() / 2 : sm_count();
+  const int64_t grid = std::min<int64_t>(total, units) * (PAIR ? 2 : 1);
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(THREADS_W);
+    cfg.dynamicSmemBytes = L::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, g, (uint32_t)tiles_m, (uint32_t)tiles_n,
+                                       (uint32_t)total, tmA, tmB);
+    if (e != cudaSuccess) {
+      set_error("tc3w: pair launch failed: %s", cudaGetErrorString(e));
+      return QF_ERR_CUDA;
+    }
+    return check_launch("cgemm_tc3w");
+  }
   kern<<<(unsigned)grid, THREADS_W, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
                                                   (uint32_t)total, tmA, tmB);
   return check_launch("cgemm_tc3w");
@@ -526,15 +634,35 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
 bool tc3w_ok(const GemmArgs &g) {
   if (g.a_roff || g.v_t || g.c_trans || g.c_nblk) return false;
   if (!tc::tma_ok(g)) return false;
-  if (g.K < 512 || g.M < 128) return false;
+  // K >= 256 (one promotion chunk of 32 k-blocks per tile and up): measured
+  // faster than the 64-column kernels from there on (scripts/c5_wide.py:
+  // 1048576 x 256 x 256 185 -> 287 TFLOP/s); QF_TC3W_MINK moves the threshold
+  static const int64_t min_k = [] {
+    const char *e = getenv("QF_TC3W_MINK");
+    return e ? (int64_t)atoll(e) : (int64_t)256;
+  }();
+  if (g.K < min_k || g.M < 128) return false;
   if (g.N < 128 || (g.N % 128 != 0 && g.N < 1024)) return false;
   return true;
 }
 
-int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck) {
-  if (ck == 128) return tcw::launch_wide<128>(g, s);
-  if (ck == 32) return tcw::launch_wide<32>(g, s);
-  return tcw::launch_wide<64>(g, s);
+// ck: promotion chunk in k-blocks (32 / 64 / 128); pair: 0 = single CTAs,
+// 1 = CTA pairs (cta_group::2), -1 = pairs when the shape fills 256-row tiles
+bool tc3w_pair_ok(const GemmArgs &g) {
+  // a pair's second CTA idles on a ragged last row tile: want many 256-row tiles
+  return g.M >= 1024 && (g.M % 256 == 0 || g.M >= 8192);
+}
+
+int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck, int pair) {
+  const bool use_pair = pair > 0 || (pair < 0 && tc3w_pair_ok(g));
+  if (use_pair) {
+    if (ck == 128) return tcw::launch_wide<128, true>(g, s);
+    if (ck == 32) return tcw::launch_wide<32, true>(g, s);
+    return tcw::launch_wide<64, true>(g, s);
+  }
+  if (ck == 128) return tcw::launch_wide<128, false>(g, s);
+  if (ck == 32) return tcw::launch_wide<32, false>(g, s);
+  return tcw::launch_wide<64, false>(g, s);
 }
 
 }  // namespace qf

@@ -320,6 +320,7 @@ bool tma_ok(const GemmArgs &g);
 
 // qf_gemm_tcw.cu: the wide (128 x 128) Gauss-form long-K kernel
 bool tc3w_ok(const GemmArgs &g);
-int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck);
+bool tc3w_pair_ok(const GemmArgs &g);
+int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck, int pair);
 
 }  // namespace qf

@@ -77,10 +77,10 @@ def set_gemm_mode(mode: str) -> str:
 def tc3_real_macs_per_complex_mac(kernel: str = "cgemm_tc3k") -> int:
     """Real TF32 MMA multiply-adds a tensor-core kernel issues per complex
     multiply-add: the real-block form (`cgemm_tc3k`) 4 real products x 3
-    (hi*hi + hi*lo + lo*hi) = 12, the Gauss form (`cgemm_tc3g`) 3 x 3 = 9.
-    The 3xTF32 ceiling in algorithmic 8-flop complex MACs is then
-    TF32_peak * 8 / (2 * that)."""
-    return 9 if kernel == "cgemm_tc3g" else 12
+    (hi*hi + hi*lo + lo*hi) = 12, the Gauss form (`cgemm_tc3g`, and the
+    128-column `cgemm_tc3w`) 3 x 3 = 9.  The 3xTF32 ceiling in algorithmic
+    8-flop complex MACs is then TF32_peak * 8 / (2 * that)."""
+    return 9 if kernel in ("cgemm_tc3g", "cgemm_tc3w") else 12
 
 
 def get_gemm_mode() -> str:

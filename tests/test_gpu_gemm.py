@@ -817,7 +817,8 @@ WIDE_SHAPES = [(1, 256, 256, 1024), (1, 128, 128, 512), (2, 384, 640, 520), (1, 
 
 @pytest.mark.parametrize("shape", WIDE_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-@pytest.mark.parametrize("variant", [40, 41, 42], ids=["ck64", "ck128", "ck32"])
+@pytest.mark.parametrize("variant", [40, 41, 42, 43, 44],
+                         ids=["ck64", "ck128", "ck32", "pair-ck64", "pair-ck128"])
 def test_tcgen05_wide_gauss_long_k(shape, ops, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
@@ -830,7 +831,7 @@ def test_tcgen05_wide_gauss_long_k(shape, ops, variant):
 
 
 @pytest.mark.parametrize("K", [4096, 32768])
-@pytest.mark.parametrize("variant", [40, 41], ids=["ck64", "ck128"])
+@pytest.mark.parametrize("variant", [40, 41, 43], ids=["ck64", "ck128", "pair-ck64"])
 def test_tcgen05_wide_accuracy_at_long_k(K, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
@@ -838,13 +839,14 @@ def test_tcgen05_wide_accuracy_at_long_k(K, variant):
         err = _gemm(1, 256, 256, K, 0, 0, np.complex64, mode=_lib.GEMM_TC3)
     finally:
         lib.qf_tc3_set_variant(prev)
-    assert err < (5e-6 if variant == 40 else 1e-5), err
+    assert err < (1e-5 if variant == 41 else 5e-6), err
 
 
 @pytest.mark.parametrize("ab", [(0.5 - 1j, 0.0), (1.0, 0.5 + 0.25j)])
-def test_tcgen05_wide_alpha_beta(ab):
+@pytest.mark.parametrize("variant", [40, 43], ids=["single", "pair"])
+def test_tcgen05_wide_alpha_beta(ab, variant):
     lib = _lib.load()
-    prev = lib.qf_tc3_set_variant(40)
+    prev = lib.qf_tc3_set_variant(variant)
     try:
         err = _gemm(2, 300, 384, 1024, 0, 1, np.complex64, _lib.GEMM_TC3, ab[0], ab[1])
     finally:
