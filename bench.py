@@ -236,11 +236,26 @@ def measured_traffic(workload: str, kernel: str, algorithmic_per_step: float, la
     if rec is None:
         return None
     dram = rec["dram_read"] + rec["dram_write"]
+    if launches <= 0:   # path workloads: the capture's own launch count (one path)
+        launches = rec["launches"]
+        algorithmic_per_step *= launches
     return {"dram_bytes_per_step": round(dram), "algorithmic_bytes_per_step": round(algorithmic_per_step),
             "dram_bytes_per_launch": round(dram / max(launches, 1)),
             "ratio": round(dram / max(algorithmic_per_step, 1), 3),
             "source": f"profiles/traffic_{workload}.json (ncu dram__bytes_read.sum + "
                       f"dram__bytes_write.sum over {rec['launches']} ncu launches of one step)"}
+
+
+def tensor_pipe_ncu(kernel: str):
+    """sm__pipe_tensor_cycles_active of `kernel` from the committed ncu
+    --set full capture (profiles/tensor_pipe.json: a separate, unthrottled
+    single-launch run -- context for the live `tensor_pipe_util`, not a
+    measurement of this run)."""
+    path = os.path.join(ROOT, "profiles", "tensor_pipe.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh).get(kernel)
 
 
 def peaks() -> dict:
@@ -636,6 +651,29 @@ def tensor_peak_of(pk: dict, sustained: bool, kernel: str = "cgemm_tc3k") -> tup
             f"/ 2 = TF32 {tf32:.1f}; x 8 / (2 x {per} real TF32 MACs per complex MAC)")
 
 
+def gemm_engines_4096(torch, tc, _lib) -> dict:
+    """Algorithmic TFLOP/s (8*M*N*K) of the FFMA kernel and of the 3xTF32
+    tensor-core kernel on the same 4096^3 complex64 GEMM, 3 launches each
+    after a warm-up, CUDA events."""
+    n = 4096
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn(n * n, dtype=torch.complex64, device="cuda", generator=g)
+    B = torch.randn(n * n, dtype=torch.complex64, device="cuda", generator=g)
+    C = torch.empty(n * n, dtype=torch.complex64, device="cuda")
+    out = {}
+    for name, mode in (("ffma_tflops", _lib.GEMM_FFMA), ("tc3_tflops", _lib.GEMM_TC3)):
+        tc.gemm_buffer(1, n, n, n, A, 0, B, 0, C, mode=mode)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            tc.gemm_buffer(1, n, n, n, A, 0, B, 0, C, mode=mode)
+        b.record()
+        torch.cuda.synchronize()
+        out[name] = round(8.0 * n ** 3 * 3 / a.elapsed_time(b) / 1e9, 1)
+        out[name.replace("_tflops", "_kernel")] = _lib.last_kernel()
+    return out
+
+
 def run_paths(args):
     """Configs 4/5 at full depth.  One step = one contraction path of the
     current unit on every rank (PlanExecutor.run, the reference's public
@@ -742,7 +780,16 @@ def run_paths(args):
             "algorithmic": f"8*m*k*n flops per {dom} launch summed over the {d['launches']} launches "
                            f"of the {args.steps} timed steps / their CUDA-event time (eager launches, "
                            f"events on the launching stream)",
-            "traffic": measured_traffic(args.workload, dom, d["bytes"], d["launches"])}
+            "traffic_detail": measured_traffic(args.workload, dom, d["bytes"] / max(d["launches"], 1), 0)}
+    roof["traffic"] = (roof["traffic_detail"] or {}).get("dram_bytes_per_launch")
+    ncu_pipe = tensor_pipe_ncu(dom)
+    if ncu_pipe:
+        roof["tensor_pipe_active_ncu"] = ncu_pipe
+
+    # ---- the plain FFMA engine (K3) beside the tensor-core engine on one
+    # 4096^3 complex GEMM (outside the timed region; rank 0)
+    if rank == 0:
+        roof["ffma_vs_tensor_4096"] = gemm_engines_4096(torch, tc, _lib)
 
     # ---- N>1 self-check: rank 0 recomputes the first path another rank walked
     selfcheck = None

@@ -295,14 +295,17 @@ int qf_fill_zero(void *y, int64_t bytes, void *stream);
 int qf_workspace_reserve(int64_t bytes, void *stream);
 int qf_workspace_release(void);
 
-/* K2 tuning/validation knob: 0 = auto; 1/2 = unpromoted SS/TS tiles;
- * 3 = promoted, register prefetch; 4 = promoted, cp.async stream; 5 = reg;
- * 6 = CTA pair (cta_group::2); 7/8 = warp-specialised with grouped handoff;
- * 9 = warp-specialised short-K; 10/11/12 = short-K run kernel with 8
- * converter warps / 16 converter warps / 16 converter + 4 epilogue warps;
- * 13/14 = long-K kernel with a TMEM master accumulator promoted every 4 / 8
- * k-blocks (13 is the long-K default); 15 = long-K warp-specialised kernel
- * promoting into converter registers.  Returns the previous setting. */
+/* K2 tuning/validation knob (A/B measurements and tests; 0 = auto, the
+ * product setting).  Short-K kernel flavours: 10/11/12 = 8 converter warps /
+ * 16 converter warps / 16 converter + 4 epilogue warps, 20/21 = TMA-fed with
+ * an 8 / 4 deep ring, 23 = 64-column tiles for narrow views.  Long-K
+ * flavours (csrc/qf_gemm_tc.cu): 13 = converter fetch (no TMA), 19/26/27 =
+ * real-block form promoted every 4/16/32 k-blocks, 30/31/32 = Gauss form on
+ * 128 x 64 tiles promoted every 16/32/64 k-blocks, 34 = Gauss, 2 stages.
+ * Wide long-K kernel (csrc/qf_gemm_tcw.cu, 128 x 128 Gauss tiles, master in
+ * registers): 40/41/42 = single CTAs promoted every 64/128/32 k-blocks,
+ * 43/44/45 = CTA pairs (cta_group::2) likewise; auto = pairs when M fills
+ * 256-row tiles.  Returns the previous setting. */
 int qf_tc3_set_variant(int variant);
 
 /* K3 tuning/validation knob for memory-bound small K x N shapes: 0 = auto

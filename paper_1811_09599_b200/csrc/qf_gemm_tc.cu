@@ -1405,7 +1405,7 @@ static int launch_short_tma(const GemmArgs &g, cudaStream_t s) {
 // converter fetch (no TMA; also the fallback when TMA cannot describe the
 // operands).
 static int launch_long(const GemmArgs &g, cudaStream_t s) {
-  // N >= 128 and K >= 512: the wide (128 x 128) Gauss kernel with its master in
+  // N >= 128 and K >= 256: the wide (128 x 128) Gauss kernel with its master in
   // registers (qf_gemm_tcw.cu).  Pins: 40/41/42 = wide single-CTA with CK
   // 64/128/32, 43/44/45 = CTA pairs (cta_group::2) with CK 64/128/32, 32 = the
   // 64-column Gauss kernel (CK 64).

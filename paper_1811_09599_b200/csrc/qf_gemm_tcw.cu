@@ -52,6 +52,7 @@ constexpr int RAW = 8;           // raw TMA ring depth (k-blocks in flight)
 // converting warps: 4 (A rows + B columns 0-63) + 2 (B columns 64-127); in a CTA
 // pair every CTA converts only its 64 columns of B, on the 4 A warps
 constexpr int NPROMO = 8;        // promotion / epilogue warps
+constexpr uint32_t EPOCH = 16;   // stages per lockstep epoch of the TMA producers
 constexpr int THREADS_W = 512;   // warps 0-3 | 4 TMA, 5 MMA, 6-7 | 8-15
 constexpr int REGS_A = 112;      // setmaxnreg targets (multiples of 8; 128 at launch)
 constexpr int REGS_MISC = 72;
@@ -293,7 +294,8 @@ template <int CK, bool PAIR>
 __global__ void __launch_bounds__(THREADS_W, 1)
     cgemm_tc3w_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, const __grid_constant__ CUtensorMap tmA,
-                      const __grid_constant__ CUtensorMap tmB) {
+                      const __grid_constant__ CUtensorMap tmB, uint32_t *epoch_sync,
+                      uint32_t max_epochs) {
   using L = Lw<PAIR>;
   constexpr int NCONV = L::NCONV;
   constexpr uint32_t NCTA = PAIR ? 2 : 1;
@@ -491,6 +493,24 @@ __global__ void __launch_bounds__(THREADS_W, 1)
             v_ra = g.v_ra >= BM ? m0 - v_rb * (int32_t)g.v_ra : 0;
           }
           for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
+            if (epoch_sync && (f & (EPOCH - 1)) == 0) {
+              // soft lockstep: every EPOCH stages announce this CTA's progress
+              // and wait until every CTA has reached the previous epoch, so the
+              // CTAs that share an A or a B panel stay within ~2 EPOCH stages of
+              // each other and the panel is read from DRAM once, from L2 after
+              // (without it the CTAs drift apart over a K = 32768 sweep: ncu
+              // counted 6.1 TB of DRAM reads per config-4 path, 7x the panels)
+              const uint32_t e = f / EPOCH;
+              asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(epoch_sync + e) : "memory");
+              if (e >= 1) {
+                uint32_t seen;
+                do {
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(epoch_sync + e - 1)
+                               : "memory");
+                  if (seen < gridDim.x) __nanosleep(200);
+                } while (seen < gridDim.x);
+              }
+            }
             const uint32_t slot = f & (RAW - 1);
             if (f >= RAW) mbar_wait(&rawfree[slot], ((f / RAW) + 1) & 1u);
             const uint32_t bar = smem_u32(&rawfull[slot]);
@@ -527,6 +547,10 @@ __global__ void __launch_bounds__(THREADS_W, 1)
                 : "memory");
           }
         }
+        // CTAs with fewer tiles arrive for the epochs they never reach
+        if (epoch_sync)
+          for (uint32_t e = (f + EPOCH - 1) / EPOCH; e < max_epochs; ++e)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(epoch_sync + e) : "memory");
       }
       __syncwarp();
     }
@@ -547,6 +571,38 @@ __global__ void __launch_bounds__(THREADS_W, 1)
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                    "r"(L::TMEM_COLS));
   }
+}
+
+// Lockstep counters of the TMA producers: a ring of 4 zeroed-per-launch
+// slots per device (launches on one stream never overlap; the ring covers a
+// second stream).  Allocated on first use outside stream capture; a launch
+// that cannot have counters (first use while capturing, too many epochs)
+// simply runs without lockstep.
+constexpr int64_t SYNC_SLOT_WORDS = 1 << 18;
+static uint32_t *sync_slot(cudaStream_t s, int64_t words) {
+  static uint32_t *base[64] = {nullptr};
+  static unsigned next[64] = {0};
+  static const bool off = getenv("QF_TC3W_NOSYNC") != nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (off || dev >= 64 || words > SYNC_SLOT_WORDS) return nullptr;
+  if (!base[dev]) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (cap != cudaStreamCaptureStatusNone) return nullptr;
+    void *p = nullptr;
+    if (cudaMalloc(&p, 4 * SYNC_SLOT_WORDS * sizeof(uint32_t)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    base[dev] = static_cast<uint32_t *>(p);
+  }
+  uint32_t *slot = base[dev] + (next[dev]++ & 3u) * SYNC_SLOT_WORDS;
+  if (cudaMemsetAsync(slot, 0, (size_t)words * sizeof(uint32_t), s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return slot;
 }
 
 template <int CK, bool PAIR>
@@ -599,7 +655,12 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
     return QF_ERR_INVALID;
   }
   const int64_t units = PAIR ? sm_count() / 2 : sm_count();
-  const int64_t grid = std::min<int64_t>(total, units) * (PAIR ? 2 : 1);
+  const int64_t nunits = std::min<int64_t>(total, units);
+  const int64_t grid = nunits * (PAIR ? 2 : 1);
+  // lockstep only where panels are long (K >= 2048) and shared by several waves
+  const int64_t nk = (g.K + KB - 1) / KB;
+  const int64_t max_epochs = ((total + nunits - 1) / nunits * nk + EPOCH - 1) / EPOCH;
+  uint32_t *epochs = (nk >= 256 && nunits > 1) ? sync_slot(s, max_epochs) : nullptr;
   if constexpr (PAIR) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -614,7 +675,7 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, g, (uint32_t)tiles_m, (uint32_t)tiles_n,
-                                       (uint32_t)total, tmA, tmB);
+                                       (uint32_t)total, tmA, tmB, epochs, (uint32_t)max_epochs);
     if (e != cudaSuccess) {
       set_error("tc3w: pair launch failed: %s", cudaGetErrorString(e));
       return QF_ERR_CUDA;
@@ -622,7 +683,8 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
     return check_launch("cgemm_tc3w");
   }
   kern<<<(unsigned)grid, THREADS_W, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
-                                                  (uint32_t)total, tmA, tmB);
+                                                  (uint32_t)total, tmA, tmB, epochs,
+                                                  (uint32_t)max_epochs);
   return check_launch("cgemm_tc3w");
 }
 

@@ -1,0 +1,8 @@
+#!/bin/bash
+# DRAM traffic of one config-4 path (the bench step) and one config-5 path
+mkdir -p gpurun_out
+for w in config4 config5; do
+timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  --clock-control none --csv --log-file gpurun_out/r2c_${w}_traffic.csv python scripts/ncu_c4_path.py $w > gpurun_out/r2c_${w}_traffic.log 2>&1
+echo "$w rc=$?"; tail -2 gpurun_out/r2c_${w}_traffic.log
+done

@@ -340,3 +340,30 @@ def test_permutation_plans_match_reference_moves():
     assert worked.move_summary() == [("L", 2), ("R", 4), ("L", 2)]
     with pytest.raises(ValueError):
         tcore.Move("X", (0,), 1)
+
+
+def test_slice_late_byte_guard():
+    """A slice-late step is refused when its open tensor (sliced result x the
+    kept cuts' dimensions) would pass the cap or half the memory budget."""
+    from types import SimpleNamespace
+    lat = qf.Lattice.rectangle(5, 5)
+    plan = qf.grid_plan(lat, n_cuts=1)
+    from paper_1811_09599_b200.circuits import edge_activations
+    from paper_1811_09599_b200.network_builder import edge_label
+    bond = {e: 2 ** k for e, k in edge_activations(lat, 24).items() if k > 0}
+    tensors = {}
+    for s in range(lat.n):
+        labels = tuple(sorted(edge_label(*e) for e in bond if s in e))
+        dims = tuple(bond[e] for l in labels for e in bond if edge_label(*e) == l)
+        tensors[s] = SimpleNamespace(labels=labels, dims=dims, dtype=np.complex64)
+    net = SimpleNamespace(tensors=tensors, circuit=SimpleNamespace(lattice=lat), late=None,
+                          bond_dim=bond)
+    ex = cp.PlanExecutor(net, plan)
+    assert ex.late, "config 2 has slice-late steps"
+    tight = cp.PlanExecutor(net, plan, memory_budget=1 << 12)
+    assert not tight.late
+    prev, cp.LATE_OPEN_MAX_BYTES = cp.LATE_OPEN_MAX_BYTES, 16
+    try:
+        assert not cp.PlanExecutor(net, plan).late
+    finally:
+        cp.LATE_OPEN_MAX_BYTES = prev
