@@ -837,6 +837,8 @@ def run_paths(args):
     # ---- end to end through the public API (host in, host out); the timed
     # walk's cached intermediates (up to ~70 GiB at config 4) are released
     # first so the API call has the device to itself
+    unit_results = [[[float(v.real), float(v.imag)] for v in r[:4].cpu().numpy()]
+                    for r in state["results"][:4]]
     state.update(ex=None, acc=None, results=[], contrib={})
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -904,8 +906,7 @@ def run_paths(args):
             "clocks": clocks.summary(), "cpu_baseline": cpu, "self_check": selfcheck,
             "units_completed_in_run": state["u"],
             # amplitudes of the units completed inside this run (first 4 values each)
-            "unit_results": [[[float(v.real), float(v.imag)] for v in r[:4].cpu().numpy()]
-                             for r in state["results"][:4]],
+            "unit_results": unit_results,
         }
         # issued TF32 MMA flops / (2048 MACs/clk/SM x 148 SMs x the SM clock
         # measured under load): what the tensor pipe did at the clock it ran at

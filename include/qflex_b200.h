@@ -304,8 +304,9 @@ int qf_workspace_release(void);
  * 128 x 64 tiles promoted every 16/32/64 k-blocks, 34 = Gauss, 2 stages.
  * Wide long-K kernel (csrc/qf_gemm_tcw.cu, 128 x 128 Gauss tiles, master in
  * registers): 40/41/42 = single CTAs promoted every 64/128/32 k-blocks,
- * 43/44/45 = CTA pairs (cta_group::2) likewise; auto = pairs when M fills
- * 256-row tiles.  Returns the previous setting. */
+ * 43/44/45 = CTA pairs (cta_group::2) likewise, 46 = pairs draining the
+ * partial in 4-column pieces; auto = pairs when M fills 256-row tiles.
+ * Returns the previous setting. */
 int qf_tc3_set_variant(int variant);
 
 /* K3 tuning/validation knob for memory-bound small K x N shapes: 0 = auto

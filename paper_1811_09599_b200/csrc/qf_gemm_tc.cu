@@ -1409,7 +1409,8 @@ static int launch_long(const GemmArgs &g, cudaStream_t s) {
   // registers (qf_gemm_tcw.cu).  Pins: 40/41/42 = wide single-CTA with CK
   // 64/128/32, 43/44/45 = CTA pairs (cta_group::2) with CK 64/128/32, 32 = the
   // 64-column Gauss kernel (CK 64).
-  if ((g_tc3_variant == 0 || (g_tc3_variant >= 40 && g_tc3_variant <= 45)) && tc3w_ok(g)) {
+  if ((g_tc3_variant == 0 || (g_tc3_variant >= 40 && g_tc3_variant <= 46)) && tc3w_ok(g)) {
+    if (g_tc3_variant == 46) return gemm_tc3w(g, s, 64, 2);
     const int v = g_tc3_variant;
     const int ck = (v == 41 || v == 44) ? 128 : (v == 42 || v == 45) ? 32 : 64;
     return gemm_tc3w(g, s, ck, v == 0 ? -1 : v >= 43 ? 1 : 0);   // auto: pairs when M fills them

@@ -24,8 +24,8 @@
 // 64-column kernel) and write the tile out of registers at its end.  The
 // register file is re-partitioned with setmaxnreg.  The pool is what the CTA
 // got at launch, and ptxas sizes that for whole warpgroups: 512 threads
-// launch with 128 registers each (all 64 K), then warps 0-3 drop to 112,
-// warps 4-7 to 72, and the promotion warps grow to 160.
+// launch with 128 registers each (all 64 K), then warps 0-3 drop to 104,
+// warps 4-7 to 72, and the promotion warps grow to 168.
 //
 // Warp roles (16 warps): 0-3 A converters (thread = one A row, all 8 k of a
 // stage; also B columns 0-63), 4 TMA producer, 5 MMA issuer, 6-7 B converters
@@ -54,9 +54,9 @@ constexpr int RAW = 8;           // raw TMA ring depth (k-blocks in flight)
 constexpr int NPROMO = 8;        // promotion / epilogue warps
 constexpr uint32_t EPOCH = 16;   // stages per lockstep epoch of the TMA producers
 constexpr int THREADS_W = 512;   // warps 0-3 | 4 TMA, 5 MMA, 6-7 | 8-15
-constexpr int REGS_A = 112;      // setmaxnreg targets (multiples of 8; 128 at launch)
+constexpr int REGS_A = 104;      // setmaxnreg targets (multiples of 8; 128 at launch)
 constexpr int REGS_MISC = 72;
-constexpr int REGS_PROMO = 160;
+constexpr int REGS_PROMO = 168;
 static_assert(128 * REGS_A + 128 * REGS_MISC + 256 * REGS_PROMO <= 65536, "register file");
 
 template <bool PAIR>
@@ -290,7 +290,7 @@ __device__ __forceinline__ void convert_loop(const GemmArgs &g, uint8_t *smem, u
   }
 }
 
-template <int CK, bool PAIR>
+template <int CK, bool PAIR, int DP>
 __global__ void __launch_bounds__(THREADS_W, 1)
     cgemm_tc3w_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, const __grid_constant__ CUtensorMap tmA,
@@ -372,23 +372,29 @@ __global__ void __launch_bounds__(THREADS_W, 1)
         mbar_wait_sleep(pbar, chunkc & 1u, 200u);   // a chunk is >= 10 us of MMAs
         tc_fence_after();
 #pragma unroll
-        for (int piece = 0; piece < 16; ++piece) {   // 4 columns of T1, T2, T3 per round trip
-          uint32_t t1[4], t2[4], t3[4];
-          tmem_ld4(pbase + piece * 4, t1);
-          tmem_ld4(pbase + BN + piece * 4, t2);
-          tmem_ld4(pbase + 2 * BN + piece * 4, t3);
+        for (int piece = 0; piece < 64 / DP; ++piece) {   // DP columns of T1, T2, T3 per round trip
+          uint32_t t1[DP], t2[DP], t3[DP];
+          if constexpr (DP == 8) {
+            tmem_ld8(pbase + piece * DP, t1);
+            tmem_ld8(pbase + BN + piece * DP, t2);
+            tmem_ld8(pbase + 2 * BN + piece * DP, t3);
+          } else {
+            tmem_ld4(pbase + piece * DP, t1);
+            tmem_ld4(pbase + BN + piece * DP, t2);
+            tmem_ld4(pbase + 2 * BN + piece * DP, t3);
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (piece == 15) {   // the partial is in registers: hand it back to the tensor pipe
+          if (piece == 64 / DP - 1) {   // the partial is in registers: hand it back to the tensor pipe
             tc_fence_before();
             __syncwarp();
             if (lane == 0) arrive_cluster(accfree_leader);
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < DP; ++j) {
             const float x1 = __uint_as_float(t1[j]), x2 = __uint_as_float(t2[j]);
             const float re = x1 - x2, im = __uint_as_float(t3[j]) - x1 - x2;
-            mr[piece * 4 + j] += re;
-            mi[piece * 4 + j] += im;
+            mr[piece * DP + j] += re;
+            mi[piece * DP + j] += im;
           }
         }
       }
@@ -605,10 +611,10 @@ static uint32_t *sync_slot(cudaStream_t s, int64_t words) {
   return slot;
 }
 
-template <int CK, bool PAIR>
+template <int CK, bool PAIR, int DP = 8>
 static int launch_wide(const GemmArgs &g, cudaStream_t s) {
   using L = Lw<PAIR>;
-  auto kern = cgemm_tc3w_kernel<CK, PAIR>;
+  auto kern = cgemm_tc3w_kernel<CK, PAIR, DP>;
   CUtensorMap tmA{}, tmB{};
   const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
   const uint64_t na = g.a_boff ? (uint64_t)g.a_nslice : nb;   // A entries addressable
@@ -717,6 +723,7 @@ bool tc3w_pair_ok(const GemmArgs &g) {
 
 int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck, int pair) {
   const bool use_pair = pair > 0 || (pair < 0 && tc3w_pair_ok(g));
+  if (pair == 2) return tcw::launch_wide<64, true, 4>(g, s);   // A/B: 4-column drain pieces (8: +0.5%)
   if (use_pair) {
     if (ck == 128) return tcw::launch_wide<128, true>(g, s);
     if (ck == 32) return tcw::launch_wide<32, true>(g, s);

@@ -657,6 +657,7 @@ def _gemm_view(nb, m, n, k, a_ptr, strideA, view, B, ldb, sB, opB, out, b_boff=N
 
 _view_enabled = True
 _tview_enabled = True
+_compute_views = True   # A/B knob: TMA views for compute-bound shapes too (contract)
 
 
 def set_tview(enabled: bool) -> bool:
@@ -728,23 +729,30 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     a_n = batch + a_free + k_order
     a_t = batch + k_order + a_free
     entry = a.size // max(bt, 1)
-    if (list(a.labels) not in (a_n, a_t) and a.data.dtype == torch.complex64
-            and list(a.labels[:len(batch)]) == batch and entry >= 4096 and entry < 2 ** 31
-            and m <= 2 ** 22 and k <= 4096 and _gather_enabled
+    nb = len(batch)
+    ldb = n if opB == _lib.OP_N else k
+    scattered = (list(a.labels) not in (a_n, a_t) and a.data.dtype == torch.complex64
+                 and list(a.labels[:nb]) == batch and entry >= 4096 and _gather_enabled)
+    # A strided view read by TMA costs nothing over a plain layout: taken
+    # whenever the layout has one, compute-bound shapes included (config 5:
+    # the 16^7-entry operands of the region builds were permuted first,
+    # 0.7 ms each, 18% of a path).
+    view = _a_view(a.labels[nb:], a.dims[nb:], a_free, k_order) if scattered else None
+    if view is not None and not _compute_views and _permute_pays(bt, m, k, n):
+        view = None
+    if view is not None and _gemm_view(bt, m, n, k, a.data.data_ptr(), entry, view, B,
+                                       max(ldb, 1), k * n, opB, out):
+        pass
+    elif (scattered and entry < 2 ** 31 and m <= 2 ** 22 and k <= 4096
             and not _permute_pays(bt, m, k, n)):
-        # fuse the big operand's permutation into the GEMM fetch: a strided
-        # view read by TMA when it has one, else offset tables
-        nb = len(batch)
-        view = _a_view(a.labels[nb:], a.dims[nb:], a_free, k_order)
-        ldb = n if opB == _lib.OP_N else k
-        if view is None or not _gemm_view(bt, m, n, k, a.data.data_ptr(), entry, view, B,
-                                          max(ldb, 1), k * n, opB, out):
-            if front:
-                a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
-            roff, coff, rows_unit = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order,
-                                                   a.data.device)
-            gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out,
-                               rows_unit=rows_unit)
+        # no view: fuse the big operand's permutation into the GEMM fetch
+        # through offset tables (memory-bound shapes only)
+        if front:
+            a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
+        roff, coff, rows_unit = _gather_tables(a.dims[nb:], a.labels[nb:], a_free, k_order,
+                                               a.data.device)
+        gemm_gather_buffer(bt, m, n, k, a.data, entry, roff, coff, B.data, opB, out,
+                           rows_unit=rows_unit)
     else:
         if front and list(a.labels) not in (a_n, a_t):   # permuted anyway
             a_free = [l for l in a_free if l in front] + [l for l in a_free if l not in front]
