@@ -812,7 +812,11 @@ def test_permute_plan_first_built_in_capture_is_refused():
 # tiles in M, N and K, several tiles per CTA, entries (batch), all operand
 # layouts, 1/2/many promotion chunks per tile
 WIDE_SHAPES = [(1, 256, 256, 1024), (1, 128, 128, 512), (2, 384, 640, 520), (1, 1000, 1152, 778),
-               (3, 2048, 1024, 1024), (1, 19000, 128, 512), (1, 128, 2048, 4100)]
+               (3, 2048, 1024, 1024), (1, 19000, 128, 512), (1, 128, 2048, 4100),
+               # K >= 2048: the TMA producers run in lockstep epochs; more tiles than
+               # CTAs / CTA pairs with a ragged last wave (CTAs with fewer tiles
+               # pre-arrive for the epochs they never reach), several entries
+               (1, 19200, 128, 2048), (2, 9500, 256, 2056)]
 
 
 @pytest.mark.parametrize("shape", WIDE_SHAPES)
