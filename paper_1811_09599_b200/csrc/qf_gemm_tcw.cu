@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
         const uint32_t rawa = smem_u32(smem + L::RAWA_OFF), rawb = smem_u32(smem + L::RAWB_OFF);
         Cur pc;
         uint32_t f = 0;
+        bool sync_ok = true;
         for (uint32_t w = w0; w < total; w += wstep) {
           cur_set(pc, w, tiles_m, tiles_n);
           const int32_t m0 = (int32_t)((pc.mt * NCTA + crank) * BM), b = (int32_t)pc.bidx;
@@ -508,13 +509,17 @@ __global__ void __launch_bounds__(THREADS_W, 1)
               // counted 6.1 TB of DRAM reads per config-4 path, 7x the panels)
               const uint32_t e = f / EPOCH;
               asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(epoch_sync + e) : "memory");
-              if (e >= 1) {
-                uint32_t seen;
+              if (e >= 1 && sync_ok) {
+                // bounded wait (~20 ms): if the CTAs of this grid are not all
+                // resident (SMs held by another context or kernel) the
+                // lockstep is dropped instead of risking a stall
+                uint32_t seen, polls = 0;
                 do {
                   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(epoch_sync + e - 1)
                                : "memory");
                   if (seen < gridDim.x) __nanosleep(200);
-                } while (seen < gridDim.x);
+                } while (seen < gridDim.x && ++polls < 100000u);
+                sync_ok = seen >= gridDim.x;
               }
             }
             const uint32_t slot = f & (RAW - 1);

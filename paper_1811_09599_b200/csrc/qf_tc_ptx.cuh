@@ -160,6 +160,9 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b,
 }
 
 __device__ __forceinline__ void split_fast(float x, uint32_t &hi, uint32_t &lo) {
+  // (measured and rejected: hi = the raw bits -- the tensor core reads the top
+  // 19 -- and lo = x - trunc(x) saves one of the three ALU ops per split:
+  // +1% on the wide kernel, +2% on K = 16 shapes, error 3.7e-6 -> 4.3e-6)
   const uint32_t h = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;  // round-half-away to tf32
   hi = h;
   lo = __float_as_uint(x - __uint_as_float(h));  // exact; the tensor core keeps its top 19 bits
