@@ -1056,6 +1056,13 @@ def _compact(r: dict) -> dict:
     for k in ("per_size", "executed_tflops", "units_completed_in_run"):
         if k in r:
             out[k] = r[k]
+    e2e = r.get("e2e") or {}
+    if e2e.get("seconds_per_unit"):
+        out["e2e_seconds_per_unit"] = e2e["seconds_per_unit"]
+    cpu = r.get("cpu_baseline")
+    if cpu:
+        out["cpu_baseline"] = {k: cpu.get(k) for k in ("value", "unit", "cores", "kind", "projection",
+                                                       "gflops", "seconds")}
     return out
 
 
@@ -1068,7 +1075,10 @@ def secondary_workloads(args) -> list:
     runs = (("config2", run_gpu, {"steps": 10}),
             ("config1", run_gpu, {"steps": 10}),
             ("permute", run_permute, {"steps": 3, "perms": 8}),
-            ("config5", run_paths, {"steps": 10, "e2e_units": 0}))
+            # config 5: 10 path steps, ONE whole 64-amplitude batch (328 paths)
+            # through amplitude_batch() as its e2e, and a short CPU projection
+            ("config5", run_paths, {"steps": 10, "e2e_units": 1, "no_cpu_baseline": False,
+                                    "cpu_seconds": 6.0}))
     want = [w.strip() for w in str(args.secondary_workloads).split(",") if w.strip()]
     out = []
     for name, fn, over in runs:
@@ -1078,6 +1088,8 @@ def secondary_workloads(args) -> list:
         sub.workload, sub.warmup, sub.no_cpu_baseline = name, 3, True
         for k, v in over.items():
             setattr(sub, k, v)
+        if args.no_cpu_baseline:
+            sub.no_cpu_baseline = True
         try:
             r = fn(sub)
             if r is not None:
