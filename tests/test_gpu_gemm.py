@@ -856,3 +856,37 @@ def test_tcgen05_wide_alpha_beta(ab, variant):
     finally:
         lib.qf_tc3_set_variant(prev)
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_long_k_view_on_the_wide_kernel(case):
+    """A compute-bound contraction whose big operand has its summed labels in
+    two runs: read in place as a 5-D TMA view by the wide long-K kernel
+    (single CTAs and CTA pairs) instead of being permuted first -- equal to
+    the permuted path and to numpy."""
+    rng = np.random.default_rng(900 + case)
+    dims = {"r0": [16, 8, 40][case], "k0": 16, "r1": [256, 128, 64][case], "k1": [16, 32, 16][case],
+            "n": [256, 128, 384][case]}
+    a_labels, b_labels = ["r0", "k0", "r1", "k1"], ["k0", "k1", "n"]
+    A = _rand(rng, [dims[l] for l in a_labels], np.complex64)
+    B = _rand(rng, [dims[l] for l in b_labels], np.complex64)
+    ref = np.einsum("akbl,kln->abn", A.astype(np.complex128), B.astype(np.complex128))
+    lib = _lib.load()
+    for variant in (0, 40, 43):
+        prev = lib.qf_tc3_set_variant(variant)
+        try:
+            with tc.KernelTimer() as kt:
+                o = tc.contract(tc.Tensor(a_labels, A), tc.Tensor(b_labels, B))
+            kinds = kt.summary(detail=True)
+        finally:
+            lib.qf_tc3_set_variant(prev)
+        assert any(" V" in k for k in kinds), kinds
+        assert _lib.last_kernel() == "cgemm_tc3w"
+        assert o.labels == ("r0", "r1", "n")
+        assert np.linalg.norm(o.array - ref) / np.linalg.norm(ref) < 1e-5
+    prev = tc.set_view(False)
+    try:
+        o2 = tc.contract(tc.Tensor(a_labels, A), tc.Tensor(b_labels, B))
+    finally:
+        tc.set_view(prev)
+    assert np.linalg.norm(o2.array - ref) / np.linalg.norm(ref) < 1e-5
