@@ -1,6 +1,6 @@
 """Config-4 paths with / without TMA views of compute-bound operands."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1811_09599_b200 as qf
 from paper_1811_09599_b200 import tensor_core as tc
