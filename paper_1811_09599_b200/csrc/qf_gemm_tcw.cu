@@ -36,6 +36,13 @@
 // in shared memory; one elected lane issues T_j += A_j(hi) B_j(hi) + A_j(hi)
 // B_j(lo) + A_j(lo) B_j(hi), j = 1..3.  Re = T1 - T2, Im = T3 - T1 - T2 at
 // promotion.
+//
+// CTA pairs (PAIR, the default when M fills 256-row tiles): a cluster of two
+// CTAs owns a 256 x 128 tile; each converts its own 128 A rows and only 64 B
+// columns, the leader issues cta_group::2 MMAs with M = 256 and multicasts the
+// completions.  Lockstep: the producers of all CTAs announce their progress
+// every EPOCH stages in a global counter array and wait for the slowest, so
+// CTAs sharing a panel read it from DRAM once (profiles/r2c_gemm_wide.md).
 #include <algorithm>
 #include <cstdlib>
 
