@@ -890,3 +890,42 @@ def test_long_k_view_on_the_wide_kernel(case):
     finally:
         tc.set_view(prev)
     assert np.linalg.norm(o2.array - ref) / np.linalg.norm(ref) < 1e-5
+
+
+@pytest.mark.parametrize("variant", [32, 40, 43], ids=["narrow", "wide", "wide-pair"])
+@pytest.mark.parametrize("ops", [(0, 0), (0, 1)])
+def test_long_k_slice_coordinates(variant, ops):
+    """qf_cgemm_c64_ex2 at a long-K shape: every entry picks its A entry and
+    its [K][N] B slice by offset (a_boff / a_nslice, b_boff / b_nslice), which
+    the TMA-fed long-K kernels (64-column and wide, single CTAs and pairs)
+    turn into slice coordinates."""
+    import ctypes
+    rng = np.random.default_rng(77)
+    nb, M, N, K, a_ns, b_ns = 6, 256, 128, 512, 4, 3
+    opA, opB = ops
+    A = _rand(rng, (a_ns, M, K), np.complex64)
+    B = _rand(rng, (b_ns, K, N) if opB == 0 else (b_ns, N, K), np.complex64)
+    pa, pb = rng.integers(0, a_ns, size=nb), rng.integers(0, b_ns, size=nb)
+    dA, dB = torch.from_numpy(A.reshape(-1)).cuda(), torch.from_numpy(B.reshape(-1)).cuda()
+    a_boff = torch.from_numpy((pa * M * K).astype(np.int64)).cuda()
+    b_boff = torch.from_numpy((pb * K * N).astype(np.int64)).cuda()
+    out = torch.zeros(nb * M * N, dtype=torch.complex64, device="cuda")
+    lib = _lib.load()
+    vp = ctypes.c_void_p
+    prev = lib.qf_tc3_set_variant(variant)
+    try:
+        st = lib.qf_cgemm_c64_ex2(
+            _lib.GEMM_TC3 | _lib.BOFF_EVEN | _lib.BBOFF_EVEN, nb, M, N, K, vp(dA.data_ptr()), K, M * K,
+            _lib.OP_N, vp(a_boff.data_ptr()), a_ns, vp(0), vp(0), vp(dB.data_ptr()),
+            N if opB == 0 else K, K * N, opB, vp(b_boff.data_ptr()), b_ns, vp(out.data_ptr()), N,
+            M * N, 1.0, 0.0, 0.0, 0.0, tc.stream_handle())
+        _lib.check(st, "ex2")
+        torch.cuda.synchronize()
+        kern = _lib.last_kernel()
+    finally:
+        lib.qf_tc3_set_variant(prev)
+    assert kern == ("cgemm_tc3g" if variant == 32 else "cgemm_tc3w"), kern
+    Bn = B if opB == 0 else B.transpose(0, 2, 1)
+    want = np.matmul(A[pa].astype(np.complex128), Bn[pb].astype(np.complex128))
+    got = out.cpu().numpy().reshape(nb, M, N)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
