@@ -1481,6 +1481,9 @@ int gemm_tc3(const GemmArgs &g_in, cudaStream_t s) {
   g.dbg = tc3_debug();
   if (g.batch == 0 || g.M == 0 || g.N == 0) return QF_OK;
   QF_REQUIRE(g.K > 0, "tc3: K must be positive (use FFMA for K == 0)");
+  // huge M with K = 16, N = 16 / 32: the streaming kernel (pin 50 = off)
+  if (g_tc3_variant != 50 && (g_tc3_variant == 0 || g_tc3_variant == 51) && tc3s_ok(g))
+    return gemm_tc3s(g, s);
   if (g.c_nblk && (!g.v_kin || g.K > 128 || g.c_trans)) {
     set_error("tc3: column-blocked C only on the short-K view kernel");
     return QF_ERR_UNSUPPORTED;

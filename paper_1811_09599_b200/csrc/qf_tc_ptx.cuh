@@ -323,6 +323,9 @@ bool tma_ok(const GemmArgs &g);
 
 // qf_gemm_tcw.cu: the wide (128 x 128) Gauss-form long-K kernel
 bool tc3w_ok(const GemmArgs &g);
+// qf_gemm_tcs.cu: streaming kernel for huge M with K = 16, N = 16 / 32
+bool tc3s_ok(const GemmArgs &g);
+int gemm_tc3s(const GemmArgs &g, cudaStream_t s);
 bool tc3w_pair_ok(const GemmArgs &g);
 int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck, int pair);
 

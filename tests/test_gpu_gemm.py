@@ -929,3 +929,24 @@ def test_long_k_slice_coordinates(variant, ops):
     want = np.matmul(A[pa].astype(np.complex128), Bn[pb].astype(np.complex128))
     got = out.cpu().numpy().reshape(nb, M, N)
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
+
+
+# streaming kernel (qf_gemm_tcs.cu): one entry, huge M, K = 16, N = 16 / 32;
+# ragged last tile, both B layouts, alpha, more tiles than CTAs
+@pytest.mark.parametrize("shape", [(1, 128 * 148, 16, 16), (1, 40000, 16, 16), (1, 128 * 148 + 77, 32, 16),
+                                   (1, 131072, 32, 16)])
+@pytest.mark.parametrize("ops", [(0, 0), (0, 1)])
+@pytest.mark.parametrize("alpha", [1.0, 0.5 - 1j])
+def test_tcgen05_streaming_k16(shape, ops, alpha):
+    err = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3, alpha=alpha)
+    assert _lib.last_kernel() == "cgemm_tc3s"
+    assert err < 1e-5, err
+    # the generic short-K kernel on the same shape (pin 50) agrees
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(50)
+    try:
+        err2 = _gemm(*shape, *ops, np.complex64, mode=_lib.GEMM_TC3, alpha=alpha)
+        assert _lib.last_kernel() != "cgemm_tc3s"
+    finally:
+        lib.qf_tc3_set_variant(prev)
+    assert err2 < 1e-5, err2
