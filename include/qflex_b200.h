@@ -322,7 +322,8 @@ int qf_small_engine(int engine);
  * (rows_a rows) and rb at element stride s_rows_b; k = ko*kin + ki with ki at
  * stride s_kin and ko at s_kout -- the four runs in any memory order, e.g.
  * [ko][rb][ki][ra].  mode may carry QF_C_TRANS (C(b, m, n) at
- * C + b*strideC + n*ldc + m).  Any N (tiles of 64 columns); K in [32, 128],
+ * C + b*strideC + n*ldc + m).  Any N (tiles of 64 columns) for K in [32, 128];
+ * K >= 256 with N >= 128 on the wide long-K kernel (row-major C only);
  * kin % 8 == 0.  Serves the same contract() as qf_cgemm_c64_ex
  * (rq/tensor_core.py:391-419) when the big operand's innermost labels are
  * free: the permute before the GEMM (rq/tensor_core.py:410-416) is folded

@@ -1497,7 +1497,8 @@ int gemm_tc3(const GemmArgs &g_in, cudaStream_t s) {
     // HBM-bound shapes do not mind)
     // long K (N-views): the promoted long-K kernel with its TMA producer
     // (plain row-major epilogue only)
-    const bool long_k = g.K > 128 && !g.v_t && !g.c_trans && g.N > 32;
+    // (transposed views with long K: the wide kernel only)
+    const bool long_k = g.K > 128 && !g.c_trans && g.N > 32 && (!g.v_t || tc3w_ok(g));
     if (!(g.K >= 32 && (g.K <= 128 || long_k) && tc::tma_ok(g))) {
       set_error("tc3: A view (kin %lld, rows %lld x %lld) not TMA-describable for K=%lld N=%lld",
                 (long long)g.v_kin, (long long)g.v_ra, (long long)g.v_rb, (long long)g.K,

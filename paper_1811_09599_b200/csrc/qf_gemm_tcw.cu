@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
           if (g.v_kin) {
             v_rb = (int32_t)(m0 / (int32_t)g.v_ra);
             v_ra = g.v_ra >= BM ? m0 - v_rb * (int32_t)g.v_ra : 0;
+            if (g.v_t) v_ra *= 2;  // float coordinate of the contiguous row run
           }
           for (uint32_t kb = 0; kb < nk; ++kb, ++f) {
             if (epoch_sync && (f & (EPOCH - 1)) == 0) {
@@ -536,7 +537,19 @@ __global__ void __launch_bounds__(THREADS_W, 1)
                          "r"((uint32_t)(L::RAWA_SLOT + L::RAWB_SLOT))
                          : "memory");
             const int32_t k0 = (int32_t)(kb * KB);
-            if (g.v_kin) {
+            if (g.v_t) {
+              // transposed view: {2 ra, rb, ki, ko, entry}; the box lands as the
+              // dense [8 k][128 rows] tile of the plain opA = T path
+              asm volatile(
+                  "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                  "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(rawa + slot * L::RAWA_SLOT),
+                  "l"(&tmA), "r"(v_ra), "r"(v_rb), "r"(v_ki * KB), "r"(v_ko), "r"(aslice), "r"(bar)
+                  : "memory");
+              if (++v_ki == v_kbi) {
+                v_ki = 0;
+                ++v_ko;
+              }
+            } else if (g.v_kin) {
               // A view: {2 ki, ra, ko, rb, entry}; the box spans 128 rows of (ra, rb)
               asm volatile(
                   "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
@@ -631,7 +644,17 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
   const uint64_t nb = (uint64_t)std::max<int64_t>(g.batch, 1);
   const uint64_t na = g.a_boff ? (uint64_t)g.a_nslice : nb;   // A entries addressable
   bool okA;
-  if (g.v_kin) {
+  if (g.v_t) {
+    // transposed view: dims {2 ra, rb, ki, ko, entry} (strides need not be
+    // monotonic), box {2 min(ra, 128), 128 / min(ra, 128), 8, 1, 1}
+    const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
+    const uint64_t dims[5] = {(uint64_t)(2 * g.v_ra), (uint64_t)g.v_rb, (uint64_t)g.v_kin,
+                              (uint64_t)g.v_kout, na};
+    const uint64_t strides[4] = {(uint64_t)g.v_srb * 8, (uint64_t)g.v_ski * 8,
+                                 (uint64_t)g.v_skout * 8, (uint64_t)std::max<int64_t>(g.sA, 1) * 8};
+    const uint32_t box[5] = {2 * bra, (uint32_t)(BM / bra), (uint32_t)KB, 1, 1};
+    okA = make_tmap5(&tmA, g.A, dims, strides, box, false);
+  } else if (g.v_kin) {
     const uint32_t bra = (uint32_t)std::min<int64_t>(g.v_ra, BM);
     const uint64_t dims[5] = {(uint64_t)(2 * g.v_kin), (uint64_t)g.v_ra, (uint64_t)g.v_kout,
                               (uint64_t)g.v_rb, na};
@@ -708,11 +731,11 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
 
 }  // namespace tcw
 
-// Shapes the wide kernel takes: TMA-describable plain operands or row-major A
-// views (no offset tables, no transposed views, plain row-major C), K long
+// Shapes the wide kernel takes: TMA-describable plain operands or A views,
+// row-major or transposed (no offset tables, plain row-major C), K long
 // enough for the per-tile drain to vanish and N filling 128-column tiles.
 bool tc3w_ok(const GemmArgs &g) {
-  if (g.a_roff || g.v_t || g.c_trans || g.c_nblk) return false;
+  if (g.a_roff || g.c_trans || g.c_nblk) return false;
   if (!tc::tma_ok(g)) return false;
   // K >= 256 (one promotion chunk of 32 k-blocks per tile and up): measured
   // faster than the 64-column kernels from there on (scripts/c5_wide.py:

@@ -655,6 +655,29 @@ def _gemm_view(nb, m, n, k, a_ptr, strideA, view, B, ldb, sB, opB, out, b_boff=N
     return True
 
 
+def _gemm_tview(nb, m, n, k, a: "Tensor", strideA, a_free, k_order, B, ldb, sB, opB, out) -> bool:
+    """Run the TMA-fed kernel on a TRANSPOSED view of the big operand (its
+    innermost labels free; long K: the wide kernel); False if the layout has
+    no such view or the library reports it unsupported (caller falls back)."""
+    if _gemm_mode == _lib.GEMM_FFMA or strideA % 2 or not (_view_enabled and _tview_enabled):
+        return False
+    off = len(a.labels) - len(a_free) - len(k_order)        # leading batch labels
+    tv = _a_tview(a.labels[off:], a.dims[off:], a_free, k_order)
+    if tv is None:
+        return False
+    ra, rb, srb, kin, ski, ko, sko = tv
+    with _timed("gemm", 8 * nb * m * n * k, 8 * nb * (m * k + k * n + m * n),
+                f"b{nb} m{m} n{n} k{k} TV{'NT'[opB]}" if _timer else ""):
+        st = _lib.load().qf_cgemm_c64_tview(
+            _gemm_mode, nb, m, n, k, ctypes.c_void_p(a.data.data_ptr()), strideA, ra, rb, srb, kin,
+            ski, ko, sko, ctypes.c_void_p(B.data.data_ptr()), ldb, sB, opB, ctypes.c_void_p(0), 0,
+            ctypes.c_void_p(out.data_ptr()), max(n, 1), m * n, 1.0, 0.0, 0.0, 0.0, stream_handle())
+    if st == _lib.QF_ERR_UNSUPPORTED:
+        return False
+    _lib.check(st, "gemm_tview")
+    return True
+
+
 _view_enabled = True
 _tview_enabled = True
 _compute_views = True   # A/B knob: TMA views for compute-bound shapes too (contract)
@@ -743,6 +766,10 @@ def contract(a: Tensor, b: Tensor, thread_count: int = 1, mu: int = 5, nu: int =
     if view is not None and _gemm_view(bt, m, n, k, a.data.data_ptr(), entry, view, B,
                                        max(ldb, 1), k * n, opB, out):
         pass
+    elif (view is None and scattered and _compute_views and k >= 256 and n >= 128
+            and _gemm_tview(bt, m, n, k, a, entry, a_free, k_order, B, max(ldb, 1), k * n, opB,
+                            out)):
+        pass     # rows innermost: a transposed TMA view on the wide long-K kernel
     elif (scattered and entry < 2 ** 31 and m <= 2 ** 22 and k <= 4096
             and not _permute_pays(bt, m, k, n)):
         # no view: fuse the big operand's permutation into the GEMM fetch

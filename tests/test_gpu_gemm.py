@@ -950,3 +950,37 @@ def test_tcgen05_streaming_k16(shape, ops, alpha):
     finally:
         lib.qf_tc3_set_variant(prev)
     assert err2 < 1e-5, err2
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_long_k_transposed_view_on_the_wide_kernel(case):
+    """Compute-bound contraction whose big operand has its innermost labels
+    FREE and its summed labels in two runs: read in place as a transposed 5-D
+    TMA view by the wide long-K kernel (no permute) -- equal to numpy and to
+    the permuted path."""
+    rng = np.random.default_rng(950 + case)
+    dims = {"k0": 16, "r0": [8, 4, 24][case], "k1": [16, 32, 16][case], "r1": [256, 128, 64][case],
+            "n": [256, 128, 384][case]}
+    a_labels, b_labels = ["k0", "r0", "k1", "r1"], ["k0", "k1", "n"]
+    A = _rand(rng, [dims[l] for l in a_labels], np.complex64)
+    B = _rand(rng, [dims[l] for l in b_labels], np.complex64)
+    ref = np.einsum("kalb,kln->abn", A.astype(np.complex128), B.astype(np.complex128))
+    lib = _lib.load()
+    for variant in (0, 40, 43):
+        prev = lib.qf_tc3_set_variant(variant)
+        try:
+            with tc.KernelTimer() as kt:
+                o = tc.contract(tc.Tensor(a_labels, A), tc.Tensor(b_labels, B))
+            kinds = kt.summary(detail=True)
+        finally:
+            lib.qf_tc3_set_variant(prev)
+        assert any(" TV" in k for k in kinds), kinds
+        assert _lib.last_kernel() == "cgemm_tc3w"
+        assert o.labels == ("r0", "r1", "n")
+        assert np.linalg.norm(o.array - ref) / np.linalg.norm(ref) < 1e-5
+    prev = tc.set_tview(False)
+    try:
+        o2 = tc.contract(tc.Tensor(a_labels, A), tc.Tensor(b_labels, B))
+    finally:
+        tc.set_tview(prev)
+    assert np.linalg.norm(o2.array - ref) / np.linalg.norm(ref) < 1e-5
