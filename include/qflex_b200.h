@@ -306,7 +306,8 @@ int qf_workspace_release(void);
  * registers): 40/41/42 = single CTAs promoted every 64/128/32 k-blocks,
  * 43/44/45 = CTA pairs (cta_group::2) likewise, 46 = pairs draining the
  * partial in 4-column pieces; auto = pairs when M fills 256-row tiles.
- * Returns the previous setting. */
+ * 50 = streaming K = 16 kernel (csrc/qf_gemm_tcs.cu) off.  Returns the
+ * previous setting. */
 int qf_tc3_set_variant(int variant);
 
 /* K3 tuning/validation knob for memory-bound small K x N shapes: 0 = auto
