@@ -151,8 +151,8 @@ __device__ __forceinline__ void reg_inc() {
 struct Cur {
   uint32_t w, mt, nt, bidx;
 };
-__device__ __forceinline__ void cur_set(Cur &c, uint32_t w, uint32_t tiles_m, uint32_t tiles_n) {
-  constexpr uint32_t GM = 12;
+__device__ __forceinline__ void cur_set(Cur &c, uint32_t w, uint32_t tiles_m, uint32_t tiles_n,
+                                        uint32_t GM) {
   c.w = w;
   const uint32_t tiles = tiles_m * tiles_n;
   c.bidx = w / tiles;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
     cgemm_tc3w_kernel(const __grid_constant__ GemmArgs g, uint32_t tiles_m, uint32_t tiles_n,
                       uint32_t total, const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, uint32_t *epoch_sync,
-                      uint32_t max_epochs) {
+                      uint32_t max_epochs, uint32_t gm) {
   using L = Lw<PAIR>;
   constexpr int NCONV = L::NCONV;
   constexpr uint32_t NCTA = PAIR ? 2 : 1;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
     uint32_t chunkc = 0;
     Cur ec;
     for (uint32_t w = w0; w < total; w += wstep) {
-      cur_set(ec, w, tiles_m, tiles_n);
+      cur_set(ec, w, tiles_m, tiles_n, gm);
 #pragma unroll
       for (int j = 0; j < 64; ++j) mr[j] = mi[j] = 0.f;
       for (uint32_t c = 0; c < nchunks; ++c, ++chunkc) {
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(THREADS_W, 1)
         uint32_t f = 0;
         bool sync_ok = true;
         for (uint32_t w = w0; w < total; w += wstep) {
-          cur_set(pc, w, tiles_m, tiles_n);
+          cur_set(pc, w, tiles_m, tiles_n, gm);
           const int32_t m0 = (int32_t)((pc.mt * NCTA + crank) * BM), b = (int32_t)pc.bidx;
           const int32_t n0 = (int32_t)(pc.nt * BN + crank * L::BNL);   // pair: this CTA's B columns
           const int32_t bslice = g.b_boff ? (int32_t)(__ldg(g.b_boff + pc.bidx) / (g.K * g.N)) : b;
@@ -702,6 +702,12 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
   const int64_t nk = (g.K + KB - 1) / KB;
   const int64_t max_epochs = ((total + nunits - 1) / nunits * nk + EPOCH - 1) / EPOCH;
   uint32_t *epochs = (nk >= 256 && nunits > 1) ? sync_slot(s, max_epochs) : nullptr;
+  // row tiles (pair: 256-row tiles) per raster group; QF_TC3W_GM for A/B runs
+  static const uint32_t gm_env = [] {
+    const char *e = getenv("QF_TC3W_GM");
+    return e ? (uint32_t)std::max(1, atoi(e)) : 0u;
+  }();
+  const uint32_t gm = gm_env ? gm_env : 8u;   // 4..12 measure the same (326 TFLOP/s at 32768^3), 24: -2%
   if constexpr (PAIR) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
@@ -716,7 +722,7 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, g, (uint32_t)tiles_m, (uint32_t)tiles_n,
-                                       (uint32_t)total, tmA, tmB, epochs, (uint32_t)max_epochs);
+                                       (uint32_t)total, tmA, tmB, epochs, (uint32_t)max_epochs, gm);
     if (e != cudaSuccess) {
       set_error("tc3w: pair launch failed: %s", cudaGetErrorString(e));
       return QF_ERR_CUDA;
@@ -725,7 +731,7 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
   }
   kern<<<(unsigned)grid, THREADS_W, L::SMEM, s>>>(g, (uint32_t)tiles_m, (uint32_t)tiles_n,
                                                   (uint32_t)total, tmA, tmB, epochs,
-                                                  (uint32_t)max_epochs);
+                                                  (uint32_t)max_epochs, gm);
   return check_launch("cgemm_tc3w");
 }
 
