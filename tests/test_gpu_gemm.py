@@ -821,8 +821,8 @@ WIDE_SHAPES = [(1, 256, 256, 1024), (1, 128, 128, 512), (2, 384, 640, 520), (1, 
 
 @pytest.mark.parametrize("shape", WIDE_SHAPES)
 @pytest.mark.parametrize("ops", [(0, 0), (1, 1), (0, 1), (1, 0)])
-@pytest.mark.parametrize("variant", [40, 41, 42, 43, 44],
-                         ids=["ck64", "ck128", "ck32", "pair-ck64", "pair-ck128"])
+@pytest.mark.parametrize("variant", [40, 41, 42, 43, 44, 46],
+                         ids=["ck64", "ck128", "ck32", "pair-ck64", "pair-ck128", "pair-drain4"])
 def test_tcgen05_wide_gauss_long_k(shape, ops, variant):
     lib = _lib.load()
     prev = lib.qf_tc3_set_variant(variant)
