@@ -107,3 +107,29 @@ def test_sliced_open_operand_as_entries():
     plan = tc.expand_plan(acc, op, op2, late)
     assert plan is not None and plan["sliced"] and plan["nb"] == nb
     assert plan["labels"][0] == "@b"
+
+
+def test_views_of_the_full_depth_region_builds():
+    """The layouts the config-4/5 region builds meet (bond 32 / 16): summed
+    labels in two runs.  Innermost summed -> row-major TMA view; innermost
+    free -> transposed view; three free runs -> neither (permute)."""
+    # config 5: [a0 .. a6] of 16, K = (a3, a6): rows (a0 a1 a2) x (a4 a5)
+    labels, dims = [f"a{i}" for i in range(7)], [16] * 7
+    kin, ra, sra, ko, sko, rb, srb = tc._a_view(labels, dims, ["a0", "a1", "a2", "a4", "a5"],
+                                                ["a3", "a6"])
+    assert (kin, ko, ra, rb) == (16, 16, 256, 4096)
+    assert (sra, sko, srb) == (16, 16 ** 3, 16 ** 4)
+    assert tc._a_tview(labels, dims, ["a0", "a1", "a2", "a4", "a5"], ["a3", "a6"]) is None
+    # config 5: K = (a0, a3) with the innermost labels free: transposed view
+    free = ["a1", "a2", "a4", "a5", "a6"]
+    assert tc._a_view(labels, dims, free, ["a0", "a3"]) is None
+    ra, rb, srb, kin, ski, ko, sko = tc._a_tview(labels, dims, free, ["a0", "a3"])
+    assert (ra, rb, kin, ko) == (4096, 256, 16, 16)
+    assert (srb, ski, sko) == (16 ** 4, 16 ** 3, 16 ** 6)
+    # config 4: [a0 .. a5] of 32, K = (a1, a5): rows (a0) x (a2 a3 a4)
+    labels, dims = [f"a{i}" for i in range(6)], [32] * 6
+    v = tc._a_view(labels, dims, ["a0", "a2", "a3", "a4"], ["a1", "a5"])
+    assert v == (32, 32768, 32, 32, 32 ** 4, 32, 32 ** 5)
+    # K = (a1, a3) with rows (a0) (a2) (a4 a5): three free runs, no view of either kind
+    assert tc._a_view(labels, dims, ["a0", "a2", "a4", "a5"], ["a1", "a3"]) is None
+    assert tc._a_tview(labels, dims, ["a0", "a2", "a4", "a5"], ["a1", "a3"]) is None
