@@ -984,3 +984,32 @@ def test_long_k_transposed_view_on_the_wide_kernel(case):
     finally:
         tc.set_tview(prev)
     assert np.linalg.norm(o2.array - ref) / np.linalg.norm(ref) < 1e-5
+
+
+def test_wide_kernel_with_lockstep_replays_from_a_cuda_graph():
+    """A long-K GEMM on the wide kernel (lockstep counters zeroed by a memset
+    node before the launch) captured in a CUDA graph: replays equal the eager
+    result, also after other launches used the counter ring in between."""
+    rng = np.random.default_rng(5)
+    M, N, K = 4096, 256, 4096
+    A = torch.from_numpy(_rand(rng, (M * K,), np.complex64)).cuda()
+    B = torch.from_numpy(_rand(rng, (K * N,), np.complex64)).cuda()
+    want = torch.empty(M * N, dtype=torch.complex64, device="cuda")
+    tc.gemm_buffer(1, M, N, K, A, 0, B, 0, want, mode=_lib.GEMM_TC3)   # eager: allocates the ring
+    assert _lib.last_kernel() == "cgemm_tc3w"
+    out = torch.zeros_like(want)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        tc.gemm_buffer(1, M, N, K, A, 0, B, 0, out, mode=_lib.GEMM_TC3)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        tc.gemm_buffer(1, M, N, K, A, 0, B, 0, out, mode=_lib.GEMM_TC3)
+    for _ in range(3):
+        out.zero_()
+        graph.replay()
+        tc.gemm_buffer(1, M, N, K, A, 0, B, 0, want, mode=_lib.GEMM_TC3)   # rotates the ring
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
