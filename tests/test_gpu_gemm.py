@@ -1013,3 +1013,34 @@ def test_wide_kernel_with_lockstep_replays_from_a_cuda_graph():
         tc.gemm_buffer(1, M, N, K, A, 0, B, 0, want, mode=_lib.GEMM_TC3)   # rotates the ring
         torch.cuda.synchronize()
         assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("case", [(1, 1000, 1152, 778, 40), (1, 1000, 1152, 778, 43), (2, 300, 384, 1024, 43),
+                                  (1, 128 * 148 + 77, 16, 16, 0), (1, 40000, 32, 16, 0)],
+                         ids=["wide-ragged", "pair-ragged", "pair-batch", "stream-n16", "stream-n32"])
+def test_new_kernels_write_nothing_outside_c(case):
+    """Canaries around C: ragged tiles of the wide kernel (register epilogue)
+    and of the streaming kernel (TMA stores clip at M) leave every byte
+    outside [C, C + batch*M*N) untouched."""
+    b, M, N, K, variant = case
+    rng = np.random.default_rng(31)
+    A = torch.from_numpy(_rand(rng, (b * M * K,), np.complex64)).cuda()
+    B = torch.from_numpy(_rand(rng, (b * K * N,), np.complex64)).cuda()
+    pad = 4096
+    big = torch.full((b * M * N + 2 * pad,), 7.0 - 3.0j, dtype=torch.complex64, device="cuda")
+    C = big[pad:pad + b * M * N]
+    lib = _lib.load()
+    prev = lib.qf_tc3_set_variant(variant)
+    try:
+        tc.gemm_buffer(b, M, N, K, A, 0, B, 0, C, mode=_lib.GEMM_TC3)
+        torch.cuda.synchronize()
+        kern = _lib.last_kernel()
+    finally:
+        lib.qf_tc3_set_variant(prev)
+    assert kern == ("cgemm_tc3s" if K == 16 else "cgemm_tc3w"), kern
+    sentinel = torch.tensor(7.0 - 3.0j, dtype=torch.complex64, device="cuda")
+    assert bool((big[:pad] == sentinel).all()) and bool((big[pad + b * M * N:] == sentinel).all())
+    want = np.matmul(A.cpu().numpy().reshape(b, M, K).astype(np.complex128),
+                     B.cpu().numpy().reshape(b, K, N).astype(np.complex128))
+    got = C.cpu().numpy().reshape(b, M, N)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-5
