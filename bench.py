@@ -379,6 +379,24 @@ def run_gpu(args):
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1) / args.steps, wall_ms), world, dev)
     e2e = amps_per_step / (e2e_ms / 1e3)
 
+    # ---- the reference's single-call API as a drop-in user calls it: one
+    # amplitude() per bit-string (rq/amplitude_engine.py:114-126), host wall
+    # time; after the first (eager) call the engine replays a captured walk
+    single = None
+    if rank == 0 and world == 1:
+        n_single = min(64, len(outs))
+        for o in outs[:4]:
+            eng.amplitude(0, o)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for o in outs[:n_single]:
+            eng.amplitude(0, o)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / n_single
+        single = {"value": round(1.0 / dt, 1), "unit": "amplitudes/s", "ms_per_call": round(dt * 1e3, 3),
+                  "calls": n_single,
+                  "api": "AmplitudeEngine.amplitude(0, bits) per bit-string, host wall time"}
+
     # ---- per-kernel profile (one extra, separately timed, eager step) ----
     with tc.KernelTimer() as kt:
         net = batched_net()
@@ -481,6 +499,7 @@ def run_gpu(args):
                     "api": "AmplitudeEngine.amplitudes(0, host bit-strings) -> host ndarray"},
             "roofline": roof, "kernels": kern, "ops": ops, "gpu_launches": int(launches),
             "clocks": clk, "cpu_baseline": cpu, "self_check": selfcheck,
+            "single_call": single,
         }
     barrier(world)
     return result
@@ -1053,7 +1072,7 @@ def _compact(r: dict) -> dict:
            "roofline": {k: r["roofline"].get(k) for k in ("bound", "kernel", "achieved", "peak",
                                                             "unit", "frac")},
            "gpu_launches": r.get("gpu_launches"), "self_check": r.get("self_check")}
-    for k in ("per_size", "executed_tflops", "units_completed_in_run"):
+    for k in ("per_size", "executed_tflops", "units_completed_in_run", "single_call"):
         if k in r:
             out[k] = r[k]
     e2e = r.get("e2e") or {}
