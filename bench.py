@@ -702,6 +702,24 @@ def gemm_engines_4096(torch, tc, _lib) -> dict:
         torch.cuda.synchronize()
         out[name] = round(8.0 * n ** 3 * 3 / a.elapsed_time(b) / 1e9, 1)
         out[name.replace("_tflops", "_kernel")] = _lib.last_kernel()
+    # the FP32 SIMT ceiling the FFMA kernel is measured against: cuBLAS SGEMM
+    # with TF32 off (a library GEMM as a yardstick, not part of the path)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        x = torch.randn(8192, 8192, device="cuda", generator=g)
+        y = torch.randn(8192, 8192, device="cuda", generator=g)
+        x @ y
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            x @ y
+        b.record()
+        torch.cuda.synchronize()
+        out["fp32_simt_sgemm_tflops"] = round(2.0 * 8192 ** 3 * 3 / a.elapsed_time(b) / 1e9, 1)
+        out["ffma_frac_of_fp32_simt"] = round(out["ffma_tflops"] / out["fp32_simt_sgemm_tflops"], 3)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
     return out
 
 
