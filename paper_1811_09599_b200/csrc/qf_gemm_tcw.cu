@@ -766,9 +766,13 @@ int gemm_tc3w(const GemmArgs &g, cudaStream_t s, int ck, int pair) {
   const bool use_pair = pair > 0 || (pair < 0 && tc3w_pair_ok(g));
   if (pair == 2) return tcw::launch_wide<64, true, 4>(g, s);   // A/B: 4-column drain pieces (8: +0.5%)
   if (use_pair) {
-    if (ck == 128) return tcw::launch_wide<128, true>(g, s);
-    if (ck == 32) return tcw::launch_wide<32, true>(g, s);
-    return tcw::launch_wide<64, true>(g, s);
+    const int st = ck == 128 ? tcw::launch_wide<128, true>(g, s)
+                   : ck == 32 ? tcw::launch_wide<32, true>(g, s)
+                              : tcw::launch_wide<64, true>(g, s);
+    // auto mode: a device that cannot co-schedule CTA pairs (cluster launch
+    // refused) still gets the single-CTA wide kernel
+    if (st == QF_OK || pair > 0) return st;
+    cudaGetLastError();
   }
   if (ck == 128) return tcw::launch_wide<128, false>(g, s);
   if (ck == 32) return tcw::launch_wide<32, false>(g, s);
