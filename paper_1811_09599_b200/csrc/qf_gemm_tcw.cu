@@ -698,10 +698,14 @@ static int launch_wide(const GemmArgs &g, cudaStream_t s) {
   const int64_t units = PAIR ? sm_count() / 2 : sm_count();
   const int64_t nunits = std::min<int64_t>(total, units);
   const int64_t grid = nunits * (PAIR ? 2 : 1);
-  // lockstep only where panels are long (K >= 2048) and shared by several waves
+  // lockstep where panels are long enough to drift apart (K >= 512; K = 256 measures the same)
   const int64_t nk = (g.K + KB - 1) / KB;
   const int64_t max_epochs = ((total + nunits - 1) / nunits * nk + EPOCH - 1) / EPOCH;
-  uint32_t *epochs = (nk >= 256 && nunits > 1) ? sync_slot(s, max_epochs) : nullptr;
+  static const int64_t sync_nk = [] {   // A/B knob: smallest k-block count that runs in lockstep
+    const char *e = getenv("QF_TC3W_SYNCNK");
+    return e ? (int64_t)atoll(e) : (int64_t)64;   // K >= 512: 2^20 x 1024 x 1024 297 -> 315 TFLOP/s
+  }();
+  uint32_t *epochs = (nk >= sync_nk && nunits > 1) ? sync_slot(s, max_epochs) : nullptr;
   // row tiles (pair: 256-row tiles) per raster group; QF_TC3W_GM for A/B runs
   static const uint32_t gm_env = [] {
     const char *e = getenv("QF_TC3W_GM");
